@@ -1,0 +1,152 @@
+/* aderdg_b200.h — C ABI of the B200-native fused ADER-DG Euler step.
+ *
+ * This library replaces the reference's *driver seam* for the fused,
+ * single-touch, optimistic time stepping of compressible Euler on a periodic
+ * Cartesian grid.  One call advances whole grid sweeps on the GPU; there is no
+ * per-cell or per-task call.  Each entry point names the reference interface
+ * it stands in for (paths relative to /root/reference/pkg/src/aderdg/):
+ *
+ *   adg_create            Driver.__init__ + build_grid + Kernels.__init__ +
+ *                         TimeControl.__init__      (scheduler.py:44-55,92-131;
+ *                         mesh.py:167-243; kernels.py:46-60)
+ *   adg_set_operators     make_basis(p) arrays consumed by Kernels.__init__
+ *                         (basis.py:91-122; kernels.py:53-60)
+ *   adg_load_state        filling grid.cells[i].Q   (tests/conftest.py:20-22)
+ *   adg_store_state       reading grid.cells[i].Q   (tests/conftest.py:77-79)
+ *   adg_seed              Driver._seed_time_control (scheduler.py:135-155)
+ *   adg_step              Driver.step, fused mode   (scheduler.py:190-208,
+ *                         370-449, incl. priming sweep and optimistic rerun)
+ *   adg_run               Driver.run(steps=N)       (scheduler.py:210-218)
+ *   adg_step_records      Driver.step_records       (scheduler.py:459-481)
+ *   adg_error_info /      exception classes NumericalError /
+ *   adg_last_error        PredictorFailureError(cell_index) (errors.py:28-39)
+ *
+ * Multi-GPU (x-slab decomposition, one process per GPU) uses the phase API
+ * (adg_phase_*) plus adg_buffer() so that the host can run the halo exchange
+ * and the lambda/error all-reduce with NCCL between phases.
+ *
+ * Conventions: all arrays are fp64, host pointers are borrowed for the
+ * duration of the call, device buffers/streams belong to the handle.  State
+ * layout = the reference's stack([c.Q for c in grid.cells]):
+ * [cell (C-order over the cell multi-index)][i_0..i_{d-1}][component].
+ * A handle is driven by one host thread.  Calls return an adg_status.
+ */
+#ifndef ADERDG_B200_H
+#define ADERDG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  ADG_OK = 0,
+  ADG_ERR_CONFIG = 2,      /* ConfigurationError / ResourceBudgetError  */
+  ADG_ERR_NUMERICAL = 3,   /* NumericalError                             */
+  ADG_ERR_RUNTIME = 4,     /* CUDA runtime failure                        */
+  ADG_ERR_PREDICTOR = 5    /* PredictorFailureError(cell_index)          */
+} adg_status;
+
+/* Numerical error kinds reported by adg_error_info (kind field). */
+typedef enum {
+  ADG_EK_NONE = 0,
+  ADG_EK_INIT_INADMISSIBLE = 1, /* "initial data inadmissible in cell {c}"   scheduler.py:146-148 */
+  ADG_EK_NO_INITIAL_STEP = 2,   /* "no admissible initial step (got {adm})"  scheduler.py:153-154 */
+  ADG_EK_INADMISSIBLE = 3,      /* "inadmissible state in cell {c} at step {s}" scheduler.py:429-432 */
+  ADG_EK_PREDICTOR = 4,         /* PredictorFailureError(c)                   kernels.py:80-100 */
+  ADG_EK_DEGENERATE = 5         /* "admissible step degenerated to {dt_adm}"  scheduler.py:81-82 */
+} adg_error_kind;
+
+typedef struct {
+  int d;                 /* 2 or 3                                         */
+  int p;                 /* polynomial order, 0..9                         */
+  int L;                 /* refinement depth: 3^L cells per axis, h = 3^-L */
+  double cfl;            /* Kernels(cfl=0.9)                               */
+  double c_dt;           /* TimeControl(c_dt=0.99)                         */
+  int creeping;          /* TimeControl(averaging="creeping") if nonzero   */
+  double forced_dt;      /* TimeControl(forced_dt=...); NaN = off          */
+  int inject_rerun;      /* Driver(inject_rerun=True)                      */
+  int spike_step;        /* Driver(spike_step=...); <0 = off               */
+  double spike_factor;   /* Driver(spike_factor=3.0)                       */
+  int device;            /* CUDA device ordinal                            */
+  int rank;              /* slab index (0 for a single GPU)                */
+  int world;             /* number of slabs along axis 0 (1 = periodic in place) */
+} adg_config;
+
+typedef struct {
+  int step;              /* realisation step (1-based)                     */
+  int reruns;            /* rerun passes booked on this step (0/1)         */
+  double T;
+  double dt_old;
+  double dt_new;
+  double dt_adm;
+  long long picard_iters;  /* Picard iterations summed over all predicts of the step */
+  long long predicts;      /* number of cell predictions in the step        */
+} adg_step_record;
+
+typedef struct adg_handle adg_handle;
+
+/* which buffer adg_buffer() returns */
+typedef enum {
+  ADG_BUF_Q = 0,         /* local state, [local cells][nodes][m]            */
+  ADG_BUF_D = 1,         /* volume/face update D_h                           */
+  ADG_BUF_TRACE0 = 2,    /* face-trace records, parity 0                     */
+  ADG_BUF_TRACE1 = 3,    /* face-trace records, parity 1                     */
+  ADG_BUF_REDUCE = 4     /* int64[2] = {lambda bits (max), INT64_MAX-err key (max)} */
+} adg_buffer_id;
+
+/* Layout queries for the halo exchange (multi-GPU). */
+typedef struct {
+  int n_cells_global;    /* 3^(d L)                                         */
+  int n_cells_local;     /* cells of this slab                              */
+  int cell_offset;       /* global index of the first local cell            */
+  int planes_local;      /* axis-0 planes of this slab                      */
+  int plane_cells;       /* 3^(L(d-1))                                      */
+  int record_doubles;    /* doubles per face-side record                     */
+  int faces_per_cell;    /* 2d                                               */
+  size_t state_doubles;  /* n_cells_local * (p+1)^d * m                      */
+} adg_layout;
+
+adg_status adg_create(const adg_config* cfg, adg_handle** out);
+void       adg_destroy(adg_handle* h);
+adg_status adg_set_operators(adg_handle* h, const double* nodes, const double* weights,
+                             const double* diff, const double* integ,
+                             const double* left, const double* right);
+adg_status adg_set_stream(adg_handle* h, void* cuda_stream);   /* cudaStream_t; NULL = handle's own */
+adg_status adg_load_state(adg_handle* h, const double* Q, size_t n_doubles);
+adg_status adg_store_state(adg_handle* h, double* Q, size_t n_doubles);
+adg_status adg_seed(adg_handle* h);
+adg_status adg_step(adg_handle* h, adg_step_record* out);
+adg_status adg_run(adg_handle* h, int steps, adg_step_record* out);
+adg_status adg_sync(adg_handle* h);
+int        adg_step_count(const adg_handle* h);
+int        adg_rerun_count(const adg_handle* h);
+int        adg_sweep_count(const adg_handle* h);
+adg_status adg_time_control(const adg_handle* h, double* T, double* dt_old,
+                            double* dt_new, double* dt_adm);
+adg_status adg_picard_histogram(const adg_handle* h, long long* hist, int n_bins);
+adg_status adg_error_info(const adg_handle* h, int* kind, long long* cell, int* step, double* value);
+const char* adg_last_error(const adg_handle* h);
+adg_status adg_layout_info(const adg_handle* h, adg_layout* out);
+adg_status adg_buffer(adg_handle* h, int which, void** dev_ptr, size_t* bytes);
+
+/* Phase API (one process per GPU; the host drives NCCL between phases).
+ * A realisation step is: rerun -> [halo exchange of the current parity] ->
+ * sweep -> [all-reduce ADG_BUF_REDUCE with MAX] -> finish.  The priming sweep
+ * (first step) is sweep(priming) -> [all-reduce] -> finish(priming). */
+adg_status adg_phase_seed(adg_handle* h);      /* seed pass: fills ADG_BUF_REDUCE   */
+adg_status adg_phase_seed_finish(adg_handle* h);
+adg_status adg_phase_rerun(adg_handle* h);     /* device-conditional rerun predict  */
+adg_status adg_phase_sweep(adg_handle* h);     /* priming on the first call          */
+adg_status adg_phase_finish(adg_handle* h);    /* time control + step record         */
+int        adg_trace_parity(const adg_handle* h); /* parity the next sweep reads      */
+
+/* Timing helpers for bench.py: launches on the handle's stream. */
+adg_status adg_flush_l2(adg_handle* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADERDG_B200_H */

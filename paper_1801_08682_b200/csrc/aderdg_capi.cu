@@ -1,0 +1,530 @@
+// aderdg_capi.cu — C ABI (include/aderdg_b200.h) over the sm_100a kernels.
+//
+// The handle owns every device buffer: Q and D per local cell, two parities
+// of face-trace records, the device-resident TimeControl (DevState) and the
+// step-record ring.  A realisation step is three stream-ordered launches
+// (rerun predict [device-conditional] -> fused sweep -> time control) with no
+// host synchronisation; adg_step syncs once at the end, adg_run only after
+// the last step.
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <string.h>
+#include <math.h>
+#include <string>
+#include <vector>
+
+#include "../../include/aderdg_b200.h"
+#include "aderdg_kernels.cuh"
+
+using namespace adg;
+
+namespace {
+
+typedef void (*launch_fn)(const SweepParams&, unsigned grid, cudaStream_t s);
+
+template <int DIM, int NQ>
+void launch_sweep(const SweepParams& P, unsigned grid, cudaStream_t s) {
+  using S = Shape<DIM, NQ>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sweep_kernel<DIM, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)S::SMEM_BYTES);
+    attr = true;
+  }
+  sweep_kernel<DIM, NQ><<<grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
+}
+
+template <int DIM, int NQ>
+int record_doubles() { return Shape<DIM, NQ>::REC; }
+
+struct Dispatch {
+  launch_fn sweep;
+  int rec;
+};
+
+template <int DIM, int NQ>
+Dispatch make_dispatch() { return Dispatch{&launch_sweep<DIM, NQ>, Shape<DIM, NQ>::REC}; }
+
+bool dispatch_for(int d, int p, Dispatch* out) {
+  const int n = p + 1;
+  if (d == 2) {
+    switch (n) {
+      case 1: *out = make_dispatch<2, 1>(); return true;
+      case 2: *out = make_dispatch<2, 2>(); return true;
+      case 3: *out = make_dispatch<2, 3>(); return true;
+      case 4: *out = make_dispatch<2, 4>(); return true;
+      case 5: *out = make_dispatch<2, 5>(); return true;
+      case 6: *out = make_dispatch<2, 6>(); return true;
+      case 7: *out = make_dispatch<2, 7>(); return true;
+      case 8: *out = make_dispatch<2, 8>(); return true;
+      case 9: *out = make_dispatch<2, 9>(); return true;
+      case 10: *out = make_dispatch<2, 10>(); return true;
+    }
+  } else if (d == 3) {
+    switch (n) {
+      case 1: *out = make_dispatch<3, 1>(); return true;
+      case 2: *out = make_dispatch<3, 2>(); return true;
+      case 3: *out = make_dispatch<3, 3>(); return true;
+      case 4: *out = make_dispatch<3, 4>(); return true;
+      case 5: *out = make_dispatch<3, 5>(); return true;
+      case 6: *out = make_dispatch<3, 6>(); return true;
+    }
+  }
+  return false;
+}
+
+}  // namespace
+
+struct adg_handle {
+  adg_config cfg;
+  int n = 0, m = 0, NS = 0, NF = 0, REC = 0, K = 0;
+  long long cells_global = 0, cells_local = 0;
+  int planes_local = 0, plane_cells = 0, plane0 = 0;
+  long long slots = 0;
+  double h = 0;
+  Ops ops;
+  bool ops_set = false;
+  Dispatch disp;
+  double* Q = nullptr;
+  double* D = nullptr;
+  double* tr[2] = {nullptr, nullptr};
+  DevState* st = nullptr;
+  StepRecord* recs = nullptr;
+  int rec_cap = 4096;
+  void* flush = nullptr;
+  size_t flush_bytes = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  int sweep_index = 0;       // index of the next regular sweep (0 = priming)
+  bool seeded = false;
+  bool loaded = false;
+  int host_steps = 0;        // steps whose records were fetched
+  DevState hst;              // host mirror after the last sync
+  std::string err;
+};
+
+static adg_status fail(adg_handle* h, adg_status code, const std::string& msg) {
+  if (h) h->err = msg;
+  return code;
+}
+
+static adg_status cuda_check(adg_handle* h, cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return ADG_OK;
+  char buf[512];
+  snprintf(buf, sizeof buf, "CUDA error in %s: %s", what, cudaGetErrorString(e));
+  return fail(h, ADG_ERR_RUNTIME, buf);
+}
+
+#define CUDA_TRY(h, expr)                                   \
+  do {                                                      \
+    adg_status _s = cuda_check((h), (expr), #expr);         \
+    if (_s != ADG_OK) return _s;                            \
+  } while (0)
+
+static SweepParams sweep_params(adg_handle* h, int mode) {
+  SweepParams P;
+  P.ops = h->ops;
+  P.Q = h->Q;
+  P.D = h->D;
+  const int par = h->sweep_index & 1;
+  // the sweep (and the rerun before it) read parity `par`; the sweep's own
+  // predictions go to the other parity, the rerun pass overwrites `par`.
+  if (mode == MODE_RERUN) {
+    P.tr_in = h->tr[par];
+    P.tr_out = h->tr[par];
+  } else {
+    P.tr_in = h->tr[par];
+    P.tr_out = h->tr[par ^ 1];
+  }
+  if (mode == MODE_PRIMING) P.tr_out = h->tr[1];
+  P.st = h->st;
+  P.slots = h->slots;
+  P.mode = mode;
+  P.K = h->K;
+  P.planes_local = h->planes_local;
+  P.plane_cells = h->plane_cells;
+  P.cell_offset = (int)(h->plane0 * (long long)h->plane_cells);
+  P.halo = h->cfg.world > 1 ? 1 : 0;
+  P.spike_step = h->cfg.spike_step;
+  P.p = h->cfg.p;
+  P.h = h->h;
+  P.cfl = h->cfg.cfl;
+  P.spike_factor = h->cfg.spike_factor;
+  return P;
+}
+
+static FinishParams finish_params(adg_handle* h, int priming, int seed) {
+  FinishParams F;
+  F.st = h->st;
+  F.recs = h->recs;
+  F.rec_cap = h->rec_cap;
+  F.priming = priming;
+  F.seed = seed;
+  F.d = h->cfg.d;
+  F.p = h->cfg.p;
+  F.h = h->h;
+  F.cfl = h->cfg.cfl;
+  F.c_dt = h->cfg.c_dt;
+  F.forced_dt = h->cfg.forced_dt;
+  F.creeping = h->cfg.creeping;
+  F.inject_rerun = h->cfg.inject_rerun;
+  return F;
+}
+
+static adg_status launch(adg_handle* h, int mode) {
+  SweepParams P = sweep_params(h, mode);
+  h->disp.sweep(P, (unsigned)h->cells_local, h->stream);
+  return cuda_check(h, cudaGetLastError(), "sweep launch");
+}
+
+static adg_status launch_finish(adg_handle* h, int priming, int seed) {
+  FinishParams F = finish_params(h, priming, seed);
+  finish_kernel<<<1, 1, 0, h->stream>>>(F);
+  return cuda_check(h, cudaGetLastError(), "finish launch");
+}
+
+static adg_status pull_state(adg_handle* h) {
+  CUDA_TRY(h, cudaMemcpyAsync(&h->hst, h->st, sizeof(DevState), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  return ADG_OK;
+}
+
+static adg_status status_from_state(adg_handle* h) {
+  const DevState& s = h->hst;
+  char buf[512];
+  switch (s.status) {
+    case 0: return ADG_OK;
+    case ADG_EK_INIT_INADMISSIBLE:
+      snprintf(buf, sizeof buf, "initial data inadmissible in cell %lld", s.err_cell);
+      return fail(h, ADG_ERR_NUMERICAL, buf);
+    case ADG_EK_NO_INITIAL_STEP:
+      snprintf(buf, sizeof buf, "no admissible initial step (got %.17g)", s.err_value);
+      return fail(h, ADG_ERR_NUMERICAL, buf);
+    case ADG_EK_INADMISSIBLE:
+      snprintf(buf, sizeof buf, "inadmissible state in cell %lld at step %d", s.err_cell, s.err_step);
+      return fail(h, ADG_ERR_NUMERICAL, buf);
+    case ADG_EK_PREDICTOR:
+      snprintf(buf, sizeof buf, "predictor produced non-finite values (cell %lld)", s.err_cell);
+      return fail(h, ADG_ERR_PREDICTOR, buf);
+    case ADG_EK_DEGENERATE:
+      snprintf(buf, sizeof buf, "admissible step degenerated to %.17g", s.err_value);
+      return fail(h, ADG_ERR_NUMERICAL, buf);
+  }
+  return fail(h, ADG_ERR_RUNTIME, "unknown device status");
+}
+
+extern "C" {
+
+adg_status adg_create(const adg_config* cfg, adg_handle** out) {
+  if (!cfg || !out) return ADG_ERR_CONFIG;
+  *out = nullptr;
+  adg_handle* h = new adg_handle();
+  h->cfg = *cfg;
+  const adg_config& c = *cfg;
+  char buf[256];
+  if (c.d != 2 && c.d != 3) { snprintf(buf, sizeof buf, "dimension must be 2 or 3, got %d", c.d); h->err = buf; *out = h; return ADG_ERR_CONFIG; }
+  if (c.L < 1 || c.L > 4) { snprintf(buf, sizeof buf, "depth L must be in [1, 4], got %d", c.L); h->err = buf; *out = h; return ADG_ERR_CONFIG; }
+  if (c.p < 0 || c.p > 9) { snprintf(buf, sizeof buf, "order p must be in [0, 9], got %d", c.p); h->err = buf; *out = h; return ADG_ERR_CONFIG; }
+  if (!(c.c_dt > 0.0 && c.c_dt <= 1.0)) { snprintf(buf, sizeof buf, "c_dt must be in (0, 1], got %g", c.c_dt); h->err = buf; *out = h; return ADG_ERR_CONFIG; }
+  if (!dispatch_for(c.d, c.p, &h->disp)) {
+    snprintf(buf, sizeof buf, "no sm_100a kernel instantiated for d=%d p=%d", c.d, c.p);
+    h->err = buf; *out = h; return ADG_ERR_CONFIG;
+  }
+  h->n = c.p + 1;
+  h->m = c.d + 2;
+  h->NS = 1; for (int a = 0; a < c.d; ++a) h->NS *= h->n;
+  h->NF = h->NS / h->n;
+  h->REC = h->disp.rec;
+  h->K = 1; for (int l = 0; l < c.L; ++l) h->K *= 3;
+  h->h = pow(3.0, -(double)c.L);   // mesh.py:71  3.0 ** (-L)
+  h->plane_cells = 1; for (int a = 1; a < c.d; ++a) h->plane_cells *= h->K;
+  h->cells_global = (long long)h->K * h->plane_cells;
+  const int world = c.world < 1 ? 1 : c.world;
+  h->cfg.world = world;
+  if (c.rank < 0 || c.rank >= world || world > h->K) { h->err = "bad rank/world for the slab decomposition"; *out = h; return ADG_ERR_CONFIG; }
+  // x-slabs of whole cell planes: the first K % world slabs get one extra plane
+  const int base = h->K / world, extra = h->K % world;
+  h->planes_local = base + (c.rank < extra ? 1 : 0);
+  h->plane0 = c.rank * base + (c.rank < extra ? c.rank : extra);
+  h->cells_local = (long long)h->planes_local * h->plane_cells;
+  h->slots = (long long)(h->planes_local + 2) * h->plane_cells;
+  *out = h;
+
+  CUDA_TRY(h, cudaSetDevice(c.device));
+  CUDA_TRY(h, cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
+  h->stream = h->own_stream;
+  const size_t state_bytes = sizeof(double) * (size_t)h->cells_local * h->NS * h->m;
+  const size_t tr_bytes = sizeof(double) * (size_t)(2 * c.d) * h->slots * h->REC;
+  CUDA_TRY(h, cudaMalloc(&h->Q, state_bytes));
+  CUDA_TRY(h, cudaMalloc(&h->D, state_bytes));
+  CUDA_TRY(h, cudaMalloc(&h->tr[0], tr_bytes));
+  CUDA_TRY(h, cudaMalloc(&h->tr[1], tr_bytes));
+  CUDA_TRY(h, cudaMalloc(&h->st, sizeof(DevState)));
+  CUDA_TRY(h, cudaMalloc(&h->recs, sizeof(StepRecord) * h->rec_cap));
+  CUDA_TRY(h, cudaMemsetAsync(h->D, 0, state_bytes, h->stream));        // mesh.py:238-239
+  CUDA_TRY(h, cudaMemsetAsync(h->tr[0], 0, tr_bytes, h->stream));
+  CUDA_TRY(h, cudaMemsetAsync(h->tr[1], 0, tr_bytes, h->stream));
+  DevState s0;
+  memset(&s0, 0, sizeof s0);
+  s0.dt_adm = INFINITY;                                                // TimeControl.__init__
+  CUDA_TRY(h, cudaMemcpyAsync(h->st, &s0, sizeof s0, cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  h->hst = s0;
+  return ADG_OK;
+}
+
+void adg_destroy(adg_handle* h) {
+  if (!h) return;
+  if (h->Q) cudaFree(h->Q);
+  if (h->D) cudaFree(h->D);
+  if (h->tr[0]) cudaFree(h->tr[0]);
+  if (h->tr[1]) cudaFree(h->tr[1]);
+  if (h->st) cudaFree(h->st);
+  if (h->recs) cudaFree(h->recs);
+  if (h->flush) cudaFree(h->flush);
+  if (h->own_stream) cudaStreamDestroy(h->own_stream);
+  delete h;
+}
+
+adg_status adg_set_operators(adg_handle* h, const double* nodes, const double* weights,
+                             const double* diff, const double* integ,
+                             const double* left, const double* right) {
+  if (!h || !weights || !diff || !integ || !left || !right) return ADG_ERR_CONFIG;
+  (void)nodes;
+  const int n = h->n;
+  memset(&h->ops, 0, sizeof h->ops);
+  for (int i = 0; i < n; ++i) {
+    h->ops.w[i] = weights[i];
+    h->ops.left[i] = left[i];
+    h->ops.right[i] = right[i];
+    h->ops.lift_lo[i] = left[i] / weights[i];     // kernels.py:58
+    h->ops.lift_hi[i] = right[i] / weights[i];    // kernels.py:59
+    for (int j = 0; j < n; ++j) {
+      h->ops.diff[i][j] = diff[i * n + j];
+      h->ops.integ[i][j] = integ[i * n + j];
+      // kvol[i, j] = diff[j, i] * w[j] / w[i]     kernels.py:56
+      h->ops.kvol[i][j] = (diff[j * n + i] * weights[j]) / weights[i];
+    }
+  }
+  h->ops_set = true;
+  return ADG_OK;
+}
+
+adg_status adg_set_stream(adg_handle* h, void* s) {
+  if (!h) return ADG_ERR_CONFIG;
+  h->stream = s ? (cudaStream_t)s : h->own_stream;
+  return ADG_OK;
+}
+
+adg_status adg_load_state(adg_handle* h, const double* Q, size_t n) {
+  if (!h || !Q) return ADG_ERR_CONFIG;
+  const size_t want = (size_t)h->cells_local * h->NS * h->m;
+  if (n != want) return fail(h, ADG_ERR_CONFIG, "state size mismatch");
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  CUDA_TRY(h, cudaMemcpyAsync(h->Q, Q, n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  h->loaded = true;
+  return ADG_OK;
+}
+
+adg_status adg_store_state(adg_handle* h, double* Q, size_t n) {
+  if (!h || !Q) return ADG_ERR_CONFIG;
+  const size_t want = (size_t)h->cells_local * h->NS * h->m;
+  if (n != want) return fail(h, ADG_ERR_CONFIG, "state size mismatch");
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  CUDA_TRY(h, cudaMemcpyAsync(Q, h->Q, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  return ADG_OK;
+}
+
+adg_status adg_phase_seed(adg_handle* h) {
+  if (!h) return ADG_ERR_CONFIG;
+  if (!h->ops_set) return fail(h, ADG_ERR_CONFIG, "operators not set");
+  if (!h->loaded) return fail(h, ADG_ERR_CONFIG, "state not loaded");
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  return launch(h, MODE_SEED);
+}
+
+adg_status adg_phase_seed_finish(adg_handle* h) {
+  if (!h) return ADG_ERR_CONFIG;
+  adg_status s = launch_finish(h, 0, 1);
+  if (s == ADG_OK) h->seeded = true;
+  return s;
+}
+
+adg_status adg_seed(adg_handle* h) {
+  adg_status s = adg_phase_seed(h);
+  if (s != ADG_OK) return s;
+  s = adg_phase_seed_finish(h);
+  if (s != ADG_OK) return s;
+  s = pull_state(h);
+  if (s != ADG_OK) return s;
+  return status_from_state(h);
+}
+
+adg_status adg_phase_rerun(adg_handle* h) {
+  if (!h) return ADG_ERR_CONFIG;
+  if (h->sweep_index == 0) return ADG_OK;       // nothing predicted yet
+  return launch(h, MODE_RERUN);
+}
+
+adg_status adg_phase_sweep(adg_handle* h) {
+  if (!h) return ADG_ERR_CONFIG;
+  if (!h->seeded) return fail(h, ADG_ERR_CONFIG, "time control not seeded");
+  adg_status s = launch(h, h->sweep_index == 0 ? MODE_PRIMING : MODE_NORMAL);
+  return s;
+}
+
+adg_status adg_phase_finish(adg_handle* h) {
+  if (!h) return ADG_ERR_CONFIG;
+  adg_status s = launch_finish(h, h->sweep_index == 0 ? 1 : 0, 0);
+  h->sweep_index += 1;
+  return s;
+}
+
+int adg_trace_parity(const adg_handle* h) { return h ? (h->sweep_index & 1) : 0; }
+
+static adg_status enqueue_step(adg_handle* h) {
+  adg_status s;
+  if (h->sweep_index == 0) {                    // Driver.step: priming sweep first
+    if ((s = adg_phase_sweep(h)) != ADG_OK) return s;
+    if ((s = adg_phase_finish(h)) != ADG_OK) return s;
+  }
+  if ((s = adg_phase_rerun(h)) != ADG_OK) return s;
+  if ((s = adg_phase_sweep(h)) != ADG_OK) return s;
+  return adg_phase_finish(h);
+}
+
+static adg_status fetch_records(adg_handle* h, int from_step, int to_step, adg_step_record* out) {
+  // records of steps (from_step, to_step] into out[0..]
+  for (int s = from_step + 1; s <= to_step; ++s) {
+    StepRecord r;
+    CUDA_TRY(h, cudaMemcpyAsync(&r, h->recs + ((s - 1) % h->rec_cap), sizeof r,
+                                cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    adg_step_record& o = out[s - from_step - 1];
+    o.step = r.step; o.reruns = r.reruns; o.T = r.T; o.dt_old = r.dt_old;
+    o.dt_new = r.dt_new; o.dt_adm = r.dt_adm; o.picard_iters = r.picard_iters; o.predicts = r.predicts;
+  }
+  return ADG_OK;
+}
+
+adg_status adg_step(adg_handle* h, adg_step_record* out) {
+  if (!h) return ADG_ERR_CONFIG;
+  if (h->hst.status) return status_from_state(h);
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  const int before = h->hst.step;
+  adg_status s = enqueue_step(h);
+  if (s != ADG_OK) return s;
+  if ((s = pull_state(h)) != ADG_OK) return s;
+  if ((s = status_from_state(h)) != ADG_OK) return s;
+  if (out && h->hst.step > before) return fetch_records(h, before, h->hst.step, out);
+  return ADG_OK;
+}
+
+adg_status adg_run(adg_handle* h, int steps, adg_step_record* out) {
+  if (!h) return ADG_ERR_CONFIG;
+  if (h->hst.status) return status_from_state(h);
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  int done = 0;
+  while (done < steps) {
+    const int chunk = (steps - done) < h->rec_cap ? (steps - done) : h->rec_cap;
+    const int before = h->hst.step;
+    for (int i = 0; i < chunk; ++i) {
+      adg_status s = enqueue_step(h);
+      if (s != ADG_OK) return s;
+    }
+    adg_status s = pull_state(h);
+    if (s != ADG_OK) return s;
+    if (out && h->hst.step > before) {
+      s = fetch_records(h, before, h->hst.step, out + done);
+      if (s != ADG_OK) return s;
+    }
+    if ((s = status_from_state(h)) != ADG_OK) return s;
+    done += chunk;
+  }
+  return ADG_OK;
+}
+
+adg_status adg_sync(adg_handle* h) {
+  if (!h) return ADG_ERR_CONFIG;
+  adg_status s = pull_state(h);
+  if (s != ADG_OK) return s;
+  return status_from_state(h);
+}
+
+int adg_step_count(const adg_handle* h) { return h ? h->hst.step : 0; }
+int adg_rerun_count(const adg_handle* h) {
+  // reruns already executed (a rerun decided for the coming step is not booked yet)
+  return h ? h->hst.reruns_total - h->hst.rerun_next : 0;
+}
+int adg_sweep_count(const adg_handle* h) {
+  // priming + one regular sweep per step + rerun passes (Driver.sweep_count)
+  if (!h || h->hst.step == 0) return 0;
+  return 1 + h->hst.step + h->hst.reruns_total - (h->hst.rerun_next ? 1 : 0);
+}
+
+adg_status adg_time_control(const adg_handle* h, double* T, double* dt_old, double* dt_new, double* dt_adm) {
+  if (!h) return ADG_ERR_CONFIG;
+  if (T) *T = h->hst.T;
+  if (dt_old) *dt_old = h->hst.dt_old;
+  if (dt_new) *dt_new = h->hst.dt_new;
+  if (dt_adm) *dt_adm = h->hst.dt_adm;
+  return ADG_OK;
+}
+
+adg_status adg_picard_histogram(const adg_handle* h, long long* hist, int n_bins) {
+  if (!h || !hist) return ADG_ERR_CONFIG;
+  for (int i = 0; i < n_bins && i < HIST_BINS; ++i) hist[i] = h->hst.hist[i];
+  return ADG_OK;
+}
+
+adg_status adg_error_info(const adg_handle* h, int* kind, long long* cell, int* step, double* value) {
+  if (!h) return ADG_ERR_CONFIG;
+  if (kind) *kind = h->hst.status;
+  if (cell) *cell = h->hst.err_cell;
+  if (step) *step = h->hst.err_step;
+  if (value) *value = h->hst.err_value;
+  return ADG_OK;
+}
+
+const char* adg_last_error(const adg_handle* h) { return h ? h->err.c_str() : "null handle"; }
+
+adg_status adg_layout_info(const adg_handle* h, adg_layout* o) {
+  if (!h || !o) return ADG_ERR_CONFIG;
+  o->n_cells_global = (int)h->cells_global;
+  o->n_cells_local = (int)h->cells_local;
+  o->cell_offset = (int)(h->plane0 * (long long)h->plane_cells);
+  o->planes_local = h->planes_local;
+  o->plane_cells = h->plane_cells;
+  o->record_doubles = h->REC;
+  o->faces_per_cell = 2 * h->cfg.d;
+  o->state_doubles = (size_t)h->cells_local * h->NS * h->m;
+  return ADG_OK;
+}
+
+adg_status adg_buffer(adg_handle* h, int which, void** ptr, size_t* bytes) {
+  if (!h || !ptr || !bytes) return ADG_ERR_CONFIG;
+  const size_t state_bytes = sizeof(double) * (size_t)h->cells_local * h->NS * h->m;
+  const size_t tr_bytes = sizeof(double) * (size_t)(2 * h->cfg.d) * h->slots * h->REC;
+  switch (which) {
+    case ADG_BUF_Q: *ptr = h->Q; *bytes = state_bytes; return ADG_OK;
+    case ADG_BUF_D: *ptr = h->D; *bytes = state_bytes; return ADG_OK;
+    case ADG_BUF_TRACE0: *ptr = h->tr[0]; *bytes = tr_bytes; return ADG_OK;
+    case ADG_BUF_TRACE1: *ptr = h->tr[1]; *bytes = tr_bytes; return ADG_OK;
+    case ADG_BUF_REDUCE: *ptr = h->st; *bytes = 2 * sizeof(long long); return ADG_OK;
+  }
+  return ADG_ERR_CONFIG;
+}
+
+adg_status adg_flush_l2(adg_handle* h) {
+  if (!h) return ADG_ERR_CONFIG;
+  if (!h->flush) {
+    h->flush_bytes = (size_t)256 << 20;
+    CUDA_TRY(h, cudaMalloc(&h->flush, h->flush_bytes));
+  }
+  CUDA_TRY(h, cudaMemsetAsync(h->flush, h->sweep_index & 0xff, h->flush_bytes, h->stream));
+  return ADG_OK;
+}
+
+}  // extern "C"

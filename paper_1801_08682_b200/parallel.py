@@ -1,0 +1,167 @@
+"""x-slab domain decomposition across GPUs (one process per GPU, NCCL).
+
+The paper's distributed scheme (``PAPER.md:1585-1625``; not implemented by the
+reference, ``SPEC.md:8,424``): non-overlapping subdomains of whole cell planes
+along axis 0, face projections of the slab-boundary cells exchanged with the
+two ring neighbours once per realisation step, boundary Riemann problems
+solved redundantly on both sides, and one global reduction of the admissible
+step (here: max of lambda, which gives dt_adm bitwise).
+
+Per step and rank:  rerun (device-conditional)  ->  halo exchange of the
+trace parity the sweep will read  ->  fused sweep  ->  all-reduce MAX of
+{lambda bits, INT64_MAX - error key}  ->  time control.
+
+Layout of the trace records (``include/aderdg_b200.h``): ``[2d faces][slots][REC]``
+with ``slots = (planes_local + 2) * plane_cells``; slot plane 0 and
+``planes_local + 1`` are the halos.  Face 0 = low-x side record of a cell,
+face 1 = high-x side record, so every message is one contiguous slice.
+"""
+
+import numpy as np
+
+from . import _lib
+from .errors import ConfigurationError
+
+
+def slab_partition(K, world, rank):
+    """Planes of rank's slab: the first K % world ranks get one extra plane
+    (mirrors adg_create in csrc/aderdg_capi.cu)."""
+    if world < 1 or not 0 <= rank < world or world > K:
+        raise ConfigurationError(f"bad slab decomposition: K={K} world={world} rank={rank}")
+    base, extra = divmod(K, world)
+    planes = base + (1 if rank < extra else 0)
+    plane0 = rank * base + min(rank, extra)
+    return plane0, planes
+
+
+class HaloExchange:
+    """Ring exchange of slab-boundary face records and the step reduction.
+
+    Works on any torch tensors (CUDA with NCCL, CPU with gloo for tests)."""
+
+    def __init__(self, planes_local, plane_cells, rank, world, group=None):
+        self.Pl, self.plane = planes_local, plane_cells
+        self.rank, self.world, self.group = rank, world, group
+        self.prev = (rank - 1) % world
+        self.next = (rank + 1) % world
+
+    def views(self, tr):
+        """tr: tensor (2d, slots, REC).  Returns (send_to_prev, recv_from_prev,
+        send_to_next, recv_from_next)."""
+        P, n = self.Pl, self.plane
+        send_prev = tr[0, n:2 * n]                    # low-x records of my first plane
+        recv_next = tr[0, (P + 1) * n:(P + 2) * n]    # -> halo-hi: next rank's first-plane low-x
+        send_next = tr[1, P * n:(P + 1) * n]          # high-x records of my last plane
+        recv_prev = tr[1, 0:n]                        # -> halo-lo: prev rank's last-plane high-x
+        return send_prev, recv_prev, send_next, recv_next
+
+    def exchange(self, tr):
+        import torch.distributed as dist
+        if self.world == 1:
+            return
+        send_prev, recv_prev, send_next, recv_next = self.views(tr)
+        # order matters when prev == next (world 2): messages between one pair
+        # are matched in issue order, so every rank sends "to next" first.
+        ops = [dist.P2POp(dist.isend, send_next, self.next, self.group),
+               dist.P2POp(dist.irecv, recv_prev, self.prev, self.group),
+               dist.P2POp(dist.isend, send_prev, self.prev, self.group),
+               dist.P2POp(dist.irecv, recv_next, self.next, self.group)]
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+
+    def reduce(self, red):
+        """red: int64[2] = {lambda bits, INT64_MAX - error key}; MAX over ranks."""
+        import torch.distributed as dist
+        if self.world == 1:
+            return
+        dist.all_reduce(red, op=dist.ReduceOp.MAX, group=self.group)
+
+
+class SlabDriver:
+    """Fused driver over an x-slab of the periodic grid on this process's GPU.
+
+    ``Q_global`` (reference layout) is sliced to the local cells; results are
+    gathered on demand with ``local_state()``.  All ranks must call every
+    method collectively.
+    """
+
+    def __init__(self, Q_global, d, L, p, rank, world, device, cfl=0.9, c_dt=0.99,
+                 averaging="strict", forced_dt=None, inject_rerun=False,
+                 spike_step=None, spike_factor=3.0, group=None):
+        import torch
+        from .basis import make_basis
+        from .solver import upload_operators
+        self.torch = torch
+        self.d, self.L, self.p = d, L, p
+        self.rank, self.world = rank, world
+        self.dev = torch.device("cuda", device)
+        cfg = _lib.AdgConfig()
+        cfg.d, cfg.p, cfg.L = d, p, L
+        cfg.cfl, cfg.c_dt = float(cfl), float(c_dt)
+        cfg.creeping = 1 if averaging == "creeping" else 0
+        cfg.forced_dt = float("nan") if forced_dt is None else float(forced_dt)
+        cfg.inject_rerun = 1 if inject_rerun else 0
+        cfg.spike_step = -1 if spike_step is None else int(spike_step)
+        cfg.spike_factor = float(spike_factor)
+        cfg.device, cfg.rank, cfg.world = int(device), int(rank), int(world)
+        self.handle = _lib.Handle(cfg)
+        self._ops = upload_operators(self.handle, make_basis(p))
+        self.lay = lay = self.handle.layout()
+        self.stream = torch.cuda.current_stream(self.dev)
+        self.handle.call("adg_set_stream", self.stream.cuda_stream)
+        K = 3 ** L
+        plane0, planes = slab_partition(K, world, rank)
+        assert planes == lay.planes_local and plane0 * lay.plane_cells == lay.cell_offset
+        self.cell_offset, self.n_local = lay.cell_offset, lay.n_cells_local
+        Ql = np.ascontiguousarray(Q_global[self.cell_offset:self.cell_offset + self.n_local],
+                                  dtype=np.float64)
+        self.handle.call("adg_load_state", _lib.dptr(Ql), Ql.size)
+        self.halo = HaloExchange(lay.planes_local, lay.plane_cells, rank, world, group)
+        slots = (lay.planes_local + 2) * lay.plane_cells
+        shape = (lay.faces_per_cell, slots, lay.record_doubles)
+        self.tr = []
+        for which in (_lib.ADG_BUF_TRACE0, _lib.ADG_BUF_TRACE1):
+            ptr, nbytes = self.handle.buffer(which)
+            assert nbytes == 8 * int(np.prod(shape))
+            self.tr.append(torch.as_tensor(_lib.DeviceArray(ptr, shape, "<f8", self.dev), device=self.dev))
+        rptr, _ = self.handle.buffer(_lib.ADG_BUF_REDUCE)
+        self.red = torch.as_tensor(_lib.DeviceArray(rptr, (2,), "<i8", self.dev), device=self.dev)
+        self.primed = False
+        # seed (Driver._seed_time_control) with the global reduction
+        self.handle.call("adg_phase_seed")
+        self.halo.reduce(self.red)
+        self.handle.call("adg_phase_seed_finish")
+        self.handle.call("adg_sync")
+
+    def enqueue_step(self):
+        """Queue one realisation step without host synchronisation."""
+        h = self.handle
+        if not self.primed:
+            h.call("adg_phase_sweep")          # priming sweep (no traces read)
+            self.halo.reduce(self.red)
+            h.call("adg_phase_finish")
+            self.primed = True
+        h.call("adg_phase_rerun")
+        self.halo.exchange(self.tr[h.lib.adg_trace_parity(h.h)])
+        h.call("adg_phase_sweep")
+        self.halo.reduce(self.red)
+        h.call("adg_phase_finish")
+
+    def run(self, steps):
+        for _ in range(steps):
+            self.enqueue_step()
+        self.handle.call("adg_sync")
+        return self.handle.lib.adg_step_count(self.handle.h)
+
+    def local_state(self):
+        lay = self.lay
+        Q = np.empty(lay.state_doubles)
+        self.handle.call("adg_store_state", _lib.dptr(Q), Q.size)
+        n = self.p + 1
+        return Q.reshape((lay.n_cells_local,) + (n,) * self.d + (self.d + 2,))
+
+    def time_control(self):
+        return self.handle.time_control()
+
+    def close(self):
+        self.handle.close()

@@ -1,0 +1,364 @@
+"""Drop-in host surface of the fused ADER-DG driver (reference driver seam).
+
+Mirrors the reference's library use (``pkg/README.md:85-98``,
+``tests/conftest.py:42-79``)::
+
+    basis = make_basis(p)
+    grid = build_grid(d, L, p, system.m)
+    init: grid.cells[i].Q[...] = ...          (or grid.Q[...] = array)
+    kernels = Kernels(EulerSystem(d), basis, grid, None, cfl=0.9)
+    driver = Driver(grid, kernels, TimeControl(c_dt=0.99), "fused")
+    driver.run(steps=N)
+    Q = gather(grid); driver.step_records
+
+Every realisation step runs on the GPU through the C ABI
+(``include/aderdg_b200.h``): one call per step (``adg_step``) or per run
+(``adg_run``).  The per-cell task methods of the reference ``Kernels`` class are
+not re-exposed: the GPU replaces the whole driver seam, and
+the PDE callbacks are compiled into the kernels (Euler, d = 2, 3).
+
+Reference citations (``src/`` = ``/root/reference/pkg/src/aderdg/``):
+  build_grid / Grid / Cell   src/mesh.py:27-243
+  EulerSystem                src/pde.py:16-67
+  Kernels (config)           src/kernels.py:37-60
+  TimeControl                src/scheduler.py:35-74
+  Driver (fused)             src/scheduler.py:88-226, 370-481
+"""
+
+import math
+from collections import Counter
+
+import numpy as np
+
+from . import _lib
+from .basis import make_basis
+from .errors import ConfigurationError, ResourceBudgetError
+
+DEFAULT_CFL = 0.9                 # src/kernels.py:21
+DEFAULT_C_DT = 0.99               # src/scheduler.py:32
+DEFAULT_BUDGET_BYTES = None       # the reference's 2 GiB guard targets host RAM; HBM is 180 GB
+GAMMA = 1.4
+
+
+class EulerSystem:
+    """Compressible Euler in d = 2, 3 (src/pde.py:16-67).  The flux,
+    signal-speed and admissibility callbacks are compiled into the sm_100a
+    kernels; this object selects the instantiation and offers the same
+    pointwise functions on host arrays for setup and checks."""
+
+    def __init__(self, dim):
+        if dim not in (2, 3):
+            from .errors import DomainError
+            raise DomainError(f"Euler system supports d in {{2, 3}}, got {dim}")
+        self.d = dim
+        self.m = dim + 2
+        self.name = "euler"
+
+    def pressure(self, Q):
+        Q = np.asarray(Q, dtype=float)
+        j = Q[..., 1:1 + self.d]
+        return (GAMMA - 1.0) * (Q[..., -1] - 0.5 * np.sum(j * j, axis=-1) / Q[..., 0])
+
+    def max_signal_speed(self, Q, axis):
+        Q = np.asarray(Q, dtype=float)
+        rho = Q[..., 0]
+        return np.abs(Q[..., 1 + axis] / rho) + np.sqrt(GAMMA * self.pressure(Q) / rho)
+
+    def is_admissible(self, Q):
+        Q = np.asarray(Q, dtype=float)
+        if not np.all(np.isfinite(Q)):
+            return False
+        if not np.all(Q[..., 0] > 1e-12):
+            return False
+        return bool(np.all(self.pressure(Q) > 1e-12))
+
+
+class Cell:
+    """Reference Cell view (src/mesh.py:27-40): ``Q`` is a view into the
+    grid's contiguous state array."""
+
+    __slots__ = ("index", "multi_index", "Q")
+
+    def __init__(self, index, multi_index, Q):
+        self.index = index
+        self.multi_index = multi_index
+        self.Q = Q
+
+
+class _CellList:
+    """Lazily materialised ``grid.cells`` (531441 cells at 81^3)."""
+
+    def __init__(self, grid):
+        self._g = grid
+
+    def __len__(self):
+        return self._g.n_cells
+
+    def __getitem__(self, i):
+        g = self._g
+        if isinstance(i, slice):
+            return [self[k] for k in range(*i.indices(len(self)))]
+        i = int(i)
+        if i < 0:
+            i += g.n_cells
+        if not 0 <= i < g.n_cells:
+            raise IndexError(i)
+        multi = tuple(int(v) for v in np.unravel_index(i, (g.cells_per_axis,) * g.d))
+        return Cell(i, multi, g.Q[i])
+
+    def __iter__(self):
+        for i in range(len(self)):
+            yield self[i]
+
+
+class Grid:
+    """Periodic 3^L-per-axis Cartesian grid on the unit cube (src/mesh.py:63-146).
+
+    ``Q`` holds every cell's coefficients in reference order
+    ``(n_cells,) + (p+1,)*d + (m,)``; ``cells[i].Q`` views into it."""
+
+    def __init__(self, d, L, p, m, boundary="periodic"):
+        self.d, self.L, self.p, self.m = d, L, p, m
+        self.boundary = boundary
+        self.storage = "hull"
+        self.h = 3.0 ** (-L)                       # src/mesh.py:71
+        n = p + 1
+        self.Q = np.zeros((3 ** (d * L),) + (n,) * d + (m,))
+        self.cells = _CellList(self)
+
+    @property
+    def n_cells(self):
+        return 3 ** (self.d * self.L)
+
+    @property
+    def cells_per_axis(self):
+        return 3 ** self.L
+
+    def node_block_shape(self):
+        return (self.p + 1,) * self.d + (self.m,)
+
+
+def device_bytes(d, L, p):
+    """Persistent HBM of one single-GPU solver: Q, D and two parities of
+    time-collapsed face records (2d per cell, 2 n^(d-1) m + 2 doubles each)."""
+    n, m, cells = p + 1, d + 2, 3 ** (d * L)
+    rec = 2 * n ** (d - 1) * m + 2
+    slots = (3 ** L + 2) * 3 ** (L * (d - 1))
+    return 8 * (2 * cells * n ** d * m + 2 * 2 * d * slots * rec)
+
+
+def build_grid(d, L, p, m, boundary="periodic", storage="hull",
+               budget_bytes=DEFAULT_BUDGET_BYTES):
+    """src/mesh.py:167-243 (periodic, hull storage)."""
+    if d not in (2, 3):
+        raise ConfigurationError(f"dimension must be 2 or 3, got {d}")
+    if not 1 <= L <= 4:
+        raise ConfigurationError(f"depth L must be in [1, 4], got {L}")
+    if not 0 <= p <= 9:
+        raise ConfigurationError(f"order p must be in [0, 9], got {p}")
+    if boundary not in ("periodic", "outflow"):
+        raise ConfigurationError(f"unknown boundary kind {boundary!r}")
+    if boundary != "periodic":
+        raise ConfigurationError("the GPU path implements periodic boundaries only")
+    if storage not in ("hull", "spacetime"):
+        raise ConfigurationError(f"unknown storage layout {storage!r}")
+    if m != d + 2:
+        raise ConfigurationError(f"the GPU path implements Euler (m = d+2), got m={m}")
+    if budget_bytes is not None:
+        req = device_bytes(d, L, p)
+        if req > budget_bytes:
+            raise ResourceBudgetError(req, budget_bytes)
+    return Grid(d, L, p, m, boundary)
+
+
+class Kernels:
+    """Configuration carrier of the reference kernel suite (src/kernels.py:46-60)."""
+
+    def __init__(self, system, basis, grid, ledger=None, cfl=DEFAULT_CFL):
+        if getattr(system, "name", None) != "euler":
+            raise ConfigurationError("the GPU kernels are instantiated for the Euler system only")
+        if system.d != grid.d or basis.p != grid.p:
+            raise ConfigurationError("system / basis / grid disagree on d or p")
+        self.system, self.basis, self.grid = system, basis, grid
+        self.ledger = ledger
+        self.cfl = cfl
+        w = basis.weights
+        self.kvol = (basis.diff.T * w[None, :]) / w[:, None]
+        self.lift_low = basis.left / w
+        self.lift_high = basis.right / w
+        self.picard_cap = max(1, 2 * basis.n)
+
+
+class TimeControl:
+    """src/scheduler.py:35-74; mirrors the device time control after each sync."""
+
+    def __init__(self, c_dt=DEFAULT_C_DT, averaging="strict", forced_dt=None):
+        if not 0.0 < c_dt <= 1.0:
+            raise ConfigurationError(f"c_dt must be in (0, 1], got {c_dt}")
+        if averaging not in ("strict", "creeping"):
+            raise ConfigurationError(f"unknown averaging mode {averaging!r}")
+        self.c_dt, self.averaging, self.forced_dt = c_dt, averaging, forced_dt
+        self.T, self.dt_old, self.dt_new, self.dt_adm = 0.0, 0.0, 0.0, math.inf
+
+
+def _config(grid, kernels, tc, inject_rerun, spike_step, spike_factor, device, rank=0, world=1):
+    cfg = _lib.AdgConfig()
+    cfg.d, cfg.p, cfg.L = grid.d, grid.p, grid.L
+    cfg.cfl = float(kernels.cfl)
+    cfg.c_dt = float(tc.c_dt)
+    cfg.creeping = 1 if tc.averaging == "creeping" else 0
+    cfg.forced_dt = float("nan") if tc.forced_dt is None else float(tc.forced_dt)
+    cfg.inject_rerun = 1 if inject_rerun else 0
+    cfg.spike_step = -1 if spike_step is None else int(spike_step)
+    cfg.spike_factor = float(spike_factor)
+    cfg.device = int(device)
+    cfg.rank, cfg.world = int(rank), int(world)
+    return cfg
+
+
+def upload_operators(handle, basis):
+    ops = [np.ascontiguousarray(a, dtype=np.float64) for a in
+           (basis.nodes, basis.weights, basis.diff, basis.integ, basis.left, basis.right)]
+    handle.call("adg_set_operators", *[_lib.dptr(a) for a in ops])
+    return ops
+
+
+class Driver:
+    """Fused single-touch driver on the GPU (src/scheduler.py:88-226).
+
+    ``host_sync``: "step" copies the state back into ``grid.Q`` after every
+    step (reference semantics: ``cell.Q`` is current after ``step()``);
+    "run" only at the end of ``run()``; "manual" never (call ``sync_state``).
+    """
+
+    def __init__(self, grid, kernels, time_control, mode="fused",
+                 traversal="lexicographic", parallel=False, n_workers=4,
+                 inject_rerun=False, spike_step=None, spike_factor=3.0,
+                 limiter=None, device=0, host_sync="step"):
+        if mode not in ("straightforward", "shifted", "fused"):
+            raise ConfigurationError(f"unknown scheduler mode {mode!r}")
+        if mode != "fused":
+            raise ConfigurationError(
+                f"the GPU driver implements the fused single-touch mode; {mode!r} is out of scope")
+        if limiter is not None:
+            raise ConfigurationError("subcell limiting is supported in straightforward mode only")
+        if isinstance(traversal, np.ndarray):
+            if sorted(traversal.tolist()) != list(range(grid.n_cells)):
+                raise ConfigurationError("traversal must be a permutation of the cells")
+        elif traversal not in ("lexicographic", "peano"):
+            raise ConfigurationError(f"unknown traversal kind {traversal!r}")
+        if host_sync not in ("step", "run", "manual"):
+            raise ConfigurationError(f"unknown host_sync {host_sync!r}")
+        # the fused result is traversal-invariant (tests/test_scheduler.py:111-116):
+        # all cells of a sweep run concurrently on the GPU.
+        self.grid, self.kernels, self.tc, self.mode = grid, kernels, time_control, mode
+        self.traversal, self.parallel, self.n_workers = traversal, parallel, n_workers
+        self.inject_rerun, self.spike_step, self.spike_factor = inject_rerun, spike_step, spike_factor
+        self.limiter = None
+        self.host_sync = host_sync
+        self.sweep_count = self.step_count = self.rerun_count = 0
+        self.reruns_by_step = Counter()
+        self.troubled_by_step = Counter()
+        self.step_records = []
+        self.picard_iters = 0
+        self.predicts = 0
+        cfg = _config(grid, kernels, time_control, inject_rerun, spike_step, spike_factor, device)
+        self.handle = _lib.Handle(cfg)
+        self._ops = upload_operators(self.handle, kernels.basis)
+        self.load_state(grid.Q)
+        self.handle.call("adg_seed")                       # Driver._seed_time_control
+        self._pull_tc()
+
+    # -- state transfer ------------------------------------------------------
+    def load_state(self, Q):
+        Q = np.ascontiguousarray(Q, dtype=np.float64)
+        self.handle.call("adg_load_state", _lib.dptr(Q), Q.size)
+
+    def sync_state(self):
+        """Copy the device state into ``grid.Q`` (``grid.cells[i].Q``)."""
+        Q = self.grid.Q
+        if not Q.flags.c_contiguous:
+            raise ConfigurationError("grid.Q must stay C-contiguous")
+        self.handle.call("adg_store_state", _lib.dptr(Q), Q.size)
+        return Q
+
+    def _pull_tc(self):
+        T, dt_old, dt_new, dt_adm = self.handle.time_control()
+        self.tc.T, self.tc.dt_old, self.tc.dt_new, self.tc.dt_adm = T, dt_old, dt_new, dt_adm
+
+    def _absorb(self, recs):
+        for r in recs:
+            if r.reruns:
+                self.reruns_by_step[r.step] += r.reruns
+            self.picard_iters += r.picard_iters
+            self.predicts += r.predicts
+            self.step_records.append({
+                "step": r.step, "T": r.T, "dt_old": r.dt_old, "dt_new": r.dt_new,
+                "dt_adm": r.dt_adm, "reruns": r.reruns, "troubled": 0,
+                "picard_iters": r.picard_iters, "predicts": r.predicts,
+            })
+        lib, h = self.handle.lib, self.handle.h
+        self.step_count = lib.adg_step_count(h)
+        self.rerun_count = lib.adg_rerun_count(h)
+        self.sweep_count = lib.adg_sweep_count(h)
+        self._pull_tc()
+
+    def _finish(self, recs, err):
+        self._absorb(recs)
+        if err is not None:
+            raise err
+
+    # -- public API (src/scheduler.py:190-226) --------------------------------
+    def step(self):
+        rec = _lib.AdgStepRecord()
+        st = self.handle.lib.adg_step(self.handle.h, rec)
+        err = None
+        try:
+            self.handle.check(st, "adg_step")
+        except Exception as e:  # keep the driver's counters consistent before raising
+            err = e
+        self._finish([rec] if st == 0 else [], err)
+        if self.host_sync == "step":
+            self.sync_state()
+        return self.step_count
+
+    def run(self, steps=None, final_time=None):
+        if (steps is None) == (final_time is None):
+            raise ConfigurationError("specify exactly one of steps / final_time")
+        if final_time is not None:
+            raise ConfigurationError(
+                "final-time integration requires the straightforward driver "
+                "(the pipelined modes realise steps one sweep late)")
+        steps = int(steps)
+        if steps <= 0:
+            return self.step_count
+        recs = (_lib.AdgStepRecord * steps)()
+        before = self.step_count
+        st = self.handle.lib.adg_run(self.handle.h, steps, recs)
+        err = None
+        try:
+            self.handle.check(st, "adg_run")
+        except Exception as e:
+            err = e
+        done = self.handle.lib.adg_step_count(self.handle.h) - before
+        if self.host_sync in ("step", "run"):
+            self.sync_state()
+        self._finish(list(recs)[:done], err)
+        return self.step_count
+
+    def picard_histogram(self):
+        """Picard iterations per predict, summed over every predict so far."""
+        h = self.handle.picard_histogram()
+        return {int(k): int(v) for k, v in enumerate(h) if v}
+
+    def close(self):
+        self.handle.close()
+
+
+def gather(grid):
+    """tests/conftest.py:77-79."""
+    return np.array(grid.Q)
+
+
+__all__ = ["EulerSystem", "Grid", "Cell", "build_grid", "Kernels", "TimeControl",
+           "Driver", "gather", "make_basis", "device_bytes"]

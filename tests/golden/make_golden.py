@@ -1,0 +1,155 @@
+"""Generate golden vectors by running the REFERENCE implementation itself.
+
+Runs only in the build container, where ``/root/reference`` exists:
+
+    python tests/golden/make_golden.py [case ...]     # default: all small cases
+    python tests/golden/make_golden.py --big          # BASELINE-size runs (minutes each)
+
+For every case it builds the reference grid (``build_grid`` with an explicit
+budget, ``src/mesh.py:167-243``), fills ``cell.Q`` from the seeded scenario in
+``paper_1801_08682_b200/scenarios.py``, runs ``Driver(..., "fused")``
+(``src/scheduler.py:92-226``) and stores under ``tests/golden/<case>.npz``:
+
+* ``records``: per step (step, T, dt_old, dt_new, dt_adm, reruns);
+* ``Q_final`` (small cases) or ``Q_sample`` + ``sample_cells`` (large cases:
+  every 97th cell) plus per-component sums/max of the final state;
+* ``Q0_sum``: checksum of the initial state (guards scenario drift);
+* ``picard``: Picard-iteration histogram observed in ``Kernels.predict``
+  (``src/kernels.py:86-97``), counted by wrapping ``system.flux``;
+* ``error``: if the reference raised, its class, message, cell and step.
+
+The scenario builders are the harness's (the reference has no random states,
+``src/cli.py:4-5``); the same array is later fed to the GPU path.
+"""
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+REF_SRC = "/root/reference/pkg/src"
+sys.path.insert(0, REPO)
+sys.path.insert(0, REF_SRC)
+
+from paper_1801_08682_b200 import scenarios  # noqa: E402
+
+# name: (scenario, d, L, p, steps, extra driver kwargs, tc kwargs, store full Q)
+SMALL = {
+    "bump_d2_L2_p3": ("bump", 2, 2, 3, 10, {}, {}, True),
+    "bump_d2_L3_p3_cfg1": ("bump", 2, 3, 3, 20, {}, {}, True),
+    "bump_d2_L1_p0": ("bump", 2, 1, 0, 6, {}, {}, True),
+    "bump_d2_L2_p1": ("bump", 2, 2, 1, 8, {}, {}, True),
+    "bump_d2_L1_p9": ("bump", 2, 1, 9, 4, {}, {}, True),
+    "bump_d2_L2_p6": ("bump", 2, 2, 6, 4, {}, {}, True),
+    "bump_d3_L1_p3": ("bump", 3, 1, 3, 5, {}, {}, True),
+    "bump_d3_L1_p2": ("bump", 3, 1, 2, 5, {}, {}, True),
+    "bump_d3_L1_p5": ("bump", 3, 1, 5, 4, {}, {}, True),
+    "bump_d3_L2_p3": ("bump", 3, 2, 3, 4, {}, {}, False),
+    "fourier_d3_L1_p4": ("fourier", 3, 1, 4, 3, {}, {}, True),
+    "wave_d2_L1_p2_spike": ("wave", 2, 1, 2, 10, {"spike_step": 4}, {}, True),
+    "wave_d2_L1_p3_inject": ("wave", 2, 1, 3, 4, {"inject_rerun": True}, {}, True),
+    "wave_d2_L2_p3_forced": ("wave", 2, 2, 3, 10, {}, {"forced_dt": 2e-4}, True),
+    "wave_d3_L1_p2_creeping": ("wave", 3, 1, 2, 5, {}, {"averaging": "creeping"}, True),
+    "uniform_d2_L1_p2": ("uniform", 2, 1, 2, 5, {}, {}, True),
+}
+BIG = {
+    "bump_d3_L3_p3_cfg2": ("bump", 3, 3, 3, 20, {}, {}, False),
+    "bump_d3_L3_p5_cfg3": ("bump", 3, 3, 5, 10, {}, {}, False),
+    "bump_d3_L3_p7_cfg3": ("bump", 3, 3, 7, 10, {}, {}, False),
+    "bump_d3_L3_p9_cfg3": ("bump", 3, 3, 9, 10, {}, {}, False),
+    "bump_d3_L2_p5": ("bump", 3, 2, 5, 10, {}, {}, False),
+}
+SAMPLE_STRIDE = 97
+
+
+def run_case(name, spec):
+    from aderdg import (Driver, EulerSystem, Kernels, NumericalError,
+                        PredictorFailureError, TimeControl, build_grid, make_basis)
+    scen, d, L, p, steps, dkw, tkw, full = spec
+    Q0 = scenarios.build(scen, d, L, p)
+    system = EulerSystem(d)
+    basis = make_basis(p)
+    grid = build_grid(d, L, p, system.m, budget_bytes=1 << 40)
+    for c in grid.cells:
+        c.Q[...] = Q0[c.index]
+    kernels = Kernels(system, basis, grid, None, cfl=0.9)
+    hist = {}
+    orig_flux = system.flux
+    calls = {"n": 0}
+
+    def counting_flux(Q):   # predict calls flux once per Picard iteration + once at the end
+        calls["n"] += 1
+        return orig_flux(Q)
+
+    system.flux = counting_flux
+    orig_predict = kernels.predict
+
+    def counting_predict(cell, dt):
+        calls["n"] = 0
+        out = orig_predict(cell, dt)
+        k = calls["n"] - 1
+        hist[k] = hist.get(k, 0) + 1
+        return out
+
+    kernels.predict = counting_predict
+    tc = TimeControl(c_dt=0.99, **tkw)
+    error = None
+    t0 = time.time()
+    try:
+        driver = Driver(grid, kernels, tc, "fused", **dkw)
+        for _ in range(steps):
+            driver.step()
+    except (NumericalError, PredictorFailureError) as e:
+        error = {"class": type(e).__name__, "message": str(e),
+                 "cell": getattr(e, "cell_index", None)}
+        driver = locals().get("driver")
+    wall = time.time() - t0
+    recs = driver.step_records if driver is not None else []
+    rec_arr = np.array([[r["step"], r["T"], r["dt_old"], r["dt_new"], r["dt_adm"], r["reruns"]]
+                        for r in recs], dtype=np.float64).reshape(-1, 6)
+    Qf = np.stack([c.Q for c in grid.cells])
+    out = {
+        "records": rec_arr,
+        "Q0_sum": np.array([np.sum(Q0), np.sum(np.abs(Q0))]),
+        "Q_final_sum": np.sum(Qf.reshape(-1, Qf.shape[-1]), axis=0),
+        "Q_final_absmax": np.max(np.abs(Qf.reshape(-1, Qf.shape[-1])), axis=0),
+        "picard_keys": np.array(sorted(hist), dtype=np.int64),
+        "picard_vals": np.array([hist[k] for k in sorted(hist)], dtype=np.int64),
+        "meta": np.array(json.dumps({"scenario": scen, "d": d, "L": L, "p": p, "steps": steps,
+                                     "driver_kwargs": dkw, "tc_kwargs": tkw, "error": error,
+                                     "wall_s": wall, "sweep_count": driver.sweep_count if driver else None,
+                                     "rerun_count": driver.rerun_count if driver else None,
+                                     "reruns_by_step": {str(k): v for k, v in
+                                                        (driver.reruns_by_step.items() if driver else [])}})),
+    }
+    if error is None:
+        if full:
+            out["Q_final"] = Qf
+        else:
+            cells = np.arange(0, Qf.shape[0], SAMPLE_STRIDE)
+            out["sample_cells"] = cells
+            out["Q_sample"] = Qf[cells]
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(f"{name}: {wall:.1f}s steps={len(recs)} error={error}", flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("cases", nargs="*")
+    ap.add_argument("--big", action="store_true")
+    args = ap.parse_args()
+    table = dict(SMALL)
+    table.update(BIG)
+    names = args.cases or (list(BIG) if args.big else list(SMALL))
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    for n in names:
+        run_case(n, table[n])
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,128 @@
+"""GPU parity: the sm_100a path (through the C ABI) against golden vectors
+produced by the reference itself and against the CPU oracle.
+
+Bar (BASELINE.json north_star): relative L-inf <= 1e-10 in fp64 after the
+stated number of steps, identical rerun steps, identical abort step/cell.
+"""
+
+import numpy as np
+import pytest
+
+import aderdg_oracle as O
+from conftest import golden_names, load_golden, rel_linf
+from paper_1801_08682_b200 import (Driver, EulerSystem, Kernels, NumericalError,
+                                   PredictorFailureError, TimeControl, build_grid,
+                                   make_basis, scenarios)
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10   # north_star: rel L-inf in fp64
+
+
+def make_driver(Q0, d, L, p, dkw=None, tkw=None, host_sync="run"):
+    grid = build_grid(d, L, p, d + 2)
+    grid.Q[...] = Q0
+    kern = Kernels(EulerSystem(d), make_basis(p), grid, None, cfl=0.9)
+    tc = TimeControl(c_dt=0.99, **(tkw or {}))
+    return Driver(grid, kern, tc, "fused", host_sync=host_sync, **(dkw or {}))
+
+
+def records_array(drv):
+    return np.array([[r["step"], r["T"], r["dt_old"], r["dt_new"], r["dt_adm"], r["reruns"]]
+                     for r in drv.step_records]).reshape(-1, 6)
+
+
+SMALL = [n for n in golden_names() if not any(t in n for t in ("cfg2", "cfg3", "L2_p5"))]
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_gpu_matches_reference_golden(cuda_ok, name):
+    g = load_golden(name)
+    meta = g["meta"]
+    d, L, p = meta["d"], meta["L"], meta["p"]
+    Q0 = scenarios.build(meta["scenario"], d, L, p)
+    drv = make_driver(Q0, d, L, p, meta["driver_kwargs"], meta["tc_kwargs"])
+    drv.run(steps=meta["steps"])
+    recs = records_array(drv)
+    ref = g["records"]
+    assert np.array_equal(recs[:, 0], ref[:, 0])
+    assert np.array_equal(recs[:, 5], ref[:, 5]), "rerun steps differ"
+    assert np.max(np.abs(recs[:, 1:5] - ref[:, 1:5]) / np.abs(ref[:, 1:5]).clip(1e-300)) < TOL
+    assert drv.sweep_count == meta["sweep_count"]
+    assert drv.rerun_count == meta["rerun_count"]
+    Q = drv.grid.Q
+    if "Q_final" in g:
+        err = rel_linf(Q, g["Q_final"])
+    else:
+        err = rel_linf(Q[g["sample_cells"]], g["Q_sample"])
+    assert err <= TOL, f"{name}: rel L-inf {err:.3e}"
+
+
+@pytest.mark.parametrize("d,L,p,steps,seed", [(3, 2, 3, 3, 7), (2, 2, 4, 6, 3), (3, 1, 4, 4, 11),
+                                              (2, 2, 7, 3, 5), (3, 2, 5, 2, 1)])
+def test_gpu_matches_oracle_random_seeds(cuda_ok, d, L, p, steps, seed):
+    Q0 = scenarios.build("bump", d, L, p, seed=seed, noise=1e-2)
+    drv = make_driver(Q0, d, L, p)
+    drv.run(steps=steps)
+    ora = O.FusedDriver(Q0.copy(), d, p, L)
+    ora.run(steps)
+    assert rel_linf(drv.grid.Q, ora.Q) <= TOL
+    assert [r["reruns"] for r in drv.step_records] == [r["reruns"] for r in ora.step_records]
+    # Picard counts follow the reference criterion (report parity, allow rare off-by-one cells)
+    gh = drv.picard_histogram()
+    oh = dict(ora.k.picard_hist)
+    assert sum(gh.values()) == sum(oh.values())
+    assert abs(sum(k * v for k, v in gh.items()) - sum(k * v for k, v in oh.items())) <= 0.01 * sum(oh.values())
+
+
+def test_uniform_state_is_fixed_point(cuda_ok):
+    # tests/test_scheduler.py:63-76
+    d, L, p = 2, 1, 2
+    ref = np.array([1.0, 0.3, -0.1, 2.5])
+    Q0 = np.broadcast_to(ref, (9, 3, 3, 4)).copy()
+    drv = make_driver(Q0, d, L, p)
+    drv.run(steps=5)
+    assert np.max(np.abs(drv.grid.Q - ref)) < 1e-13
+
+
+def test_step_by_step_equals_run(cuda_ok):
+    Q0 = scenarios.build("bump", 3, 1, 3)
+    a = make_driver(Q0, 3, 1, 3, host_sync="step")
+    for _ in range(4):
+        a.step()
+    b = make_driver(Q0, 3, 1, 3)
+    b.run(steps=4)
+    assert np.array_equal(a.grid.Q, b.grid.Q)
+    assert records_array(a).tolist() == records_array(b).tolist()
+
+
+def test_inadmissible_initial_data_refused(cuda_ok):
+    # tests/test_scheduler.py:238-246: Driver construction raises NumericalError
+    Q0 = scenarios.build("bump", 2, 1, 2)
+    Q0[5, 1, 1, 0] = -1.0
+    with pytest.raises(NumericalError) as e:
+        make_driver(Q0, 2, 1, 2)
+    assert "initial data inadmissible in cell 5" in str(e.value)
+
+
+def test_nonfinite_initial_data_refused(cuda_ok):
+    Q0 = scenarios.build("bump", 3, 1, 2)
+    Q0[13, 0, 0, 0, 2] = np.nan
+    with pytest.raises(NumericalError) as e:
+        make_driver(Q0, 3, 1, 2)
+    assert "cell 13" in str(e.value)
+
+
+def test_conservation_at_baseline_size(cuda_ok):
+    """Size-independent property at cfg 2 size (27^3, p=3): the periodic DG
+    scheme conserves sum_cells sum_nodes w Q exactly up to rounding."""
+    d, L, p = 3, 3, 3
+    Q0 = scenarios.build("bump", d, L, p)
+    drv = make_driver(Q0, d, L, p)
+    drv.run(steps=20)
+    w = make_basis(p).weights
+    W = np.einsum("i,j,k->ijk", w, w, w)
+    tot0 = np.einsum("cijkm,ijk->m", Q0, W)
+    tot1 = np.einsum("cijkm,ijk->m", drv.grid.Q, W)
+    scale = np.einsum("cijkm,ijk->m", np.abs(Q0), W)
+    assert np.all(np.abs(tot1 - tot0) <= 1e-12 * scale), (tot1 - tot0) / scale
+    assert [r["reruns"] for r in drv.step_records] == [0] * 20
