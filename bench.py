@@ -1,0 +1,357 @@
+#!/usr/bin/env python
+"""bench.py — fp64 DoF-updates/s of the fused ADER-DG Euler step on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+
+Metric (BASELINE.json): fp64 DoF-updates/s for 3D Euler ADER-DG at order p,
+DoF = cells * (p+1)^d * m.  Default workload = BASELINE config 2 (3D, p=3,
+27^3 periodic cells, Gaussian bump + seeded 1e-3 density noise, Rusanov,
+CFL 0.9/(d(2p+1)), c_dt 0.99): a "step" is one fused realisation step of
+the whole grid (rerun pass when the optimistic step fails, fused
+Riemann/corrector/update/CFL/predictor sweep, device time control).
+N > 1: x-slab decomposition, one process per GPU (torchrun), NCCL halo
+exchange + lambda all-reduce per step; total work fixed (strong scaling).
+
+Reported on one JSON line (rank 0):
+  value      DoF-updates/s, device-timed (CUDA events, max over ranks), state resident in HBM
+  e2e        same metric through the C ABI with host buffers: per step H2D of Q from
+             pinned memory, adg step, D2H of Q (wall clock, max over ranks)
+  roofline   dominant kernel (sweep_kernel: fused sweep + rerun passes), algorithmic
+             flops (paper_1801_08682_b200/roofline.py, measured Picard counts) / its
+             CUDA-event time, against the measured FP64 peak (profiles/fp64_peaks_r01.jsonl)
+  cpu_baseline  the CPU oracle port (oracle/aderdg_oracle.py, batched numpy) timed on
+             this host on a bounded sample (rank 0, N=1 only)
+--impl reference: times the oracle port (the reference is CPU-only Python; the oracle is
+its batched restatement) on a bounded sample of the same workload, rank 0 only.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+CONFIGS = {
+    "cfg1": dict(d=2, L=3, p=3, scenario="bump", steps=20,
+                 desc="BASELINE cfg1: 2D Euler p=3, 27^2 periodic, bump+1e-3 noise, 20 steps"),
+    "cfg2": dict(d=3, L=3, p=3, scenario="bump", steps=20,
+                 desc="BASELINE cfg2: 3D Euler p=3, 27^3 periodic, bump+1e-3 noise, 20 steps"),
+    "cfg3_p5": dict(d=3, L=3, p=5, scenario="bump", steps=10,
+                    desc="BASELINE cfg3: 3D Euler p=5, 27^3 periodic, bump+1e-3 noise, 10 steps"),
+    "cfg4": dict(d=3, L=4, p=5, scenario="bump", steps=10,
+                 desc="BASELINE cfg4: 3D Euler p=5, 81^3 periodic, bump+1e-3 noise, 10 steps"),
+}
+
+PEAKS_FILE = os.path.join(REPO, "profiles", "fp64_peaks_r01.jsonl")
+NCU_TRAFFIC_FILE = os.path.join(REPO, "profiles", "sweep_traffic_r01.json")
+
+
+def load_peaks():
+    dmma = dfma = None
+    try:
+        with open(PEAKS_FILE) as fh:
+            for line in fh:
+                r = json.loads(line)
+                if r.get("test") == "dfma":
+                    dfma = max(dfma or 0, r["tflops"])
+                if r.get("test", "").startswith("dmma"):
+                    dmma = max(dmma or 0, r["tflops"])
+    except OSError:
+        pass
+    hbm = None
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            hbm = json.load(fh).get("hbm_gbs")
+    except OSError:
+        pass
+    return dfma, dmma, hbm
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = f"/tmp/adg_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.fh.close()
+        sms, maxs, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm = float(parts[1])
+                    mx = float(parts[2])
+                except ValueError:
+                    continue
+                sms.append(sm)
+                maxs.append(mx)
+                for nm, v in zip(names, parts[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+        os.unlink(self.path)
+        if not sms:
+            return None
+        busy = [s for s in sms if s > 500] or sms
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": max(maxs),
+                "samples": len(sms), "reasons": sorted(reasons)}
+
+
+def cpu_oracle_rate(cfgd, steps, warmup, L_override=None):
+    """Time the CPU oracle (oracle/aderdg_oracle.py) on a bounded sample."""
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import aderdg_oracle as O
+    from paper_1801_08682_b200 import roofline, scenarios
+    d, p = cfgd["d"], cfgd["p"]
+    L = L_override or cfgd["L"]
+    Q0 = scenarios.build(cfgd["scenario"], d, L, p)
+    drv = O.FusedDriver(Q0, d, p, L)
+    drv.step()                       # priming + first step (not timed)
+    for _ in range(warmup):
+        drv.step()
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        drv.step()
+        times.append(time.perf_counter() - t0)
+    dofs = roofline.dof(d, p, 3 ** (d * L))
+    try:
+        from threadpoolctl import threadpool_info
+        blas = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        blas = 1
+    return dofs * len(times) / sum(times), times, blas, L
+
+
+def run_reference(args, cfgd):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    # bounded sample: same d, p and state family on the 9^3 (3D) / 27^2 (2D) grid
+    L_s = 2 if cfgd["d"] == 3 else 3
+    rate, times, blas, L = cpu_oracle_rate(cfgd, args.steps, args.warmup, L_override=L_s)
+    sample = (f"oracle port (batched numpy restatement of the reference fused driver), "
+              f"{3 ** L}^{cfgd['d']} cells p={cfgd['p']}, {len(times)} steps after priming+"
+              f"{args.warmup} warm-up; BLAS threads {blas}, numpy elementwise single-threaded")
+    ms = 1e3 * sum(times) / len(times)
+    line = {
+        "impl": "reference", "metric": "fp64 DoF-updates/s (3D Euler ADER-DG, fused step)",
+        "value": rate, "unit": "DoF-updates/s", "n_gpus": args.gpus, "steps": len(times),
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfgd["desc"], "d": cfgd["d"], "p": cfgd["p"],
+                   "cells_sample": 3 ** (cfgd["d"] * L)},
+        "cpu_baseline": {"value": rate, "unit": "DoF-updates/s", "cores": blas, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": rate, "unit": "DoF-updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfgd = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfgd)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_1801_08682_b200 import _lib, roofline, scenarios
+    from paper_1801_08682_b200.parallel import SlabDriver
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    d, L, p = cfgd["d"], cfgd["L"], cfgd["p"]
+    cells = 3 ** (d * L)
+    dofs = roofline.dof(d, p, cells)
+    Q0 = scenarios.build(cfgd["scenario"], d, L, p)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---------------- device-resident timing (value) ----------------
+    drv = SlabDriver(Q0, d, L, p, rank, world, local)
+    h = drv.handle
+    for _ in range(args.warmup):
+        drv.enqueue_step()
+    h.call("adg_sync")
+    step0 = h.lib.adg_step_count(h.h)
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(K)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.05)
+    start.record()
+    for i in range(K):
+        e0, e1, e2, e3 = ev[i]
+        e0.record()
+        h.call("adg_phase_rerun")
+        e1.record()
+        drv.halo.exchange(drv.tr[h.lib.adg_trace_parity(h.h)])
+        e2.record()
+        h.call("adg_phase_sweep")
+        e3.record()
+        drv.halo.reduce(drv.red)
+        h.call("adg_phase_finish")
+    stop.record()
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    h.call("adg_sync")
+    elapsed_ms = max_over_ranks(start.elapsed_time(stop))
+    kern_ms = sum(ev[i][0].elapsed_time(ev[i][1]) + ev[i][2].elapsed_time(ev[i][3]) for i in range(K))
+    recs = h.step_records(step0 + 1, K)
+    iters = sum(r.picard_iters for r in recs)
+    preds = sum(r.predicts for r in recs)
+    reruns = sum(r.reruns for r in recs)
+    local_cells = drv.n_local
+    flops = roofline.flops_step(d, p, local_cells, iters, preds) if K else 0
+    # per-rank picard counts are local; the flop count is local too (per-GPU roofline)
+    ms_per_step = elapsed_ms / K
+    value = dofs * K / (elapsed_ms * 1e-3)
+    kern_ms_per_step = kern_ms / K
+    achieved_tf = flops / (kern_ms * 1e-3) / 1e12
+    dfma, dmma, hbm = load_peaks()
+    peak_tf = dmma or dfma or 37.1
+    traffic = None
+    try:
+        with open(NCU_TRAFFIC_FILE) as fh:
+            tinfo = json.load(fh)
+        traffic = tinfo.get(args.config, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        pass
+    bytes_alg = roofline.bytes_step(d, p, local_cells, preds // K if K else None)
+    hbm_frac = (bytes_alg / (kern_ms_per_step * 1e-3) / 1e9) / hbm if hbm else None
+
+    # ---------------- end-to-end through the C ABI with host buffers ----------------
+    e2e = None
+    if not args.no_e2e:
+        n_state = int(drv.lay.state_doubles)
+        pinned = torch.empty(n_state, dtype=torch.float64, pin_memory=True)
+        hostQ = pinned.numpy()
+        hostQ[:] = drv.local_state().reshape(-1)
+        ptr = _lib.dptr(hostQ)
+        e2e_steps = K
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            h.call("adg_load_state", ptr, n_state)       # H2D of the step's input state
+            drv.enqueue_step()
+            h.call("adg_store_state", ptr, n_state)      # D2H of the step's result (synchronous)
+        t1 = time.perf_counter()
+        barrier()
+        e2e_s = max_over_ranks(t1 - t0)
+        h.call("adg_sync")
+        e2e = {"value": dofs * e2e_steps / e2e_s, "unit": "DoF-updates/s",
+               "h2d_bytes_per_step": 8 * n_state * world, "d2h_bytes_per_step": 8 * n_state * world,
+               "ms_per_step": 1e3 * e2e_s / e2e_steps,
+               "path": "adg_load_state (pinned H2D) + phase step + adg_store_state (D2H), per step"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        L_s = 2 if d == 3 else L
+        rate, times, blas, Ls = cpu_oracle_rate(cfgd, 2, 0, L_override=L_s)
+        cpu = {"value": rate, "unit": "DoF-updates/s", "cores": blas, "kind": "port",
+               "sample": (f"oracle/aderdg_oracle.py (batched numpy restatement of the reference "
+                          f"fused driver), {3 ** Ls}^{d} cells p={p}, 2 steps after priming; "
+                          f"BLAS threads {blas}, numpy elementwise single-threaded")}
+
+    if rank == 0:
+        line = {
+            "metric": "fp64 DoF-updates/s (3D Euler ADER-DG, fused step)",
+            "value": value, "unit": "DoF-updates/s", "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfgd["desc"], "d": d, "p": p, "L": L, "cells": cells,
+                       "nodes": cells * (p + 1) ** d, "dof": dofs,
+                       "parallelism": f"x-slab x{world}" if world > 1 else "single GPU",
+                       "l2": "no flush: per-step working set (Q,D r/w + 2 trace parities) "
+                             f"{roofline.bytes_step(d, p, cells) / 1e6:.0f} MB > 126 MB L2",
+                       "steps_simulated": args.warmup + K + (K if e2e else 0),
+                       "reruns_in_timed": reruns, "picard_mean": iters / max(preds, 1)},
+            "roofline": {"bound": "fp64", "achieved": achieved_tf, "peak": peak_tf,
+                         "unit": "TFLOP/s", "frac": achieved_tf / peak_tf, "traffic": traffic,
+                         "kernel": f"sweep_kernel<{d},{p + 1}> (fused sweep + rerun passes)",
+                         "kernel_ms_per_step": kern_ms_per_step,
+                         "kernel_share_of_step": kern_ms_per_step / ms_per_step,
+                         "flops_per_step_per_gpu": flops / K if K else 0,
+                         "peak_source": "profiles/fp64_peaks_r01.jsonl (measured DMMA m8n8k4; "
+                                        f"DFMA {dfma} TF/s) — MEASURED_PEAKS.json has no fp64 entry",
+                         "hbm_alg_bytes_per_step": bytes_alg, "hbm_frac_of_measured": hbm_frac},
+            "gpu_launches": 3 * K,
+            "clocks": clk,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    drv.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

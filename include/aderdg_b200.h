@@ -120,6 +120,8 @@ adg_status adg_store_state(adg_handle* h, double* Q, size_t n_doubles);
 adg_status adg_seed(adg_handle* h);
 adg_status adg_step(adg_handle* h, adg_step_record* out);
 adg_status adg_run(adg_handle* h, int steps, adg_step_record* out);
+/* records of steps first..first+count-1 (1-based; the last 4096 steps are kept) */
+adg_status adg_step_records(adg_handle* h, int first, int count, adg_step_record* out);
 adg_status adg_sync(adg_handle* h);
 int        adg_step_count(const adg_handle* h);
 int        adg_rerun_count(const adg_handle* h);

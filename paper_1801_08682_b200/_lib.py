@@ -23,6 +23,7 @@ ADG_BUF_Q, ADG_BUF_D, ADG_BUF_TRACE0, ADG_BUF_TRACE1, ADG_BUF_REDUCE = range(5)
 EXPORTS = (
     "adg_create", "adg_destroy", "adg_set_operators", "adg_set_stream",
     "adg_load_state", "adg_store_state", "adg_seed", "adg_step", "adg_run",
+    "adg_step_records",
     "adg_sync", "adg_step_count", "adg_rerun_count", "adg_sweep_count",
     "adg_time_control", "adg_picard_histogram", "adg_error_info",
     "adg_last_error", "adg_layout_info", "adg_buffer", "adg_phase_seed",
@@ -85,6 +86,8 @@ def load_library(path=None):
         "adg_seed": (ctypes.c_int, [H]),
         "adg_step": (ctypes.c_int, [H, ctypes.POINTER(AdgStepRecord)]),
         "adg_run": (ctypes.c_int, [H, ctypes.c_int, ctypes.POINTER(AdgStepRecord)]),
+        "adg_step_records": (ctypes.c_int, [H, ctypes.c_int, ctypes.c_int,
+                                            ctypes.POINTER(AdgStepRecord)]),
         "adg_sync": (ctypes.c_int, [H]),
         "adg_step_count": (ctypes.c_int, [H]),
         "adg_rerun_count": (ctypes.c_int, [H]),
@@ -181,6 +184,11 @@ class Handle:
         v = [ctypes.c_double() for _ in range(4)]
         self.call("adg_time_control", *[ctypes.byref(x) for x in v])
         return tuple(x.value for x in v)
+
+    def step_records(self, first, count):
+        recs = (AdgStepRecord * max(count, 1))()
+        self.call("adg_step_records", int(first), int(count), recs)
+        return list(recs)[:count]
 
     def picard_histogram(self, bins=32):
         arr = (ctypes.c_longlong * bins)()

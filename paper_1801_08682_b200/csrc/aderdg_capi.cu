@@ -446,6 +446,13 @@ adg_status adg_run(adg_handle* h, int steps, adg_step_record* out) {
   return ADG_OK;
 }
 
+adg_status adg_step_records(adg_handle* h, int first, int count, adg_step_record* out) {
+  if (!h || !out || first < 1 || count < 0) return ADG_ERR_CONFIG;
+  if (first + count - 1 > h->hst.step || h->hst.step - first >= h->rec_cap)
+    return fail(h, ADG_ERR_CONFIG, "requested step records are not available");
+  return fetch_records(h, first - 1, first - 1 + count, out);
+}
+
 adg_status adg_sync(adg_handle* h) {
   if (!h) return ADG_ERR_CONFIG;
   adg_status s = pull_state(h);
