@@ -114,7 +114,13 @@ void       adg_destroy(adg_handle* h);
 adg_status adg_set_operators(adg_handle* h, const double* nodes, const double* weights,
                              const double* diff, const double* integ,
                              const double* left, const double* right);
-adg_status adg_set_stream(adg_handle* h, void* cuda_stream);   /* cudaStream_t; NULL = handle's own */
+/* Launch stream: a cudaStream_t (NULL = the legacy default stream).  Until this
+ * is called the handle uses its own non-blocking stream. */
+adg_status adg_set_stream(adg_handle* h, void* cuda_stream);
+/* Back to the state right after adg_create: time control, counters, D and the
+ * face records are cleared (Q is kept; load a new one with adg_load_state and
+ * call adg_seed).  Used to restart an episode from the initial data. */
+adg_status adg_reset(adg_handle* h);
 adg_status adg_load_state(adg_handle* h, const double* Q, size_t n_doubles);
 adg_status adg_store_state(adg_handle* h, double* Q, size_t n_doubles);
 adg_status adg_seed(adg_handle* h);

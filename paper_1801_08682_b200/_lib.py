@@ -28,7 +28,7 @@ EXPORTS = (
     "adg_time_control", "adg_picard_histogram", "adg_error_info",
     "adg_last_error", "adg_layout_info", "adg_buffer", "adg_phase_seed",
     "adg_phase_seed_finish", "adg_phase_rerun", "adg_phase_sweep",
-    "adg_phase_finish", "adg_trace_parity", "adg_flush_l2",
+    "adg_phase_finish", "adg_trace_parity", "adg_flush_l2", "adg_reset",
 )
 
 
@@ -108,6 +108,7 @@ def load_library(path=None):
         "adg_phase_finish": (ctypes.c_int, [H]),
         "adg_trace_parity": (ctypes.c_int, [H]),
         "adg_flush_l2": (ctypes.c_int, [H]),
+        "adg_reset": (ctypes.c_int, [H]),
     }
     for name, (res, args) in proto.items():
         fn = getattr(lib, name)

@@ -312,7 +312,27 @@ adg_status adg_set_operators(adg_handle* h, const double* nodes, const double* w
 
 adg_status adg_set_stream(adg_handle* h, void* s) {
   if (!h) return ADG_ERR_CONFIG;
-  h->stream = s ? (cudaStream_t)s : h->own_stream;
+  h->stream = (cudaStream_t)s;
+  return ADG_OK;
+}
+
+adg_status adg_reset(adg_handle* h) {
+  if (!h) return ADG_ERR_CONFIG;
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  const size_t state_bytes = sizeof(double) * (size_t)h->cells_local * h->NS * h->m;
+  const size_t tr_bytes = sizeof(double) * (size_t)(2 * h->cfg.d) * h->slots * h->REC;
+  CUDA_TRY(h, cudaMemsetAsync(h->D, 0, state_bytes, h->stream));
+  CUDA_TRY(h, cudaMemsetAsync(h->tr[0], 0, tr_bytes, h->stream));
+  CUDA_TRY(h, cudaMemsetAsync(h->tr[1], 0, tr_bytes, h->stream));
+  DevState s0;
+  memset(&s0, 0, sizeof s0);
+  s0.dt_adm = INFINITY;
+  CUDA_TRY(h, cudaMemcpyAsync(h->st, &s0, sizeof s0, cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  h->hst = s0;
+  h->sweep_index = 0;
+  h->seeded = false;
+  h->err.clear();
   return ADG_OK;
 }
 

@@ -113,9 +113,6 @@ class SlabDriver:
         plane0, planes = slab_partition(K, world, rank)
         assert planes == lay.planes_local and plane0 * lay.plane_cells == lay.cell_offset
         self.cell_offset, self.n_local = lay.cell_offset, lay.n_cells_local
-        Ql = np.ascontiguousarray(Q_global[self.cell_offset:self.cell_offset + self.n_local],
-                                  dtype=np.float64)
-        self.handle.call("adg_load_state", _lib.dptr(Ql), Ql.size)
         self.halo = HaloExchange(lay.planes_local, lay.plane_cells, rank, world, group)
         slots = (lay.planes_local + 2) * lay.plane_cells
         shape = (lay.faces_per_cell, slots, lay.record_doubles)
@@ -127,7 +124,17 @@ class SlabDriver:
         rptr, _ = self.handle.buffer(_lib.ADG_BUF_REDUCE)
         self.red = torch.as_tensor(_lib.DeviceArray(rptr, (2,), "<i8", self.dev), device=self.dev)
         self.primed = False
-        # seed (Driver._seed_time_control) with the global reduction
+        self.load(Q_global, reset=False)
+
+    def load(self, Q_global, reset=True):
+        """(Re)start from global initial data: upload the local slab and seed the
+        time control (Driver._seed_time_control) with the global reduction."""
+        if reset:
+            self.handle.call("adg_reset")
+            self.primed = False
+        Ql = np.ascontiguousarray(Q_global[self.cell_offset:self.cell_offset + self.n_local],
+                                  dtype=np.float64)
+        self.handle.call("adg_load_state", _lib.dptr(Ql), Ql.size)
         self.handle.call("adg_phase_seed")
         self.halo.reduce(self.red)
         self.handle.call("adg_phase_seed_finish")
