@@ -10,11 +10,13 @@
 #include <stdio.h>
 #include <string.h>
 #include <math.h>
+#include <stdlib.h>
 #include <string>
 #include <vector>
 
 #include "../../include/aderdg_b200.h"
 #include "aderdg_kernels.cuh"
+#include "aderdg_sweep_v2.cuh"
 
 using namespace adg;
 
@@ -34,8 +36,17 @@ void launch_sweep(const SweepParams& P, unsigned grid, cudaStream_t s) {
   sweep_kernel<DIM, NQ><<<grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
 }
 
-template <int DIM, int NQ>
-int record_doubles() { return Shape<DIM, NQ>::REC; }
+template <int NQ, int TS, bool DMMA>
+void launch_sweep_v2(const SweepParams& P, unsigned grid, cudaStream_t s) {
+  using S = ShapeV2<NQ, TS, DMMA>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sweep_kernel_v2<NQ, TS, DMMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)S::SMEM_BYTES);
+    attr = true;
+  }
+  sweep_kernel_v2<NQ, TS, DMMA><<<grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
+}
 
 struct Dispatch {
   launch_fn sweep;
@@ -44,6 +55,18 @@ struct Dispatch {
 
 template <int DIM, int NQ>
 Dispatch make_dispatch() { return Dispatch{&launch_sweep<DIM, NQ>, Shape<DIM, NQ>::REC}; }
+
+template <int NQ, int TS, bool DMMA>
+Dispatch make_dispatch_v2() {
+  static_assert(ShapeV2<NQ, TS, DMMA>::REC == Shape<3, NQ>::REC, "record layout must match");
+  return Dispatch{&launch_sweep_v2<NQ, TS, DMMA>, ShapeV2<NQ, TS, DMMA>::REC};
+}
+
+int kernel_variant() {
+  // ADG_KERNEL=1: first-generation kernel; 2: time-split v2; 3 (default): v2 without time split
+  const char* v = getenv("ADG_KERNEL");
+  return v ? (v[0] - '0') : 3;
+}
 
 bool dispatch_for(int d, int p, Dispatch* out) {
   const int n = p + 1;
@@ -65,9 +88,15 @@ bool dispatch_for(int d, int p, Dispatch* out) {
       case 1: *out = make_dispatch<3, 1>(); return true;
       case 2: *out = make_dispatch<3, 2>(); return true;
       case 3: *out = make_dispatch<3, 3>(); return true;
-      case 4: *out = make_dispatch<3, 4>(); return true;
+      case 4:
+        *out = kernel_variant() == 1 ? make_dispatch<3, 4>()
+             : kernel_variant() == 2 ? make_dispatch_v2<4, 2, true>() : make_dispatch_v2<4, 1, true>();
+        return true;
       case 5: *out = make_dispatch<3, 5>(); return true;
-      case 6: *out = make_dispatch<3, 6>(); return true;
+      case 6:
+        *out = kernel_variant() == 1 ? make_dispatch<3, 6>()
+             : kernel_variant() == 2 ? make_dispatch_v2<6, 2, false>() : make_dispatch_v2<6, 1, false>();
+        return true;
     }
   }
   return false;

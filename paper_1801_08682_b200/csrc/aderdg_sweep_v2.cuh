@@ -1,0 +1,616 @@
+// aderdg_sweep_v2.cuh — second-generation fused sweep kernel (3D, even p+1).
+//
+// Changes against sweep_kernel (aderdg_kernels.cuh), driven by the r01 ncu
+// profile (12 warps/SM, 168 regs, 30% smem bank conflicts, long-scoreboard
+// stalls on the staging loads):
+//   * time split: TS threads per spatial node, each owning NQ/TS time levels
+//     of the space-time predictor -> TS x more warps, fewer registers.  The
+//     time contraction of the Picard update (integ) reads the per-slice
+//     divergence of all time levels from shared memory (sDiv).
+//   * TMA bulk copies (cp.async.bulk + mbarrier) stage Q, D and the 4d face
+//     records of the cell into shared memory in one shot; Q and D go back
+//     with bulk stores.
+//   * padded flux slices: the axis-0 plane stride is NQ^2 + pad so that the
+//     derivative gathers of a warp are bank-conflict free (broadcasts only).
+//   * p = 3 (NQ = 4): node index bits i2 sit in lane bits 0-1, so the axis-2
+//     derivative is one DMMA.8x8x4 per component with the flux in the A
+//     fragment and an interleaved diff^T in B: the result lands in the lane
+//     that owns the node (no shared-memory round trip for that axis).
+//
+// Reference (src/ = /root/reference/pkg/src/aderdg/): same as sweep_kernel —
+// kernels.py:68-229 (seven tasks), scheduler.py:370-449 (fused sweep).
+#pragma once
+#include "aderdg_kernels.cuh"
+
+namespace adg {
+
+__host__ __device__ constexpr int plane_pad(int nq) {
+  // smallest pad so that (nq*nq + pad) mod 16 lies in [nq, 16 - nq] (8-byte banks)
+  return ((nq * nq) % 16 >= nq && (nq * nq) % 16 <= 16 - nq) ? 0
+         : (((nq * nq + 2) % 16 >= nq && (nq * nq + 2) % 16 <= 16 - nq) ? 2
+         : (((nq * nq + 4) % 16 >= nq && (nq * nq + 4) % 16 <= 16 - nq) ? 4
+         : (((nq * nq + 6) % 16 >= nq && (nq * nq + 6) % 16 <= 16 - nq) ? 6 : 8)));
+}
+
+template <int NQ, int TS, bool DMMA>
+struct ShapeV2 {
+  static constexpr int DIM = 3, M = 5;
+  static constexpr int NS = NQ * NQ * NQ;
+  static constexpr int NF = NQ * NQ;
+  static constexpr int NSP = (NS + 31) / 32 * 32;
+  static constexpr int THREADS = TS * NSP;
+  static constexpr int NWARPS = THREADS / 32;
+  static constexpr int TH = NQ / TS;
+  // CTAs/SM the register allocation must allow (TS = 1 at NQ = 6 keeps 60 doubles of Picard state)
+  static constexpr int MINB = (TS == 1 && NQ >= 6) ? 1
+                            : THREADS <= 64 ? 6 : THREADS <= 128 ? 4 : (THREADS <= 256 ? 2 : 1);
+  static constexpr int P0 = NQ * NQ + plane_pad(NQ);   // padded axis-0 plane stride
+  static constexpr int PS = NQ * P0;                   // padded slice size
+  static constexpr int DS = DMMA ? DIM - 1 : DIM;      // axes through shared memory
+  static constexpr bool F1T = (NQ == 4);               // axis-1 flux stored transposed, 16-byte gathers
+  static constexpr int P1T = NQ * NQ + 2;              // its plane stride (odd number of 16-byte chunks)
+  static constexpr int REC = 2 * NF * M + 2;
+  // shared memory (doubles), all region sizes even (16-byte alignment)
+  static constexpr int R_RED = 2 * NWARPS + 2 * DIM + 4;
+  static constexpr int R_Q = NS * M;
+  static constexpr int R_REC = 4 * DIM * REC;
+  static constexpr int R_F = TS * DS * M * PS;
+  static constexpr int R_FB = DIM * M * PS;            // fbar (after the Picard loop)
+  static constexpr int R_DIV = NQ * M * NSP;           // divergence of all slices / q slices
+  static constexpr int R_PRED = (R_F > R_FB ? R_F : R_FB) + R_DIV;
+  static constexpr int R_U = R_REC > R_PRED ? R_REC : R_PRED;
+  static constexpr int R_FACE = 2 * DIM * NF * M;
+  static constexpr int OFF_BAR = 0;                    // 2 doubles for the mbarrier
+  static constexpr int OFF_RED = 2;
+  static constexpr int OFF_Q = OFF_RED + ((R_RED + 1) & ~1);
+  static constexpr int OFF_D = OFF_Q + R_Q;
+  static constexpr int OFF_U = OFF_D + R_Q;
+  static constexpr int OFF_FACE = OFF_U + R_U;
+  static constexpr int TOTAL = OFF_FACE + R_FACE;
+  static constexpr size_t SMEM_BYTES = sizeof(double) * TOTAL;
+  static_assert((NS * M) % 2 == 0, "bulk copies need 16-byte sizes");
+  static_assert(NQ % TS == 0, "time split must divide NQ");
+  static_assert(!DMMA || NQ == 4, "DMMA axis-2 path needs i2 in lane bits 0-1");
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit_wait() {
+  asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// D = A(8x4) * B(4x8) + C, fp64, one element of A and B per lane.
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b, double c0, double c1) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};\n"
+               : "=d"(d0), "=d"(d1)
+               : "d"(a), "d"(b), "d"(c0), "d"(c1));
+}
+
+template <int NQ, int TS, bool DMMA>
+__global__ void __launch_bounds__(ShapeV2<NQ, TS, DMMA>::THREADS, ShapeV2<NQ, TS, DMMA>::MINB)
+sweep_kernel_v2(const SweepParams P) {
+  using S = ShapeV2<NQ, TS, DMMA>;
+  constexpr int DIM = 3, M = 5, NS = S::NS, NF = S::NF, NSP = S::NSP, REC = S::REC;
+  constexpr int THREADS = S::THREADS, NW = S::NWARPS, TH = S::TH, P0 = S::P0, PS = S::PS;
+  constexpr int DS = S::DS;
+
+  extern __shared__ __align__(16) double smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR);
+  double* sRed = smem + S::OFF_RED;
+  unsigned long long* sSmax = reinterpret_cast<unsigned long long*>(sRed + 2 * NW);
+  double* sQ = smem + S::OFF_Q;
+  double* sD = smem + S::OFF_D;
+  double* sU = smem + S::OFF_U;
+  double* sRec = sU;                                   // corrector phase
+  double* sF = sU;                                     // predictor: [TS][DS][M][PS]
+  double* sDiv = sU + (S::R_F > S::R_FB ? S::R_F : S::R_FB);   // [NQ][M][NSP]
+  double* sFace = smem + S::OFF_FACE;
+
+  DevState* st = P.st;
+  if (st->status != 0) return;
+  const int mode = P.mode;
+  if (mode == MODE_RERUN && !st->rerun_next) return;
+  if (mode == MODE_NORMAL && st->reduce[1] != 0) return;
+
+  const int tid = threadIdx.x;
+  const int ts = tid / NSP;
+  const int x0 = tid % NSP;
+  const bool act = x0 < NS;
+  const int x = act ? x0 : 0;
+  const long long cell = blockIdx.x;
+  const long long gcell = cell + P.cell_offset;
+  const int i0 = x / (NQ * NQ), i1 = (x / NQ) % NQ, i2 = x % NQ;
+  const int px = i0 * P0 + i1 * NQ + i2;              // padded slice index
+
+  const int plane = (int)(cell / P.plane_cells);
+  const int rest = (int)(cell % P.plane_cells);
+  const long long own_slot = (long long)(plane + 1) * P.plane_cells + rest;
+  const int step_idx = (mode == MODE_NORMAL) ? st->step + 1 : 0;
+  double* Qg = P.Q + cell * (NS * M);
+  double* Dg = P.D + cell * (NS * M);
+
+  // ---------------- TMA bulk staging of Q (+ D and the 4d face records) ----------------
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t bytes = NS * M * 8;
+    if (mode == MODE_NORMAL) bytes += NS * M * 8 + 4 * DIM * REC * 8;
+    mbar_arrive_expect_tx(bar, bytes);
+    bulk_g2s(sQ, Qg, NS * M * 8, bar);
+    if (mode == MODE_NORMAL) {
+      bulk_g2s(sD, Dg, NS * M * 8, bar);
+      for (int f = 0; f < 2 * DIM; ++f) {
+        const int a = f >> 1;
+        const int dir = (f & 1) ? 1 : -1;
+        long long nb;
+        if (a == 0) {
+          int pl = plane + dir;
+          if (!P.halo) pl = (pl + P.K) % P.K;
+          nb = (long long)(pl + 1) * P.plane_cells + rest;
+        } else {
+          const int st_a = (a == 1) ? P.K : 1;
+          const int ia = (rest / st_a) % P.K;
+          const int ja = (ia + dir + P.K) % P.K;
+          nb = (long long)(plane + 1) * P.plane_cells + rest + (ja - ia) * st_a;
+        }
+        bulk_g2s(sRec + f * REC, P.tr_in + ((long long)f * P.slots + own_slot) * REC, REC * 8, bar);
+        bulk_g2s(sRec + (2 * DIM + f) * REC, P.tr_in + ((long long)(f ^ 1) * P.slots + nb) * REC, REC * 8,
+                 bar);
+      }
+    }
+  }
+  mbar_wait(bar, 0);
+
+  double Qx[M];
+#pragma unroll
+  for (int c = 0; c < M; ++c) Qx[c] = sQ[x * M + c];
+
+  if (mode == MODE_NORMAL) {
+    // ------------- Riemann (kernels.py:147-179), time-collapsed -------------
+    for (int e = tid; e < 2 * DIM * NF * M; e += THREADS) {
+      const int f = e / (NF * M);
+      const int yc = e % (NF * M);
+      const double* own = sRec + f * REC;
+      const double* nb = sRec + (2 * DIM + f) * REC;
+      const double* mr = (f & 1) ? own : nb;
+      const double* pr = (f & 1) ? nb : own;
+      const double alpha = fmax(mr[2 * NF * M], pr[2 * NF * M]);
+      const double fs = __dsub_rn(__dmul_rn(0.5, __dadd_rn(mr[NF * M + yc], pr[NF * M + yc])),
+                                  __dmul_rn(__dmul_rn(0.5, alpha), __dsub_rn(pr[yc], mr[yc])));
+      sFace[e] = (f & 1) ? fs : -fs;
+    }
+    __syncthreads();
+    // ------------- integrate_face + update (kernels.py:183-214) -------------
+    if (ts == 0 && act) {
+      double Dx[M];
+#pragma unroll
+      for (int c = 0; c < M; ++c) Dx[c] = sD[x * M + c];
+      const double scale_old = st->dt_old / P.h;
+      const int idx[3] = {i0, i1, i2};
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) {
+        const int y = (a == 0) ? i1 * NQ + i2 : (a == 1) ? i0 * NQ + i2 : i0 * NQ + i1;
+        const double slo = __dmul_rn(scale_old, P.ops.lift_lo[idx[a]]);
+        const double shi = __dmul_rn(scale_old, P.ops.lift_hi[idx[a]]);
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          Dx[c] = __dsub_rn(Dx[c], __dmul_rn(slo, sFace[((2 * a) * NF + y) * M + c]));
+          Dx[c] = __dsub_rn(Dx[c], __dmul_rn(shi, sFace[((2 * a + 1) * NF + y) * M + c]));
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < M; ++c) Qx[c] = __dadd_rn(Qx[c], Dx[c]);
+      if (P.spike_step >= 0 && step_idx == P.spike_step) {
+        const double rho = Qx[0];
+        const double pr = pressure_exact<DIM>(Qx);
+#pragma unroll
+        for (int b = 0; b < DIM; ++b) Qx[1 + b] = __dmul_rn(Qx[1 + b], P.spike_factor);
+        double jj = __dmul_rn(Qx[1], Qx[1]);
+#pragma unroll
+        for (int b = 1; b < DIM; ++b) jj = __dadd_rn(jj, __dmul_rn(Qx[1 + b], Qx[1 + b]));
+        Qx[M - 1] = __dadd_rn(__ddiv_rn(pr, 0.4), __ddiv_rn(__dmul_rn(0.5, jj), rho));
+      }
+#pragma unroll
+      for (int c = 0; c < M; ++c) sQ[x * M + c] = Qx[c];
+      fence_proxy_async();
+    }
+    __syncthreads();
+    if (tid == 0) bulk_s2g(Qg, sQ, NS * M * 8);   // committed with the D store below
+    if (ts != 0 || !act) {
+#pragma unroll
+      for (int c = 0; c < M; ++c) Qx[c] = sQ[x * M + c];
+    }
+  }
+
+  if (mode != MODE_RERUN) {
+    // ------------- calc_time_step (kernels.py:216-229) -------------
+    bool ok = true;
+    double lam = 0.0;
+    if (ts == 0 && act) {
+#pragma unroll
+      for (int c = 0; c < M; ++c) ok = ok && finite(Qx[c]);
+      if (ok) {
+        const double pr = pressure_exact<DIM>(Qx);
+        ok = (Qx[0] > ADM_EPS) && (pr > ADM_EPS);
+        if (ok) {
+#pragma unroll
+          for (int a = 0; a < DIM; ++a) lam = fmax(lam, speed_exact<DIM>(Qx, a, pr));
+        }
+      }
+    }
+    if (!__syncthreads_and(ok)) {
+      if (tid == 0) {
+        report_error(st, 2 * gcell + 0);
+        if (mode == MODE_NORMAL) bulk_commit_wait();
+      }
+      return;
+    }
+    lam = block_max<NW>(lam, sRed);
+    if (tid == 0) atomicMax(&st->reduce[0], __double_as_longlong(lam));
+    if (mode == MODE_SEED) return;
+  } else {
+    bool ok = true;
+    if (act) {
+#pragma unroll
+      for (int c = 0; c < M; ++c) ok = ok && finite(Qx[c]);
+    }
+    if (!__syncthreads_and(ok)) {
+      if (tid == 0) report_error(st, 2 * gcell + 1);
+      return;
+    }
+  }
+
+  // ---------------- predictor (kernels.py:68-105) ----------------
+  const double dt = (mode == MODE_RERUN) ? st->dt_old : st->dt_new;
+  const double scale = dt / P.h;
+  double absmax;
+  {
+    double am = 0.0;
+#pragma unroll
+    for (int c = 0; c < M; ++c) am = fmax(am, fabs(Qx[c]));
+    absmax = block_max<NW>(act ? am : 0.0, sRed);
+  }
+  const double tol = 1e-10 * (1.0 + absmax);
+  const int cap = 2 * NQ;
+
+  // derivative rows of the shared-memory axes; DMMA B fragment for axis 2
+  double drow[DS][NQ];
+  {
+    const int idx[3] = {i0, i1, i2};
+#pragma unroll
+    for (int a = 0; a < DS; ++a)
+#pragma unroll
+      for (int j = 0; j < NQ; ++j) drow[a][j] = P.ops.diff[idx[a]][j];
+  }
+  double bfrag = 0.0;
+  if (DMMA) {
+    const int lane = tid & 31;
+    const int g = lane >> 2, t4 = lane & 3;      // B[k=t4][n=g]: n even -> diff[n/2][k]
+    bfrag = (g & 1) ? 0.0 : P.ops.diff[g >> 1][t4];
+  }
+  // padded gather bases for the shared-memory axes
+  int gbase[DIM], gstr[DIM];
+  gbase[0] = px - i0 * P0; gstr[0] = P0;
+  gbase[1] = px - i1 * NQ; gstr[1] = NQ;
+  gbase[2] = px - i2;      gstr[2] = 1;
+  // F1T: axis-1 flux stored with i1 fastest (plane stride P1T), gathered as
+  // 16-byte pairs; 8 distinct 16-byte chunks per warp -> one wavefront.
+  const int p1t = i0 * S::P1T + i2 * NQ + i1;
+  const int g1t = i0 * S::P1T + i2 * NQ;
+
+  double q[TH][M];
+#pragma unroll
+  for (int s = 0; s < TH; ++s)
+#pragma unroll
+    for (int c = 0; c < M; ++c) q[s][c] = Qx[c];
+
+  double* sFt = sF + ts * (DS * M * PS);
+  int iters = 0;
+  bool failed = false;
+  for (int it = 0; it < cap; ++it) {
+    double accr[TS == 1 ? NQ : 1][M];           // register time contraction (TS == 1)
+    if (TS == 1) {
+#pragma unroll
+      for (int t = 0; t < (TS == 1 ? NQ : 1); ++t)
+#pragma unroll
+        for (int c = 0; c < M; ++c) accr[t][c] = 0.0;
+    }
+#pragma unroll
+    for (int s = 0; s < TH; ++s) {
+      const int k = ts * TH + s;
+      double F[DIM][M];
+      flux<DIM>(q[s], F);
+      if (act) {
+#pragma unroll
+        for (int a = 0; a < DS; ++a)
+#pragma unroll
+          for (int c = 0; c < M; ++c)
+            sFt[(a * M + c) * PS + ((S::F1T && a == 1) ? p1t : px)] = F[a][c];
+      }
+      __syncthreads();
+      double dv[M];
+#pragma unroll
+      for (int c = 0; c < M; ++c) {
+        double part[DS];
+#pragma unroll
+        for (int a = 0; a < DS; ++a) {
+          double v = 0.0;
+          if (S::F1T && a == 1) {
+            const double2* b2 = reinterpret_cast<const double2*>(sFt + (a * M + c) * PS + g1t);
+#pragma unroll
+            for (int jj = 0; jj < NQ / 2; ++jj) {
+              const double2 w2 = b2[jj];
+              v = fma(drow[a][2 * jj], w2.x, v);
+              v = fma(drow[a][2 * jj + 1], w2.y, v);
+            }
+          } else {
+            const double* b = sFt + (a * M + c) * PS + gbase[a];
+#pragma unroll
+            for (int j = 0; j < NQ; ++j) v = fma(drow[a][j], b[j * gstr[a]], v);
+          }
+          part[a] = v;
+        }
+        double sum = part[0];
+#pragma unroll
+        for (int a = 1; a < DS; ++a) sum += part[a];
+        dv[c] = sum;
+      }
+      if (DMMA) {
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          double d1;
+          dmma_8x8x4(dv[c], d1, F[2][c], bfrag, dv[c], 0.0);
+        }
+      }
+      if (TS == 1) {
+#pragma unroll
+        for (int t = 0; t < (TS == 1 ? NQ : 1); ++t)
+#pragma unroll
+          for (int c = 0; c < M; ++c) accr[t][c] = fma(P.ops.integ[t][k], dv[c], accr[t][c]);
+      } else if (act) {
+#pragma unroll
+        for (int c = 0; c < M; ++c) sDiv[(k * M + c) * NSP + x] = dv[c];
+      }
+      __syncthreads();
+    }
+    // time contraction (integ) for the owned time levels, then the Picard update
+    double dmax = 0.0;
+    bool bad = false;
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+      double dvk[NQ];
+      if (TS > 1) {
+#pragma unroll
+        for (int k = 0; k < NQ; ++k) dvk[k] = sDiv[(k * M + c) * NSP + x];
+      }
+#pragma unroll
+      for (int s = 0; s < TH; ++s) {
+        const int t = ts * TH + s;
+        double acc = 0.0;
+        if (TS == 1) {
+          acc = accr[TS == 1 ? s : 0][c];
+        } else {
+#pragma unroll
+          for (int k = 0; k < NQ; ++k) acc = fma(P.ops.integ[t][k], dvk[k], acc);
+        }
+        const double qn = Qx[c] - scale * acc;
+        const double dd = fabs(qn - q[s][c]);
+        bad |= !(dd <= 1.7976931348623157e308);
+        dmax = fmax(dmax, dd);
+        q[s][c] = qn;
+      }
+    }
+    iters = it + 1;
+    if (__syncthreads_or(act && bad)) { failed = true; break; }
+    const double delta = block_max<NW>(act ? dmax : 0.0, sRed);
+    if (delta <= tol) break;
+  }
+
+  // final flux: time average of the owned levels (partial fbar) + finiteness
+  double fb[DIM][M];
+#pragma unroll
+  for (int a = 0; a < DIM; ++a)
+#pragma unroll
+    for (int c = 0; c < M; ++c) fb[a][c] = 0.0;
+  if (!failed) {
+    bool bad = false;
+#pragma unroll
+    for (int s = 0; s < TH; ++s) {
+      const int t = ts * TH + s;
+      double F[DIM][M];
+      flux<DIM>(q[s], F);
+#pragma unroll
+      for (int a = 0; a < DIM; ++a)
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          bad |= !finite(F[a][c]);
+          fb[a][c] = fma(P.ops.w[t], F[a][c], fb[a][c]);
+        }
+    }
+    failed = __syncthreads_or(act && bad);
+  }
+  if (failed) {
+    if (tid == 0) {
+      report_error(st, 2 * gcell + 1);
+      if (mode == MODE_NORMAL) bulk_commit_wait();
+    }
+    return;
+  }
+  if (tid == 0) {
+    atomicAdd((unsigned long long*)&st->picard_iters, (unsigned long long)iters);
+    atomicAdd((unsigned long long*)&st->predicts, 1ull);
+    atomicAdd((unsigned long long*)&st->hist[iters < HIST_BINS ? iters : HIST_BINS - 1], 1ull);
+  }
+
+  // all time levels of q into sDiv's region: [t][c][NSP]  (for s_max and qbar)
+  double* sQt = sDiv;
+  double* sFb = sF;                                    // [DIM][M][PS] total fbar
+  if (act) {
+#pragma unroll
+    for (int s = 0; s < TH; ++s)
+#pragma unroll
+      for (int c = 0; c < M; ++c) sQt[((ts * TH + s) * M + c) * NSP + x] = q[s][c];
+  }
+  // fbar = sum over the TS partial time averages
+  if (TS > 1) {
+    if (ts == 1 && act) {
+#pragma unroll
+      for (int a = 0; a < DIM; ++a)
+#pragma unroll
+        for (int c = 0; c < M; ++c) sFb[(a * M + c) * PS + px] = fb[a][c];
+    }
+    __syncthreads();
+    if (ts == 0 && act) {
+#pragma unroll
+      for (int a = 0; a < DIM; ++a)
+#pragma unroll
+        for (int c = 0; c < M; ++c) fb[a][c] += sFb[(a * M + c) * PS + px];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 2; r < TS; ++r) {
+      if (ts == r && act) {
+#pragma unroll
+        for (int a = 0; a < DIM; ++a)
+#pragma unroll
+          for (int c = 0; c < M; ++c) sFb[(a * M + c) * PS + px] = fb[a][c];
+      }
+      __syncthreads();
+      if (ts == 0 && act) {
+#pragma unroll
+        for (int a = 0; a < DIM; ++a)
+#pragma unroll
+          for (int c = 0; c < M; ++c) fb[a][c] += sFb[(a * M + c) * PS + px];
+      }
+      __syncthreads();
+    }
+  }
+  if (ts == 0 && act) {
+#pragma unroll
+    for (int a = 0; a < DIM; ++a)
+#pragma unroll
+      for (int c = 0; c < M; ++c) sFb[(a * M + c) * PS + px] = fb[a][c];
+  }
+  if (tid < 2 * DIM) sSmax[tid] = 0ull;
+  __syncthreads();
+
+  // ---------------- integrate_volume (kernels.py:130-143) ----------------
+  if (ts == 0 && act) {
+    const double sdt = dt / P.h;
+    const int idx[3] = {i0, i1, i2};
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+      double s = 0.0;
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) {
+        const double* b = sFb + (a * M + c) * PS + gbase[a];
+#pragma unroll
+        for (int j = 0; j < NQ; ++j) s = fma(P.ops.kvol[idx[a]][j], b[j * gstr[a]], s);
+      }
+      sD[x * M + c] = s * sdt;
+    }
+    fence_proxy_async();
+  }
+
+  // ---------------- s_max over the space-time face traces ----------------
+  for (int e = tid; e < 2 * DIM * NF * NQ; e += THREADS) {
+    const int t = e / (2 * DIM * NF);
+    const int fy = e % (2 * DIM * NF);
+    const int f = fy / NF, y = fy % NF, a = f >> 1;
+    const double* vec = (f & 1) ? P.ops.right : P.ops.left;
+    const int ya = y / NQ, yb = y % NQ;
+    int xb, sta;
+    if (a == 0) { xb = ya * NQ + yb; sta = NQ * NQ; }
+    else if (a == 1) { xb = ya * NQ * NQ + yb; sta = NQ; }
+    else { xb = ya * NQ * NQ + yb * NQ; sta = 1; }
+    double qs[M];
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+      double v = 0.0;
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) v = fma(vec[i], sQt[(t * M + c) * NSP + xb + i * sta], v);
+      qs[c] = v;
+    }
+    const double pr = pressure_exact<DIM>(qs);
+    const double sp = speed_exact<DIM>(qs, a, pr);
+    atomicMax(&sSmax[f], (unsigned long long)__double_as_longlong(sp));
+  }
+  __syncthreads();
+  if (tid == 0) {
+    bulk_s2g(Dg, sD, NS * M * 8);
+    bulk_commit_wait();   // also covers the Q store issued in the corrector
+  }
+  // ---------------- face records: qbar and fbar traces ----------------
+  for (int e = tid; e < 2 * DIM * NF * M; e += THREADS) {
+    const int f = e / (NF * M), yc = e % (NF * M), y = yc / M, c = yc % M, a = f >> 1;
+    const double* vec = (f & 1) ? P.ops.right : P.ops.left;
+    const int ya = y / NQ, yb = y % NQ;
+    int xb, sta, pxb, psta;
+    if (a == 0) { xb = ya * NQ + yb; sta = NQ * NQ; pxb = ya * NQ + yb; psta = P0; }
+    else if (a == 1) { xb = ya * NQ * NQ + yb; sta = NQ; pxb = ya * P0 + yb; psta = NQ; }
+    else { xb = ya * NQ * NQ + yb * NQ; sta = 1; pxb = ya * P0 + yb * NQ; psta = 1; }
+    double vq = 0.0, vf = 0.0;
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) {
+      double qb = 0.0;
+#pragma unroll
+      for (int t = 0; t < NQ; ++t) qb = fma(P.ops.w[t], sQt[(t * M + c) * NSP + xb + i * sta], qb);
+      vq = fma(vec[i], qb, vq);
+      vf = fma(vec[i], sFb[(a * M + c) * PS + pxb + i * psta], vf);
+    }
+    double* rec = P.tr_out + ((long long)f * P.slots + own_slot) * REC;
+    rec[yc] = vq;
+    rec[NF * M + yc] = vf;
+  }
+  if (tid < 2 * DIM) {
+    double* rec = P.tr_out + ((long long)tid * P.slots + own_slot) * REC;
+    rec[2 * NF * M] = __longlong_as_double((long long)sSmax[tid]);
+    rec[2 * NF * M + 1] = 0.0;
+  }
+}
+
+}  // namespace adg
