@@ -56,7 +56,7 @@ struct ShapeV2 {
   static constexpr int R_REC = 4 * DIM * REC;
   static constexpr int R_F = TS * DS * M * PS;
   static constexpr int R_FB = DIM * M * PS;            // fbar (after the Picard loop)
-  static constexpr int R_DIV = NQ * M * NSP;           // divergence of all slices / q slices
+  static constexpr int R_DIV = (NQ + 1) * M * NSP;     // divergence of all slices / q slices + qbar
   static constexpr int R_PRED = (R_F > R_FB ? R_F : R_FB) + R_DIV;
   static constexpr int R_U = R_REC > R_PRED ? R_REC : R_PRED;
   static constexpr int R_FACE = 2 * DIM * NF * M;
@@ -125,6 +125,16 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};\n"
                : "=d"(d0), "=d"(d1)
                : "d"(a), "d"(b), "d"(c0), "d"(c1));
+}
+
+// Node address in the trace-phase q layout.  NQ = 4: Latin-cube swizzle
+// 16*i2 + 4*((i0+i2)&3) + ((i1+i2)&3): for every axis, the 16 nodes of a face
+// plane hit 16 distinct 8-byte banks, so the face-trace gathers of a
+// half-warp are conflict free along all three axes.
+template <int NQ>
+__device__ __forceinline__ int trace_addr(int i0, int i1, int i2) {
+  if (NQ == 4) return 16 * i2 + 4 * ((i0 + i2) & 3) + ((i1 + i2) & 3);
+  return (i0 * NQ + i1) * NQ + i2;
 }
 
 template <int NQ, int TS, bool DMMA>
@@ -353,12 +363,6 @@ sweep_kernel_v2(const SweepParams P) {
   bool failed = false;
   for (int it = 0; it < cap; ++it) {
     double accr[TS == 1 ? NQ : 1][M];           // register time contraction (TS == 1)
-    if (TS == 1) {
-#pragma unroll
-      for (int t = 0; t < (TS == 1 ? NQ : 1); ++t)
-#pragma unroll
-        for (int c = 0; c < M; ++c) accr[t][c] = 0.0;
-    }
 #pragma unroll
     for (int s = 0; s < TH; ++s) {
       const int k = ts * TH + s;
@@ -410,16 +414,18 @@ sweep_kernel_v2(const SweepParams P) {
 #pragma unroll
         for (int t = 0; t < (TS == 1 ? NQ : 1); ++t)
 #pragma unroll
-          for (int c = 0; c < M; ++c) accr[t][c] = fma(P.ops.integ[t][k], dv[c], accr[t][c]);
+          for (int c = 0; c < M; ++c)
+            accr[t][c] = (k == 0) ? P.ops.integ[t][0] * dv[c] : fma(P.ops.integ[t][k], dv[c], accr[t][c]);
       } else if (act) {
 #pragma unroll
         for (int c = 0; c < M; ++c) sDiv[(k * M + c) * NSP + x] = dv[c];
       }
       __syncthreads();
     }
-    // time contraction (integ) for the owned time levels, then the Picard update
-    double dmax = 0.0;
-    bool bad = false;
+    // time contraction (integ) for the owned time levels, then the Picard update.
+    // max |q_new - q| via the bit patterns of non-negative doubles (NaN/inf
+    // patterns sort above every finite value): one integer max per node.
+    unsigned long long dbits = 0ull;
 #pragma unroll
     for (int c = 0; c < M; ++c) {
       double dvk[NQ];
@@ -438,15 +444,15 @@ sweep_kernel_v2(const SweepParams P) {
           for (int k = 0; k < NQ; ++k) acc = fma(P.ops.integ[t][k], dvk[k], acc);
         }
         const double qn = Qx[c] - scale * acc;
-        const double dd = fabs(qn - q[s][c]);
-        bad |= !(dd <= 1.7976931348623157e308);
-        dmax = fmax(dmax, dd);
+        const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(qn - q[s][c]));
+        dbits = b > dbits ? b : dbits;
         q[s][c] = qn;
       }
     }
     iters = it + 1;
+    const bool bad = dbits >= 0x7ff0000000000000ull;      // inf or NaN
     if (__syncthreads_or(act && bad)) { failed = true; break; }
-    const double delta = block_max<NW>(act ? dmax : 0.0, sRed);
+    const double delta = block_max<NW>(act ? __longlong_as_double((long long)dbits) : 0.0, sRed);
     if (delta <= tol) break;
   }
 
@@ -486,14 +492,16 @@ sweep_kernel_v2(const SweepParams P) {
     atomicAdd((unsigned long long*)&st->hist[iters < HIST_BINS ? iters : HIST_BINS - 1], 1ull);
   }
 
-  // all time levels of q into sDiv's region: [t][c][NSP]  (for s_max and qbar)
+  // all time levels of q into sDiv's region: [t][c][NSP] in the trace layout
   double* sQt = sDiv;
+  double* sQb = sDiv + NQ * M * NSP;                   // qbar [c][NSP] (trace layout)
   double* sFb = sF;                                    // [DIM][M][PS] total fbar
+  const int qax = trace_addr<NQ>(i0, i1, i2);
   if (act) {
 #pragma unroll
     for (int s = 0; s < TH; ++s)
 #pragma unroll
-      for (int c = 0; c < M; ++c) sQt[((ts * TH + s) * M + c) * NSP + x] = q[s][c];
+      for (int c = 0; c < M; ++c) sQt[((ts * TH + s) * M + c) * NSP + qax] = q[s][c];
   }
   // fbar = sum over the TS partial time averages
   if (TS > 1) {
@@ -556,23 +564,35 @@ sweep_kernel_v2(const SweepParams P) {
     fence_proxy_async();
   }
 
+  // qbar = sum_t w_t q_t per node (trace layout)
+  if (ts == 0 && act) {
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+      double v = 0.0;
+#pragma unroll
+      for (int t = 0; t < NQ; ++t) v = fma(P.ops.w[t], sQt[(t * M + c) * NSP + qax], v);
+      sQb[c * NSP + qax] = v;
+    }
+  }
+
   // ---------------- s_max over the space-time face traces ----------------
+  // task = (face f, time t, face node y), y fastest: a half-warp gathers one face plane
   for (int e = tid; e < 2 * DIM * NF * NQ; e += THREADS) {
-    const int t = e / (2 * DIM * NF);
-    const int fy = e % (2 * DIM * NF);
-    const int f = fy / NF, y = fy % NF, a = f >> 1;
+    const int y = e % NF;
+    const int ft = e / NF;
+    const int f = ft / NQ, t = ft % NQ, a = f >> 1;
     const double* vec = (f & 1) ? P.ops.right : P.ops.left;
     const int ya = y / NQ, yb = y % NQ;
-    int xb, sta;
-    if (a == 0) { xb = ya * NQ + yb; sta = NQ * NQ; }
-    else if (a == 1) { xb = ya * NQ * NQ + yb; sta = NQ; }
-    else { xb = ya * NQ * NQ + yb * NQ; sta = 1; }
     double qs[M];
 #pragma unroll
     for (int c = 0; c < M; ++c) {
       double v = 0.0;
 #pragma unroll
-      for (int i = 0; i < NQ; ++i) v = fma(vec[i], sQt[(t * M + c) * NSP + xb + i * sta], v);
+      for (int i = 0; i < NQ; ++i) {
+        const int ad = (a == 0) ? trace_addr<NQ>(i, ya, yb)
+                     : (a == 1) ? trace_addr<NQ>(ya, i, yb) : trace_addr<NQ>(ya, yb, i);
+        v = fma(vec[i], sQt[(t * M + c) * NSP + ad], v);
+      }
       qs[c] = v;
     }
     const double pr = pressure_exact<DIM>(qs);
@@ -586,25 +606,26 @@ sweep_kernel_v2(const SweepParams P) {
   }
   // ---------------- face records: qbar and fbar traces ----------------
   for (int e = tid; e < 2 * DIM * NF * M; e += THREADS) {
-    const int f = e / (NF * M), yc = e % (NF * M), y = yc / M, c = yc % M, a = f >> 1;
+    const int y = e % NF;
+    const int fc = e / NF;
+    const int f = fc / M, c = fc % M, a = f >> 1;
     const double* vec = (f & 1) ? P.ops.right : P.ops.left;
     const int ya = y / NQ, yb = y % NQ;
-    int xb, sta, pxb, psta;
-    if (a == 0) { xb = ya * NQ + yb; sta = NQ * NQ; pxb = ya * NQ + yb; psta = P0; }
-    else if (a == 1) { xb = ya * NQ * NQ + yb; sta = NQ; pxb = ya * P0 + yb; psta = NQ; }
-    else { xb = ya * NQ * NQ + yb * NQ; sta = 1; pxb = ya * P0 + yb * NQ; psta = 1; }
+    int pxb, psta;
+    if (a == 0) { pxb = ya * NQ + yb; psta = P0; }
+    else if (a == 1) { pxb = ya * P0 + yb; psta = NQ; }
+    else { pxb = ya * P0 + yb * NQ; psta = 1; }
     double vq = 0.0, vf = 0.0;
 #pragma unroll
     for (int i = 0; i < NQ; ++i) {
-      double qb = 0.0;
-#pragma unroll
-      for (int t = 0; t < NQ; ++t) qb = fma(P.ops.w[t], sQt[(t * M + c) * NSP + xb + i * sta], qb);
-      vq = fma(vec[i], qb, vq);
+      const int ad = (a == 0) ? trace_addr<NQ>(i, ya, yb)
+                   : (a == 1) ? trace_addr<NQ>(ya, i, yb) : trace_addr<NQ>(ya, yb, i);
+      vq = fma(vec[i], sQb[c * NSP + ad], vq);
       vf = fma(vec[i], sFb[(a * M + c) * PS + pxb + i * psta], vf);
     }
     double* rec = P.tr_out + ((long long)f * P.slots + own_slot) * REC;
-    rec[yc] = vq;
-    rec[NF * M + yc] = vf;
+    rec[y * M + c] = vq;
+    rec[NF * M + y * M + c] = vf;
   }
   if (tid < 2 * DIM) {
     double* rec = P.tr_out + ((long long)tid * P.slots + own_slot) * REC;
