@@ -47,7 +47,8 @@ struct ShapeV2 {
   static constexpr int P0 = NQ * NQ + plane_pad(NQ);   // padded axis-0 plane stride
   static constexpr int PS = NQ * P0;                   // padded slice size
   static constexpr int DS = DMMA ? DIM - 1 : DIM;      // axes through shared memory
-  static constexpr bool F1T = (NQ == 4);               // axis-1 flux stored transposed, 16-byte gathers
+  static constexpr bool F1T = (NQ == 4);
+  static constexpr bool ROLL = (NQ == 4);              // rolled slice loop (i-cache); NQ = 6 stays unrolled               // axis-1 flux stored transposed, 16-byte gathers
   static constexpr int P1T = NQ * NQ + 2;              // its plane stride (odd number of 16-byte chunks)
   static constexpr int REC = 2 * NF * M + 2;
   // shared memory (doubles), all region sizes even (16-byte alignment)
@@ -361,8 +362,100 @@ sweep_kernel_v2(const SweepParams P) {
   double* sFt = sF + ts * (DS * M * PS);
   int iters = 0;
   bool failed = false;
+  if constexpr (TS == 1 && S::ROLL) {
+    // Rolled slice loop (keeps the Picard loop inside the instruction cache):
+    // the slice being processed is always q[0]; the time line rotates by one
+    // register slot per slice and is back in order after NQ slices.
+#pragma unroll 1
+    for (int it = 0; it < cap; ++it) {
+      double acc[NQ][M];
+#pragma unroll
+      for (int t = 0; t < NQ; ++t)
+#pragma unroll
+        for (int c = 0; c < M; ++c) acc[t][c] = 0.0;
+#pragma unroll 1
+      for (int k = 0; k < NQ; ++k) {
+      double F[DIM][M];
+      flux<DIM>(q[0], F);
+      if (act) {
+#pragma unroll
+        for (int a = 0; a < DS; ++a)
+#pragma unroll
+          for (int c = 0; c < M; ++c)
+            sFt[(a * M + c) * PS + ((S::F1T && a == 1) ? p1t : px)] = F[a][c];
+      }
+      __syncthreads();
+      double dv[M];
+#pragma unroll
+      for (int c = 0; c < M; ++c) {
+        double part[DS];
+#pragma unroll
+        for (int a = 0; a < DS; ++a) {
+          double v = 0.0;
+          if (S::F1T && a == 1) {
+            const double2* b2 = reinterpret_cast<const double2*>(sFt + (a * M + c) * PS + g1t);
+#pragma unroll
+            for (int jj = 0; jj < NQ / 2; ++jj) {
+              const double2 w2 = b2[jj];
+              v = fma(drow[a][2 * jj], w2.x, v);
+              v = fma(drow[a][2 * jj + 1], w2.y, v);
+            }
+          } else {
+            const double* b = sFt + (a * M + c) * PS + gbase[a];
+#pragma unroll
+            for (int j = 0; j < NQ; ++j) v = fma(drow[a][j], b[j * gstr[a]], v);
+          }
+          part[a] = v;
+        }
+        double sum = part[0];
+#pragma unroll
+        for (int a = 1; a < DS; ++a) sum += part[a];
+        dv[c] = sum;
+      }
+      if (DMMA) {
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          double d1;
+          dmma_8x8x4(dv[c], d1, F[2][c], bfrag, dv[c], 0.0);
+        }
+      }
+        double icol[NQ];
+#pragma unroll
+        for (int t = 0; t < NQ; ++t) icol[t] = P.ops.integ[t][k];
+#pragma unroll
+        for (int t = 0; t < NQ; ++t)
+#pragma unroll
+          for (int c = 0; c < M; ++c) acc[t][c] = fma(icol[t], dv[c], acc[t][c]);
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          const double q0 = q[0][c];
+#pragma unroll
+          for (int t = 0; t + 1 < NQ; ++t) q[t][c] = q[t + 1][c];
+          q[NQ - 1][c] = q0;
+        }
+        __syncthreads();
+      }
+      // Picard update; max |q_new - q| via the bit patterns of non-negative
+      // doubles (NaN/inf patterns sort above every finite value)
+      unsigned long long dbits = 0ull;
+#pragma unroll
+      for (int t = 0; t < NQ; ++t)
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          const double qn = Qx[c] - scale * acc[t][c];
+          const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(qn - q[t][c]));
+          dbits = b > dbits ? b : dbits;
+          q[t][c] = qn;
+        }
+      iters = it + 1;
+      const bool bad = dbits >= 0x7ff0000000000000ull;
+      if (__syncthreads_or(act && bad)) { failed = true; break; }
+      const double delta = block_max<NW>(act ? __longlong_as_double((long long)dbits) : 0.0, sRed);
+      if (delta <= tol) break;
+    }
+  } else {
   for (int it = 0; it < cap; ++it) {
-    double accr[TS == 1 ? NQ : 1][M];           // register time contraction (TS == 1)
+    double accr[TS == 1 ? NQ : 1][M];            // register time contraction (TS == 1)
 #pragma unroll
     for (int s = 0; s < TH; ++s) {
       const int k = ts * TH + s;
@@ -422,9 +515,6 @@ sweep_kernel_v2(const SweepParams P) {
       }
       __syncthreads();
     }
-    // time contraction (integ) for the owned time levels, then the Picard update.
-    // max |q_new - q| via the bit patterns of non-negative doubles (NaN/inf
-    // patterns sort above every finite value): one integer max per node.
     unsigned long long dbits = 0ull;
 #pragma unroll
     for (int c = 0; c < M; ++c) {
@@ -450,10 +540,11 @@ sweep_kernel_v2(const SweepParams P) {
       }
     }
     iters = it + 1;
-    const bool bad = dbits >= 0x7ff0000000000000ull;      // inf or NaN
+    const bool bad = dbits >= 0x7ff0000000000000ull;
     if (__syncthreads_or(act && bad)) { failed = true; break; }
     const double delta = block_max<NW>(act ? __longlong_as_double((long long)dbits) : 0.0, sRed);
     if (delta <= tol) break;
+  }
   }
 
   // final flux: time average of the owned levels (partial fbar) + finiteness

@@ -39,11 +39,14 @@ class HaloExchange:
 
     Works on any torch tensors (CUDA with NCCL, CPU with gloo for tests)."""
 
-    def __init__(self, planes_local, plane_cells, rank, world, group=None):
+    def __init__(self, planes_local, plane_cells, rank, world, group=None, staged=False):
         self.Pl, self.plane = planes_local, plane_cells
         self.rank, self.world, self.group = rank, world, group
         self.prev = (rank - 1) % world
         self.next = (rank + 1) % world
+        # staged: device tensors go through host copies (gloo transport; used to
+        # test the multi-slab device path with several ranks on one GPU)
+        self.staged = staged
 
     def views(self, tr):
         """tr: tensor (2d, slots, REC).  Returns (send_to_prev, recv_from_prev,
@@ -60,6 +63,10 @@ class HaloExchange:
         if self.world == 1:
             return
         send_prev, recv_prev, send_next, recv_next = self.views(tr)
+        if self.staged:
+            dev_recv = (recv_prev, recv_next)
+            send_prev, send_next = send_prev.cpu(), send_next.cpu()
+            recv_prev, recv_next = recv_prev.cpu(), recv_next.cpu()
         # order matters when prev == next (world 2): messages between one pair
         # are matched in issue order, so every rank sends "to next" first.
         ops = [dist.P2POp(dist.isend, send_next, self.next, self.group),
@@ -68,11 +75,19 @@ class HaloExchange:
                dist.P2POp(dist.irecv, recv_next, self.next, self.group)]
         for r in dist.batch_isend_irecv(ops):
             r.wait()
+        if self.staged:
+            dev_recv[0].copy_(recv_prev)
+            dev_recv[1].copy_(recv_next)
 
     def reduce(self, red):
         """red: int64[2] = {lambda bits, INT64_MAX - error key}; MAX over ranks."""
         import torch.distributed as dist
         if self.world == 1:
+            return
+        if self.staged:
+            host = red.cpu()
+            dist.all_reduce(host, op=dist.ReduceOp.MAX, group=self.group)
+            red.copy_(host)
             return
         dist.all_reduce(red, op=dist.ReduceOp.MAX, group=self.group)
 
@@ -87,7 +102,7 @@ class SlabDriver:
 
     def __init__(self, Q_global, d, L, p, rank, world, device, cfl=0.9, c_dt=0.99,
                  averaging="strict", forced_dt=None, inject_rerun=False,
-                 spike_step=None, spike_factor=3.0, group=None):
+                 spike_step=None, spike_factor=3.0, group=None, staged=False):
         import torch
         from .basis import make_basis
         from .solver import upload_operators
@@ -113,7 +128,7 @@ class SlabDriver:
         plane0, planes = slab_partition(K, world, rank)
         assert planes == lay.planes_local and plane0 * lay.plane_cells == lay.cell_offset
         self.cell_offset, self.n_local = lay.cell_offset, lay.n_cells_local
-        self.halo = HaloExchange(lay.planes_local, lay.plane_cells, rank, world, group)
+        self.halo = HaloExchange(lay.planes_local, lay.plane_cells, rank, world, group, staged)
         slots = (lay.planes_local + 2) * lay.plane_cells
         shape = (lay.faces_per_cell, slots, lay.record_doubles)
         self.tr = []
