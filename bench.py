@@ -43,6 +43,14 @@ CONFIGS = {
                  desc="BASELINE cfg2: 3D Euler p=3, 27^3 periodic, bump+1e-3 noise, 20 steps"),
     "cfg3_p5": dict(d=3, L=3, p=5, scenario="bump", steps=10,
                     desc="BASELINE cfg3: 3D Euler p=5, 27^3 periodic, bump+1e-3 noise, 10 steps"),
+    # p = 7 / 9 with the specified noise blow up in the reference itself (NumericalError at
+    # step 7 / step 5): timed on the steps before the abort
+    "cfg3_p7": dict(d=3, L=3, p=7, scenario="bump", steps=6,
+                    desc="BASELINE cfg3: 3D Euler p=7, 27^3 periodic, bump+1e-3 noise (6 pre-abort steps)"),
+    "cfg3_p9": dict(d=3, L=3, p=9, scenario="bump", steps=4,
+                    desc="BASELINE cfg3: 3D Euler p=9, 27^3 periodic, bump+1e-3 noise (4 pre-abort steps)"),
+    "cfg5_1gpu": dict(d=3, L=4, p=9, scenario="fourier", steps=5,
+                      desc="BASELINE cfg5: 3D Euler p=9, 81^3 periodic, random Fourier state, 5 steps"),
     "cfg4": dict(d=3, L=4, p=5, scenario="bump", steps=10,
                  desc="BASELINE cfg4: 3D Euler p=5, 81^3 periodic, bump+1e-3 noise, 10 steps"),
 }

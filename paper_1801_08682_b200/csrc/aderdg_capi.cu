@@ -97,6 +97,12 @@ bool dispatch_for(int d, int p, Dispatch* out) {
         *out = kernel_variant() == 1 ? make_dispatch<3, 6>()
              : kernel_variant() == 2 ? make_dispatch_v2<6, 2, false>() : make_dispatch_v2<6, 1, false>();
         return true;
+      // p >= 6: the space-time line no longer fits the register file at one
+      // thread per node; the per-thread arrays live in (L1/L2-backed) local memory
+      case 7: *out = make_dispatch<3, 7>(); return true;
+      case 8: *out = make_dispatch<3, 8>(); return true;
+      case 9: *out = make_dispatch<3, 9>(); return true;
+      case 10: *out = make_dispatch<3, 10>(); return true;
     }
   }
   return false;
