@@ -47,8 +47,9 @@ struct ShapeV2 {
   static constexpr int P0 = NQ * NQ + plane_pad(NQ);   // padded axis-0 plane stride
   static constexpr int PS = NQ * P0;                   // padded slice size
   static constexpr int DS = DMMA ? DIM - 1 : DIM;      // axes through shared memory
-  static constexpr bool F1T = (NQ == 4);
-  static constexpr bool ROLL = (NQ == 4);              // rolled slice loop (i-cache); NQ = 6 stays unrolled               // axis-1 flux stored transposed, 16-byte gathers
+  static constexpr bool F1T = (NQ == 4);               // axis-1 flux stored transposed, 16-byte gathers
+  static constexpr bool ROLL = (NQ == 4);              // rolled slice loop (i-cache); NQ = 6 stays unrolled
+  static constexpr int RR = 1;                         // slices per rolled trip
   static constexpr int P1T = NQ * NQ + 2;              // its plane stride (odd number of 16-byte chunks)
   static constexpr int REC = 2 * NF * M + 2;
   // shared memory (doubles), all region sizes even (16-byte alignment)
@@ -58,7 +59,8 @@ struct ShapeV2 {
   static constexpr int R_F = TS * DS * M * PS;
   static constexpr int R_FB = DIM * M * PS;            // fbar (after the Picard loop)
   static constexpr int R_DIV = (NQ + 1) * M * NSP;     // divergence of all slices / q slices + qbar
-  static constexpr int R_PRED = (R_F > R_FB ? R_F : R_FB) + R_DIV;
+  static constexpr int R_PRED0 = (R_F > R_FB ? R_F : R_FB) + R_DIV;
+  static constexpr int R_PRED = (TS == 1 && ROLL && 2 * R_F > R_PRED0) ? 2 * R_F : R_PRED0;
   static constexpr int R_U = R_REC > R_PRED ? R_REC : R_PRED;
   static constexpr int R_FACE = 2 * DIM * NF * M;
   static constexpr int OFF_BAR = 0;                    // 2 doubles for the mbarrier
@@ -284,14 +286,10 @@ sweep_kernel_v2(const SweepParams P) {
     if (ts == 0 && act) {
 #pragma unroll
       for (int c = 0; c < M; ++c) ok = ok && finite(Qx[c]);
-      if (ok) {
-        const double pr = pressure_exact<DIM>(Qx);
-        ok = (Qx[0] > ADM_EPS) && (pr > ADM_EPS);
-        if (ok) {
-#pragma unroll
-          for (int a = 0; a < DIM; ++a) lam = fmax(lam, speed_exact<DIM>(Qx, a, pr));
-        }
-      }
+      bool adm = false;
+      lam = max_speed_fast<DIM>(Qx, 0, DIM, adm);
+      ok = ok && adm;
+      if (!ok) lam = 0.0;
     }
     if (!__syncthreads_and(ok)) {
       if (tid == 0) {
@@ -364,8 +362,8 @@ sweep_kernel_v2(const SweepParams P) {
   bool failed = false;
   if constexpr (TS == 1 && S::ROLL) {
     // Rolled slice loop (keeps the Picard loop inside the instruction cache):
-    // the slice being processed is always q[0]; the time line rotates by one
-    // register slot per slice and is back in order after NQ slices.
+    // each trip processes RR slices from register slots 0..RR-1, then the
+    // time line rotates by RR slots (back in order after NQ slices).
 #pragma unroll 1
     for (int it = 0; it < cap; ++it) {
       double acc[NQ][M];
@@ -373,59 +371,32 @@ sweep_kernel_v2(const SweepParams P) {
       for (int t = 0; t < NQ; ++t)
 #pragma unroll
         for (int c = 0; c < M; ++c) acc[t][c] = 0.0;
+      // one barrier per slice: the flux slice is double-buffered by slice
+      // parity, and the time-contraction update of slice k is applied while
+      // slice k+1's flux stores drain (hides the DMMA -> FMA latency)
+      double dvp[M];
+#pragma unroll
+      for (int c = 0; c < M; ++c) dvp[c] = 0.0;
 #pragma unroll 1
       for (int k = 0; k < NQ; ++k) {
-      double F[DIM][M];
-      flux<DIM>(q[0], F);
-      if (act) {
+        double* sFk = sF + (k & 1) * (DS * M * PS);
+        double F[DIM][M];
+        flux<DIM>(q[0], F);
+        if (act) {
 #pragma unroll
-        for (int a = 0; a < DS; ++a)
+          for (int a = 0; a < DS; ++a)
 #pragma unroll
-          for (int c = 0; c < M; ++c)
-            sFt[(a * M + c) * PS + ((S::F1T && a == 1) ? p1t : px)] = F[a][c];
-      }
-      __syncthreads();
-      double dv[M];
+            for (int c = 0; c < M; ++c)
+              sFk[(a * M + c) * PS + ((S::F1T && a == 1) ? p1t : px)] = F[a][c];
+        }
+        if (k > 0) {
 #pragma unroll
-      for (int c = 0; c < M; ++c) {
-        double part[DS];
+          for (int t = 0; t < NQ; ++t) {
+            const double ic = P.ops.integ[t][k - 1];
 #pragma unroll
-        for (int a = 0; a < DS; ++a) {
-          double v = 0.0;
-          if (S::F1T && a == 1) {
-            const double2* b2 = reinterpret_cast<const double2*>(sFt + (a * M + c) * PS + g1t);
-#pragma unroll
-            for (int jj = 0; jj < NQ / 2; ++jj) {
-              const double2 w2 = b2[jj];
-              v = fma(drow[a][2 * jj], w2.x, v);
-              v = fma(drow[a][2 * jj + 1], w2.y, v);
-            }
-          } else {
-            const double* b = sFt + (a * M + c) * PS + gbase[a];
-#pragma unroll
-            for (int j = 0; j < NQ; ++j) v = fma(drow[a][j], b[j * gstr[a]], v);
+            for (int c = 0; c < M; ++c) acc[t][c] = fma(ic, dvp[c], acc[t][c]);
           }
-          part[a] = v;
         }
-        double sum = part[0];
-#pragma unroll
-        for (int a = 1; a < DS; ++a) sum += part[a];
-        dv[c] = sum;
-      }
-      if (DMMA) {
-#pragma unroll
-        for (int c = 0; c < M; ++c) {
-          double d1;
-          dmma_8x8x4(dv[c], d1, F[2][c], bfrag, dv[c], 0.0);
-        }
-      }
-        double icol[NQ];
-#pragma unroll
-        for (int t = 0; t < NQ; ++t) icol[t] = P.ops.integ[t][k];
-#pragma unroll
-        for (int t = 0; t < NQ; ++t)
-#pragma unroll
-          for (int c = 0; c < M; ++c) acc[t][c] = fma(icol[t], dv[c], acc[t][c]);
 #pragma unroll
         for (int c = 0; c < M; ++c) {
           const double q0 = q[0][c];
@@ -434,23 +405,65 @@ sweep_kernel_v2(const SweepParams P) {
           q[NQ - 1][c] = q0;
         }
         __syncthreads();
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          double part[DS];
+#pragma unroll
+          for (int a = 0; a < DS; ++a) {
+            double v = 0.0;
+            if (S::F1T && a == 1) {
+              const double2* b2 = reinterpret_cast<const double2*>(sFk + (a * M + c) * PS + g1t);
+#pragma unroll
+              for (int jj = 0; jj < NQ / 2; ++jj) {
+                const double2 w2 = b2[jj];
+                v = fma(drow[a][2 * jj], w2.x, v);
+                v = fma(drow[a][2 * jj + 1], w2.y, v);
+              }
+            } else {
+              const double* b = sFk + (a * M + c) * PS + gbase[a];
+#pragma unroll
+              for (int j = 0; j < NQ; ++j) v = fma(drow[a][j], b[j * gstr[a]], v);
+            }
+            part[a] = v;
+          }
+          double sum = part[0];
+#pragma unroll
+          for (int a = 1; a < DS; ++a) sum += part[a];
+          dvp[c] = sum;
+        }
+        if (DMMA) {
+#pragma unroll
+          for (int c = 0; c < M; ++c) {
+            double d1;
+            dmma_8x8x4(dvp[c], d1, F[2][c], bfrag, dvp[c], 0.0);
+          }
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < NQ; ++t) {
+        const double ic = P.ops.integ[t][NQ - 1];
+#pragma unroll
+        for (int c = 0; c < M; ++c) acc[t][c] = fma(ic, dvp[c], acc[t][c]);
       }
       // Picard update; max |q_new - q| via the bit patterns of non-negative
       // doubles (NaN/inf patterns sort above every finite value)
-      unsigned long long dbits = 0ull;
+      // max |q_new - q| (fmax drops NaN, so a running sum of the same
+      // differences carries any inf/NaN into the finiteness test)
+      double dmax = 0.0, dsum = 0.0;
 #pragma unroll
       for (int t = 0; t < NQ; ++t)
 #pragma unroll
         for (int c = 0; c < M; ++c) {
           const double qn = Qx[c] - scale * acc[t][c];
-          const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(qn - q[t][c]));
-          dbits = b > dbits ? b : dbits;
+          const double dd = fabs(qn - q[t][c]);
+          dmax = fmax(dmax, dd);
+          dsum += dd;
           q[t][c] = qn;
         }
       iters = it + 1;
-      const bool bad = dbits >= 0x7ff0000000000000ull;
+      const bool bad = !finite(dsum);
       if (__syncthreads_or(act && bad)) { failed = true; break; }
-      const double delta = block_max<NW>(act ? __longlong_as_double((long long)dbits) : 0.0, sRed);
+      const double delta = block_max<NW>(act ? dmax : 0.0, sRed);
       if (delta <= tol) break;
     }
   } else {
@@ -667,28 +680,29 @@ sweep_kernel_v2(const SweepParams P) {
   }
 
   // ---------------- s_max over the space-time face traces ----------------
-  // task = (face f, time t, face node y), y fastest: a half-warp gathers one face plane
-  for (int e = tid; e < 2 * DIM * NF * NQ; e += THREADS) {
-    const int y = e % NF;
-    const int ft = e / NF;
-    const int f = ft / NQ, t = ft % NQ, a = f >> 1;
-    const double* vec = (f & 1) ? P.ops.right : P.ops.left;
-    const int ya = y / NQ, yb = y % NQ;
-    double qs[M];
+  // tasks per face axis a (compile-time): (side, t, face node y), y fastest, so a
+  // warp gathers whole face planes with one address formula
 #pragma unroll
-    for (int c = 0; c < M; ++c) {
-      double v = 0.0;
+  for (int a = 0; a < DIM; ++a) {
+    for (int e = tid; e < 2 * NQ * NF; e += THREADS) {
+      const int y = e % NF, st_ = e / NF, t = st_ % NQ, side = st_ / NQ;
+      const double* vec = side ? P.ops.right : P.ops.left;
+      const int ya = y / NQ, yb = y % NQ;
+      double qs[M];
+#pragma unroll
+      for (int c = 0; c < M; ++c) qs[c] = 0.0;
 #pragma unroll
       for (int i = 0; i < NQ; ++i) {
         const int ad = (a == 0) ? trace_addr<NQ>(i, ya, yb)
                      : (a == 1) ? trace_addr<NQ>(ya, i, yb) : trace_addr<NQ>(ya, yb, i);
-        v = fma(vec[i], sQt[(t * M + c) * NSP + ad], v);
+        const double v = vec[i];
+#pragma unroll
+        for (int c = 0; c < M; ++c) qs[c] = fma(v, sQt[(t * M + c) * NSP + ad], qs[c]);
       }
-      qs[c] = v;
+      bool adm;
+      const double sp = max_speed_fast<DIM>(qs, a, a + 1, adm);
+      atomicMax(&sSmax[2 * a + side], (unsigned long long)__double_as_longlong(sp));
     }
-    const double pr = pressure_exact<DIM>(qs);
-    const double sp = speed_exact<DIM>(qs, a, pr);
-    atomicMax(&sSmax[f], (unsigned long long)__double_as_longlong(sp));
   }
   __syncthreads();
   if (tid == 0) {
@@ -696,27 +710,26 @@ sweep_kernel_v2(const SweepParams P) {
     bulk_commit_wait();   // also covers the Q store issued in the corrector
   }
   // ---------------- face records: qbar and fbar traces ----------------
-  for (int e = tid; e < 2 * DIM * NF * M; e += THREADS) {
-    const int y = e % NF;
-    const int fc = e / NF;
-    const int f = fc / M, c = fc % M, a = f >> 1;
-    const double* vec = (f & 1) ? P.ops.right : P.ops.left;
-    const int ya = y / NQ, yb = y % NQ;
-    int pxb, psta;
-    if (a == 0) { pxb = ya * NQ + yb; psta = P0; }
-    else if (a == 1) { pxb = ya * P0 + yb; psta = NQ; }
-    else { pxb = ya * P0 + yb * NQ; psta = 1; }
-    double vq = 0.0, vf = 0.0;
 #pragma unroll
-    for (int i = 0; i < NQ; ++i) {
-      const int ad = (a == 0) ? trace_addr<NQ>(i, ya, yb)
-                   : (a == 1) ? trace_addr<NQ>(ya, i, yb) : trace_addr<NQ>(ya, yb, i);
-      vq = fma(vec[i], sQb[c * NSP + ad], vq);
-      vf = fma(vec[i], sFb[(a * M + c) * PS + pxb + i * psta], vf);
+  for (int a = 0; a < DIM; ++a) {
+    const int pst = (a == 0) ? P0 : (a == 1) ? NQ : 1;
+    for (int e = tid; e < 2 * M * NF; e += THREADS) {
+      const int y = e % NF, sc = e / NF, c = sc % M, side = sc / M;
+      const double* vec = side ? P.ops.right : P.ops.left;
+      const int ya = y / NQ, yb = y % NQ;
+      const int pxb = (a == 0) ? ya * NQ + yb : (a == 1) ? ya * P0 + yb : ya * P0 + yb * NQ;
+      double vq = 0.0, vf = 0.0;
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) {
+        const int ad = (a == 0) ? trace_addr<NQ>(i, ya, yb)
+                     : (a == 1) ? trace_addr<NQ>(ya, i, yb) : trace_addr<NQ>(ya, yb, i);
+        vq = fma(vec[i], sQb[c * NSP + ad], vq);
+        vf = fma(vec[i], sFb[(a * M + c) * PS + pxb + i * pst], vf);
+      }
+      double* rec = P.tr_out + ((long long)(2 * a + side) * P.slots + own_slot) * REC;
+      rec[y * M + c] = vq;
+      rec[NF * M + y * M + c] = vf;
     }
-    double* rec = P.tr_out + ((long long)f * P.slots + own_slot) * REC;
-    rec[y * M + c] = vq;
-    rec[NF * M + y * M + c] = vf;
   }
   if (tid < 2 * DIM) {
     double* rec = P.tr_out + ((long long)tid * P.slots + own_slot) * REC;
