@@ -36,16 +36,16 @@ void launch_sweep(const SweepParams& P, unsigned grid, cudaStream_t s) {
   sweep_kernel<DIM, NQ><<<grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
 }
 
-template <int NQ, int TS, bool DMMA>
+template <int NQ, int TS, bool DMMA, bool ROLLED = (NQ == 4)>
 void launch_sweep_v2(const SweepParams& P, unsigned grid, cudaStream_t s) {
-  using S = ShapeV2<NQ, TS, DMMA>;
+  using S = ShapeV2<NQ, TS, DMMA, ROLLED>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(sweep_kernel_v2<NQ, TS, DMMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(sweep_kernel_v2<NQ, TS, DMMA, ROLLED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)S::SMEM_BYTES);
     attr = true;
   }
-  sweep_kernel_v2<NQ, TS, DMMA><<<grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
+  sweep_kernel_v2<NQ, TS, DMMA, ROLLED><<<grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
 }
 
 struct Dispatch {
@@ -56,10 +56,10 @@ struct Dispatch {
 template <int DIM, int NQ>
 Dispatch make_dispatch() { return Dispatch{&launch_sweep<DIM, NQ>, Shape<DIM, NQ>::REC}; }
 
-template <int NQ, int TS, bool DMMA>
+template <int NQ, int TS, bool DMMA, bool ROLLED = (NQ == 4)>
 Dispatch make_dispatch_v2() {
-  static_assert(ShapeV2<NQ, TS, DMMA>::REC == Shape<3, NQ>::REC, "record layout must match");
-  return Dispatch{&launch_sweep_v2<NQ, TS, DMMA>, ShapeV2<NQ, TS, DMMA>::REC};
+  static_assert(ShapeV2<NQ, TS, DMMA, ROLLED>::REC == Shape<3, NQ>::REC, "record layout must match");
+  return Dispatch{&launch_sweep_v2<NQ, TS, DMMA, ROLLED>, ShapeV2<NQ, TS, DMMA, ROLLED>::REC};
 }
 
 int kernel_variant() {
@@ -90,7 +90,8 @@ bool dispatch_for(int d, int p, Dispatch* out) {
       case 3: *out = make_dispatch<3, 3>(); return true;
       case 4:
         *out = kernel_variant() == 1 ? make_dispatch<3, 4>()
-             : kernel_variant() == 2 ? make_dispatch_v2<4, 2, true>() : make_dispatch_v2<4, 1, true>();
+             : kernel_variant() == 2 ? make_dispatch_v2<4, 2, true>()
+             : kernel_variant() == 5 ? make_dispatch_v2<4, 1, true, true>() : make_dispatch_v2<4, 1, true, false>();
         return true;
       case 5: *out = make_dispatch<3, 5>(); return true;
       case 6:

@@ -32,7 +32,7 @@ __host__ __device__ constexpr int plane_pad(int nq) {
          : (((nq * nq + 6) % 16 >= nq && (nq * nq + 6) % 16 <= 16 - nq) ? 6 : 8)));
 }
 
-template <int NQ, int TS, bool DMMA>
+template <int NQ, int TS, bool DMMA, bool ROLLED = (NQ == 4)>
 struct ShapeV2 {
   static constexpr int DIM = 3, M = 5;
   static constexpr int NS = NQ * NQ * NQ;
@@ -48,8 +48,9 @@ struct ShapeV2 {
   static constexpr int PS = NQ * P0;                   // padded slice size
   static constexpr int DS = DMMA ? DIM - 1 : DIM;      // axes through shared memory
   static constexpr bool F1T = (NQ == 4);               // axis-1 flux stored transposed, 16-byte gathers
-  static constexpr bool ROLL = (NQ == 4);              // rolled slice loop (i-cache); NQ = 6 stays unrolled
+  static constexpr bool ROLL = ROLLED;                 // rolled slice loop (i-cache); NQ = 6 stays unrolled
   static constexpr int RR = 1;                         // slices per rolled trip
+  static constexpr bool DBUF = (TS == 1 && NQ == 4);   // double-buffered flux slices (one barrier per slice)
   static constexpr int P1T = NQ * NQ + 2;              // its plane stride (odd number of 16-byte chunks)
   static constexpr int REC = 2 * NF * M + 2;
   // shared memory (doubles), all region sizes even (16-byte alignment)
@@ -60,7 +61,7 @@ struct ShapeV2 {
   static constexpr int R_FB = DIM * M * PS;            // fbar (after the Picard loop)
   static constexpr int R_DIV = (NQ + 1) * M * NSP;     // divergence of all slices / q slices + qbar
   static constexpr int R_PRED0 = (R_F > R_FB ? R_F : R_FB) + R_DIV;
-  static constexpr int R_PRED = (TS == 1 && ROLL && 2 * R_F > R_PRED0) ? 2 * R_F : R_PRED0;
+  static constexpr int R_PRED = ((ROLL || DBUF) && 2 * R_F > R_PRED0) ? 2 * R_F : R_PRED0;
   static constexpr int R_U = R_REC > R_PRED ? R_REC : R_PRED;
   static constexpr int R_FACE = 2 * DIM * NF * M;
   static constexpr int OFF_BAR = 0;                    // 2 doubles for the mbarrier
@@ -140,10 +141,10 @@ __device__ __forceinline__ int trace_addr(int i0, int i1, int i2) {
   return (i0 * NQ + i1) * NQ + i2;
 }
 
-template <int NQ, int TS, bool DMMA>
-__global__ void __launch_bounds__(ShapeV2<NQ, TS, DMMA>::THREADS, ShapeV2<NQ, TS, DMMA>::MINB)
+template <int NQ, int TS, bool DMMA, bool ROLLED = (NQ == 4)>
+__global__ void __launch_bounds__(ShapeV2<NQ, TS, DMMA, ROLLED>::THREADS, ShapeV2<NQ, TS, DMMA, ROLLED>::MINB)
 sweep_kernel_v2(const SweepParams P) {
-  using S = ShapeV2<NQ, TS, DMMA>;
+  using S = ShapeV2<NQ, TS, DMMA, ROLLED>;
   constexpr int DIM = 3, M = 5, NS = S::NS, NF = S::NF, NSP = S::NSP, REC = S::REC;
   constexpr int THREADS = S::THREADS, NW = S::NWARPS, TH = S::TH, P0 = S::P0, PS = S::PS;
   constexpr int DS = S::DS;
@@ -472,6 +473,9 @@ sweep_kernel_v2(const SweepParams P) {
 #pragma unroll
     for (int s = 0; s < TH; ++s) {
       const int k = ts * TH + s;
+      // TS == 1: flux slices alternate between two buffers, so the barrier
+      // that publishes slice k also retires the reads of slice k-2's buffer
+      double* sFs = (TS == 1 && S::DBUF) ? sF + (k & 1) * (DS * M * PS) : sFt;
       double F[DIM][M];
       flux<DIM>(q[s], F);
       if (act) {
@@ -479,7 +483,7 @@ sweep_kernel_v2(const SweepParams P) {
         for (int a = 0; a < DS; ++a)
 #pragma unroll
           for (int c = 0; c < M; ++c)
-            sFt[(a * M + c) * PS + ((S::F1T && a == 1) ? p1t : px)] = F[a][c];
+            sFs[(a * M + c) * PS + ((S::F1T && a == 1) ? p1t : px)] = F[a][c];
       }
       __syncthreads();
       double dv[M];
@@ -490,7 +494,7 @@ sweep_kernel_v2(const SweepParams P) {
         for (int a = 0; a < DS; ++a) {
           double v = 0.0;
           if (S::F1T && a == 1) {
-            const double2* b2 = reinterpret_cast<const double2*>(sFt + (a * M + c) * PS + g1t);
+            const double2* b2 = reinterpret_cast<const double2*>(sFs + (a * M + c) * PS + g1t);
 #pragma unroll
             for (int jj = 0; jj < NQ / 2; ++jj) {
               const double2 w2 = b2[jj];
@@ -498,7 +502,7 @@ sweep_kernel_v2(const SweepParams P) {
               v = fma(drow[a][2 * jj + 1], w2.y, v);
             }
           } else {
-            const double* b = sFt + (a * M + c) * PS + gbase[a];
+            const double* b = sFs + (a * M + c) * PS + gbase[a];
 #pragma unroll
             for (int j = 0; j < NQ; ++j) v = fma(drow[a][j], b[j * gstr[a]], v);
           }
@@ -526,7 +530,7 @@ sweep_kernel_v2(const SweepParams P) {
 #pragma unroll
         for (int c = 0; c < M; ++c) sDiv[(k * M + c) * NSP + x] = dv[c];
       }
-      __syncthreads();
+      if (!(TS == 1 && S::DBUF)) __syncthreads();
     }
     unsigned long long dbits = 0ull;
 #pragma unroll
