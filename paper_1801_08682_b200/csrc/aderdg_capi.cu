@@ -17,6 +17,7 @@
 #include "../../include/aderdg_b200.h"
 #include "aderdg_kernels.cuh"
 #include "aderdg_sweep_v2.cuh"
+#include "aderdg_sweep_ho.cuh"
 
 using namespace adg;
 
@@ -55,6 +56,23 @@ struct Dispatch {
 
 template <int DIM, int NQ>
 Dispatch make_dispatch() { return Dispatch{&launch_sweep<DIM, NQ>, Shape<DIM, NQ>::REC}; }
+
+template <int NQ>
+void launch_sweep_ho(const SweepParams& P, unsigned grid, cudaStream_t s) {
+  using S = ShapeHO<NQ>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sweep_kernel_ho<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM_BYTES);
+    attr = true;
+  }
+  sweep_kernel_ho<NQ><<<grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
+}
+
+template <int NQ>
+Dispatch make_dispatch_ho() {
+  static_assert(ShapeHO<NQ>::REC == Shape<3, NQ>::REC, "record layout must match");
+  return Dispatch{&launch_sweep_ho<NQ>, ShapeHO<NQ>::REC};
+}
 
 template <int NQ, int TS, bool DMMA, bool ROLLED = (NQ == 4)>
 Dispatch make_dispatch_v2() {
@@ -98,12 +116,11 @@ bool dispatch_for(int d, int p, Dispatch* out) {
         *out = kernel_variant() == 1 ? make_dispatch<3, 6>()
              : kernel_variant() == 2 ? make_dispatch_v2<6, 2, false>() : make_dispatch_v2<6, 1, false>();
         return true;
-      // p >= 6: the space-time line no longer fits the register file at one
-      // thread per node; the per-thread arrays live in (L1/L2-backed) local memory
-      case 7: *out = make_dispatch<3, 7>(); return true;
-      case 8: *out = make_dispatch<3, 8>(); return true;
-      case 9: *out = make_dispatch<3, 9>(); return true;
-      case 10: *out = make_dispatch<3, 10>(); return true;
+      // p >= 6: time line in local memory, spatial derivatives as DMMA GEMMs
+      case 7: *out = kernel_variant() == 1 ? make_dispatch<3, 7>() : make_dispatch_ho<7>(); return true;
+      case 8: *out = kernel_variant() == 1 ? make_dispatch<3, 8>() : make_dispatch_ho<8>(); return true;
+      case 9: *out = kernel_variant() == 1 ? make_dispatch<3, 9>() : make_dispatch_ho<9>(); return true;
+      case 10: *out = kernel_variant() == 1 ? make_dispatch<3, 10>() : make_dispatch_ho<10>(); return true;
     }
   }
   return false;

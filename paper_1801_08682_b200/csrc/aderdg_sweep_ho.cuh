@@ -1,0 +1,488 @@
+// aderdg_sweep_ho.cuh — high-order fused sweep kernel (3D, p = 6..9).
+//
+// At p >= 6 one cell's space-time predictor (n^4 * 5 doubles: 96 KB at p=6,
+// 400 KB at p=9) no longer fits a thread-per-node register file, and the
+// unblocked shared-memory derivative gathers (n loads per output per axis)
+// would make the kernel shared-memory bound.  This kernel therefore:
+//   * runs 512 threads per cell, each owning NPT = ceil(n^3/512) nodes;
+//   * keeps the per-node time line (old iterate qo[t][c], divergence history
+//     dh[k][c]) in thread-private local memory (L1/L2 backed, coalesced);
+//   * computes the spatial derivative of every time slice as three GEMMs on
+//     the FP64 tensor cores: Out_a[i'][r] = sum_j diff[i'][j] F_a[j][r], with
+//     r = (the two other node indices, component).  A = diff (constant
+//     fragments in registers), B = the flux staged in shared memory with the
+//     contraction index fastest (row stride JS = 12 doubles: a B-fragment load
+//     of a warp touches every 8-byte bank exactly twice).  At p = 7 (n = 8) the
+//     m8n8k4 tiles fit exactly (no padding); at p = 9, M pads 10 -> 16 and
+//     K 10 -> 12.
+//   * everything else (Riemann, corrector, calc_time_step, final flux, volume
+//     integral, face traces, s_max) follows sweep_kernel, staged per axis /
+//     per time level through one shared node buffer.
+//
+// Reference (src/ = /root/reference/pkg/src/aderdg/): kernels.py:68-229,
+// scheduler.py:370-449 (same tasks as sweep_kernel).
+#pragma once
+#include "aderdg_kernels.cuh"
+#include "aderdg_sweep_v2.cuh"
+
+namespace adg {
+
+template <int NQ>
+struct ShapeHO {
+  static constexpr int DIM = 3, M = 5;
+  static constexpr int NS = NQ * NQ * NQ;
+  static constexpr int NF = NQ * NQ;
+  static constexpr int THREADS = 512;
+  static constexpr int NW = THREADS / 32;
+  static constexpr int NPT = (NS + THREADS - 1) / THREADS;   // nodes per thread
+  static constexpr int KC = (NQ + 3) / 4;                    // k-chunks of m8n8k4
+  static constexpr int MT = (NQ + 7) / 8;                    // m-tiles (output positions)
+  static constexpr int RR = NF * M;                          // GEMM columns per axis
+  static constexpr int NT = (RR + 7) / 8;                    // n-tiles
+  static constexpr int RP = NT * 8;
+  static constexpr int JS = 12;                              // row stride of the B staging
+  static constexpr int REC = 2 * NF * M + 2;
+  // shared memory (doubles)
+  static constexpr int R_RED = 2 * NW + 2 * DIM + 4;
+  static constexpr int R_FA = RP * JS;                       // B staging of one axis
+  static constexpr int R_DV = M * NS;                        // derivative accumulator
+  static constexpr int R_NODE = M * NS;                      // per-node staging (q_t / qbar / fbar_a / D / Q)
+  static constexpr int R_FACE = 2 * DIM * NF * M;
+  static constexpr int OFF_RED = 0;
+  static constexpr int OFF_FA = (R_RED + 1) & ~1;
+  static constexpr int OFF_DV = OFF_FA + R_FA;
+  static constexpr int OFF_NODE = OFF_DV + R_DV;
+  static constexpr int OFF_FACE = OFF_NODE + R_NODE;
+  static constexpr int TOTAL = OFF_FACE + R_FACE;
+  static constexpr size_t SMEM_BYTES = sizeof(double) * TOTAL;
+};
+
+template <int NQ>
+__global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
+  using S = ShapeHO<NQ>;
+  constexpr int DIM = 3, M = 5, NS = S::NS, NF = S::NF, NPT = S::NPT, REC = S::REC;
+  constexpr int THREADS = S::THREADS, NW = S::NW, KC = S::KC, MT = S::MT, NT = S::NT;
+  constexpr int RR = S::RR, JS = S::JS;
+
+  extern __shared__ __align__(16) double smem[];
+  double* sRed = smem + S::OFF_RED;
+  unsigned long long* sSmax = reinterpret_cast<unsigned long long*>(sRed + 2 * NW);
+  double* sFA = smem + S::OFF_FA;     // [RP][JS]
+  double* sDv = smem + S::OFF_DV;     // [M][NS]
+  double* sN = smem + S::OFF_NODE;    // [M][NS] node staging
+  double* sFace = smem + S::OFF_FACE;
+
+  DevState* st = P.st;
+  if (st->status != 0) return;
+  const int mode = P.mode;
+  if (mode == MODE_RERUN && !st->rerun_next) return;
+  if (mode == MODE_NORMAL && st->reduce[1] != 0) return;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long cell = blockIdx.x;
+  const long long gcell = cell + P.cell_offset;
+  const int plane = (int)(cell / P.plane_cells);
+  const int rest = (int)(cell % P.plane_cells);
+  const long long own_slot = (long long)(plane + 1) * P.plane_cells + rest;
+  const int step_idx = (mode == MODE_NORMAL) ? st->step + 1 : 0;
+  double* Qg = P.Q + cell * (NS * M);
+  double* Dg = P.D + cell * (NS * M);
+
+  // nodes of this thread
+  int xn[NPT];
+  bool an[NPT];
+#pragma unroll
+  for (int n = 0; n < NPT; ++n) {
+    xn[n] = tid + n * THREADS;
+    an[n] = xn[n] < NS;
+    if (!an[n]) xn[n] = 0;
+  }
+  auto idx3 = [](int x, int& i0, int& i1, int& i2) {
+    i0 = x / (NQ * NQ); i1 = (x / NQ) % NQ; i2 = x % NQ;
+  };
+
+  double Qx[NPT][M];
+#pragma unroll
+  for (int n = 0; n < NPT; ++n)
+#pragma unroll
+    for (int c = 0; c < M; ++c) Qx[n][c] = Qg[xn[n] * M + c];
+
+  if (mode == MODE_NORMAL) {
+    // ------------- Riemann on the 2d faces (kernels.py:147-179), time-collapsed -------------
+    long long nb_slot[2 * DIM];
+#pragma unroll
+    for (int f = 0; f < 2 * DIM; ++f) {
+      const int a = f >> 1, dir = (f & 1) ? 1 : -1;
+      if (a == 0) {
+        int pl = plane + dir;
+        if (!P.halo) pl = (pl + P.K) % P.K;
+        nb_slot[f] = (long long)(pl + 1) * P.plane_cells + rest;
+      } else {
+        const int st_a = (a == 1) ? P.K : 1;
+        const int ia = (rest / st_a) % P.K;
+        const int ja = (ia + dir + P.K) % P.K;
+        nb_slot[f] = (long long)(plane + 1) * P.plane_cells + rest + (ja - ia) * st_a;
+      }
+    }
+    for (int e = tid; e < 2 * DIM * NF * M; e += THREADS) {
+      const int f = e / (NF * M), yc = e % (NF * M);
+      const double* own = P.tr_in + ((long long)f * P.slots + own_slot) * REC;
+      const double* nb = P.tr_in + ((long long)(f ^ 1) * P.slots + nb_slot[f]) * REC;
+      const double* mr = (f & 1) ? own : nb;
+      const double* pr = (f & 1) ? nb : own;
+      const double alpha = fmax(mr[2 * NF * M], pr[2 * NF * M]);
+      const double fs = __dsub_rn(__dmul_rn(0.5, __dadd_rn(mr[NF * M + yc], pr[NF * M + yc])),
+                                  __dmul_rn(__dmul_rn(0.5, alpha), __dsub_rn(pr[yc], mr[yc])));
+      sFace[e] = (f & 1) ? fs : -fs;
+    }
+    __syncthreads();
+    // ------------- integrate_face + update (kernels.py:183-214) -------------
+    const double scale_old = st->dt_old / P.h;
+#pragma unroll
+    for (int n = 0; n < NPT; ++n) {
+      if (!an[n]) continue;
+      int i[3];
+      idx3(xn[n], i[0], i[1], i[2]);
+      double Dx[M];
+#pragma unroll
+      for (int c = 0; c < M; ++c) Dx[c] = Dg[xn[n] * M + c];
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) {
+        const int y = (a == 0) ? i[1] * NQ + i[2] : (a == 1) ? i[0] * NQ + i[2] : i[0] * NQ + i[1];
+        const double slo = __dmul_rn(scale_old, P.ops.lift_lo[i[a]]);
+        const double shi = __dmul_rn(scale_old, P.ops.lift_hi[i[a]]);
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          Dx[c] = __dsub_rn(Dx[c], __dmul_rn(slo, sFace[((2 * a) * NF + y) * M + c]));
+          Dx[c] = __dsub_rn(Dx[c], __dmul_rn(shi, sFace[((2 * a + 1) * NF + y) * M + c]));
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < M; ++c) Qx[n][c] = __dadd_rn(Qx[n][c], Dx[c]);
+      if (P.spike_step >= 0 && step_idx == P.spike_step) {
+        const double rho = Qx[n][0];
+        const double pr = pressure_exact<DIM>(Qx[n]);
+#pragma unroll
+        for (int b = 0; b < DIM; ++b) Qx[n][1 + b] = __dmul_rn(Qx[n][1 + b], P.spike_factor);
+        double jj = __dmul_rn(Qx[n][1], Qx[n][1]);
+#pragma unroll
+        for (int b = 1; b < DIM; ++b) jj = __dadd_rn(jj, __dmul_rn(Qx[n][1 + b], Qx[n][1 + b]));
+        Qx[n][M - 1] = __dadd_rn(__ddiv_rn(pr, 0.4), __ddiv_rn(__dmul_rn(0.5, jj), rho));
+      }
+#pragma unroll
+      for (int c = 0; c < M; ++c) Qg[xn[n] * M + c] = Qx[n][c];
+    }
+  }
+
+  if (mode != MODE_RERUN) {
+    // ------------- calc_time_step (kernels.py:216-229) -------------
+    bool ok = true;
+    double lam = 0.0;
+#pragma unroll
+    for (int n = 0; n < NPT; ++n) {
+      if (!an[n]) continue;
+      bool fin = true;
+#pragma unroll
+      for (int c = 0; c < M; ++c) fin = fin && finite(Qx[n][c]);
+      bool adm = false;
+      const double l = max_speed_fast<DIM>(Qx[n], 0, DIM, adm);
+      ok = ok && fin && adm;
+      if (fin && adm) lam = fmax(lam, l);
+    }
+    if (!__syncthreads_and(ok)) {
+      if (tid == 0) report_error(st, 2 * gcell + 0);
+      return;
+    }
+    lam = block_max<NW>(lam, sRed);
+    if (tid == 0) atomicMax(&st->reduce[0], __double_as_longlong(lam));
+    if (mode == MODE_SEED) return;
+  } else {
+    bool ok = true;
+#pragma unroll
+    for (int n = 0; n < NPT; ++n)
+      if (an[n])
+#pragma unroll
+        for (int c = 0; c < M; ++c) ok = ok && finite(Qx[n][c]);
+    if (!__syncthreads_and(ok)) {
+      if (tid == 0) report_error(st, 2 * gcell + 1);
+      return;
+    }
+  }
+
+  // ---------------- predictor (kernels.py:68-105) ----------------
+  const double dt = (mode == MODE_RERUN) ? st->dt_old : st->dt_new;
+  const double scale = dt / P.h;
+  double am = 0.0;
+#pragma unroll
+  for (int n = 0; n < NPT; ++n)
+    if (an[n])
+#pragma unroll
+      for (int c = 0; c < M; ++c) am = fmax(am, fabs(Qx[n][c]));
+  const double tol = 1e-10 * (1.0 + block_max<NW>(am, sRed));
+  const int cap = 2 * NQ;
+
+  // zero the padding of the B staging once (rows >= RR, columns >= NQ)
+  for (int e = tid; e < S::R_FA; e += THREADS) sFA[e] = 0.0;
+  // constant A fragments: A[i'][j] = diff[i'][j]; lane holds A[mt*8 + g][kc*4 + t4]
+  double afr[MT][KC];
+  {
+    const int g = lane >> 2, t4 = lane & 3;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int kc = 0; kc < KC; ++kc) {
+        const int ii = mt * 8 + g, jj = kc * 4 + t4;
+        afr[mt][kc] = (ii < NQ && jj < NQ) ? P.ops.diff[ii][jj] : 0.0;
+      }
+  }
+  // per-node time line in thread-private (local) memory
+  double qo[NPT][NQ][M];
+  double dh[NPT][NQ][M];
+  int iters = 0;
+  bool failed = false;
+  __syncthreads();
+#pragma unroll 1
+  for (int it = 0; it < cap; ++it) {
+#pragma unroll 1
+    for (int k = 0; k < NQ; ++k) {
+      double F[NPT][DIM][M];
+#pragma unroll
+      for (int n = 0; n < NPT; ++n) {
+        double qq[M];
+#pragma unroll
+        for (int c = 0; c < M; ++c) qq[c] = (it == 0) ? Qx[n][c] : qo[n][k][c];
+        flux<DIM>(qq, F[n]);
+      }
+#pragma unroll 1
+      for (int a = 0; a < DIM; ++a) {
+        // stage F_a with the contraction index (i_a) fastest: row r = (ib, ic, c)
+#pragma unroll
+        for (int n = 0; n < NPT; ++n) {
+          if (!an[n]) continue;
+          int i[3];
+          idx3(xn[n], i[0], i[1], i[2]);
+          const int ib = (a == 0) ? i[1] : i[0];
+          const int ic = (a == 2) ? i[1] : i[2];
+          const int ia = i[a];
+#pragma unroll
+          for (int c = 0; c < M; ++c) {
+            const double v = (a == 0) ? F[n][0][c] : (a == 1) ? F[n][1][c] : F[n][2][c];
+            sFA[((ib * NQ + ic) * M + c) * JS + ia] = v;
+          }
+        }
+        __syncthreads();
+        // GEMM tiles: warp w takes n-tiles w, w+NW, ...
+        for (int nt = warp; nt < NT; nt += NW) {
+          double cacc[MT][2];
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) { cacc[mt][0] = 0.0; cacc[mt][1] = 0.0; }
+          const double* brow = sFA + (nt * 8 + (lane >> 2)) * JS + (lane & 3);
+#pragma unroll
+          for (int kc = 0; kc < KC; ++kc) {
+            const double b = brow[kc * 4];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt)
+              dmma_8x8x4(cacc[mt][0], cacc[mt][1], afr[mt][kc], b, cacc[mt][0], cacc[mt][1]);
+          }
+          // C[i'][r]: lane holds rows mt*8 + g, columns nt*8 + 2*t4 + {0,1}
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int e2 = 0; e2 < 2; ++e2) {
+              const int ip = mt * 8 + (lane >> 2);
+              const int r = nt * 8 + 2 * (lane & 3) + e2;
+              if (ip < NQ && r < RR) {
+                const int c = r % M, bc = r / M, ib = bc / NQ, ic = bc % NQ;
+                const int x = (a == 0) ? (ip * NQ + ib) * NQ + ic
+                            : (a == 1) ? (ib * NQ + ip) * NQ + ic : (ib * NQ + ic) * NQ + ip;
+                if (a == 0) sDv[c * NS + x] = cacc[mt][e2];
+                else sDv[c * NS + x] += cacc[mt][e2];
+              }
+            }
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int n = 0; n < NPT; ++n)
+#pragma unroll
+        for (int c = 0; c < M; ++c) dh[n][k][c] = sDv[c * NS + xn[n]];
+    }
+    // time contraction + Picard update per node
+    double dmax = 0.0, dsum = 0.0;
+#pragma unroll
+    for (int n = 0; n < NPT; ++n) {
+#pragma unroll 1
+      for (int t = 0; t < NQ; ++t) {
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          double acc = 0.0;
+#pragma unroll
+          for (int k = 0; k < NQ; ++k) acc = fma(P.ops.integ[t][k], dh[n][k][c], acc);
+          const double qn = Qx[n][c] - scale * acc;
+          const double qold = (it == 0) ? Qx[n][c] : qo[n][t][c];
+          const double dd = fabs(qn - qold);
+          if (an[n]) { dmax = fmax(dmax, dd); dsum += dd; }
+          qo[n][t][c] = qn;
+        }
+      }
+    }
+    iters = it + 1;
+    if (__syncthreads_or(!finite(dsum))) { failed = true; break; }
+    const double delta = block_max<NW>(dmax, sRed);
+    if (delta <= tol) break;
+  }
+
+  // final flux: time average fbar (per node, registers) + finiteness
+  double fb[NPT][DIM][M];
+  double qb[NPT][M];
+#pragma unroll
+  for (int n = 0; n < NPT; ++n) {
+#pragma unroll
+    for (int a = 0; a < DIM; ++a)
+#pragma unroll
+      for (int c = 0; c < M; ++c) fb[n][a][c] = 0.0;
+#pragma unroll
+    for (int c = 0; c < M; ++c) qb[n][c] = 0.0;
+  }
+  if (!failed) {
+    bool bad = false;
+#pragma unroll
+    for (int n = 0; n < NPT; ++n) {
+#pragma unroll 1
+      for (int t = 0; t < NQ; ++t) {
+        double F[DIM][M];
+        flux<DIM>(qo[n][t], F);
+        const double w = P.ops.w[t];
+#pragma unroll
+        for (int a = 0; a < DIM; ++a)
+#pragma unroll
+          for (int c = 0; c < M; ++c) {
+            bad |= an[n] && !finite(F[a][c]);
+            fb[n][a][c] = fma(w, F[a][c], fb[n][a][c]);
+          }
+#pragma unroll
+        for (int c = 0; c < M; ++c) qb[n][c] = fma(w, qo[n][t][c], qb[n][c]);
+      }
+    }
+    failed = __syncthreads_or(bad);
+  }
+  if (failed) {
+    if (tid == 0) report_error(st, 2 * gcell + 1);
+    return;
+  }
+  if (tid == 0) {
+    atomicAdd((unsigned long long*)&st->picard_iters, (unsigned long long)iters);
+    atomicAdd((unsigned long long*)&st->predicts, 1ull);
+    atomicAdd((unsigned long long*)&st->hist[iters < HIST_BINS ? iters : HIST_BINS - 1], 1ull);
+  }
+
+  // ---------------- integrate_volume + f̄ traces, one axis at a time ----------------
+  double Dv[NPT][M];
+#pragma unroll
+  for (int n = 0; n < NPT; ++n)
+#pragma unroll
+    for (int c = 0; c < M; ++c) Dv[n][c] = 0.0;
+#pragma unroll 1
+  for (int a = 0; a < DIM; ++a) {
+    __syncthreads();
+#pragma unroll
+    for (int n = 0; n < NPT; ++n)
+      if (an[n])
+#pragma unroll
+        for (int c = 0; c < M; ++c)
+          sN[c * NS + xn[n]] = (a == 0) ? fb[n][0][c] : (a == 1) ? fb[n][1][c] : fb[n][2][c];
+    __syncthreads();
+    const int sa = (a == 0) ? NQ * NQ : (a == 1) ? NQ : 1;
+#pragma unroll
+    for (int n = 0; n < NPT; ++n) {
+      if (!an[n]) continue;
+      int i[3];
+      idx3(xn[n], i[0], i[1], i[2]);
+      const int base = xn[n] - i[a] * sa;
+#pragma unroll
+      for (int c = 0; c < M; ++c) {
+        double s = Dv[n][c];
+#pragma unroll
+        for (int j = 0; j < NQ; ++j) s = fma(P.ops.kvol[i[a]][j], sN[c * NS + base + j * sa], s);
+        Dv[n][c] = s;
+      }
+    }
+    // f̄ face traces of axis a (both sides)
+    for (int e = tid; e < 2 * NF * M; e += THREADS) {
+      const int y = e % NF, sc = e / NF, c = sc % M, side = sc / M;
+      const double* vec = side ? P.ops.right : P.ops.left;
+      const int ya = y / NQ, yb = y % NQ;
+      const int xb = (a == 0) ? ya * NQ + yb : (a == 1) ? ya * NQ * NQ + yb : (ya * NQ + yb) * NQ;
+      double v = 0.0;
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) v = fma(vec[i], sN[c * NS + xb + i * sa], v);
+      P.tr_out[((long long)(2 * a + side) * P.slots + own_slot) * REC + NF * M + y * M + c] = v;
+    }
+  }
+  {
+    const double sdt = dt / P.h;
+#pragma unroll
+    for (int n = 0; n < NPT; ++n)
+      if (an[n])
+#pragma unroll
+        for (int c = 0; c < M; ++c) Dg[xn[n] * M + c] = Dv[n][c] * sdt;
+  }
+
+  // ---------------- q̄ face traces ----------------
+  __syncthreads();
+#pragma unroll
+  for (int n = 0; n < NPT; ++n)
+    if (an[n])
+#pragma unroll
+      for (int c = 0; c < M; ++c) sN[c * NS + xn[n]] = qb[n][c];
+  if (tid < 2 * DIM) sSmax[tid] = 0ull;
+  __syncthreads();
+  for (int e = tid; e < 2 * DIM * NF * M; e += THREADS) {
+    const int y = e % NF, fc = e / NF, c = fc % M, f = fc / M, a = f >> 1;
+    const double* vec = (f & 1) ? P.ops.right : P.ops.left;
+    const int ya = y / NQ, yb = y % NQ;
+    const int sa = (a == 0) ? NQ * NQ : (a == 1) ? NQ : 1;
+    const int xb = (a == 0) ? ya * NQ + yb : (a == 1) ? ya * NQ * NQ + yb : (ya * NQ + yb) * NQ;
+    double v = 0.0;
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) v = fma(vec[i], sN[c * NS + xb + i * sa], v);
+    P.tr_out[((long long)f * P.slots + own_slot) * REC + y * M + c] = v;
+  }
+  // ---------------- s_max over the space-time traces, one time level at a time ----------------
+#pragma unroll 1
+  for (int t = 0; t < NQ; ++t) {
+    __syncthreads();
+#pragma unroll
+    for (int n = 0; n < NPT; ++n)
+      if (an[n])
+#pragma unroll
+        for (int c = 0; c < M; ++c) sN[c * NS + xn[n]] = qo[n][t][c];
+    __syncthreads();
+    for (int e = tid; e < 2 * DIM * NF; e += THREADS) {
+      const int y = e % NF, f = e / NF, a = f >> 1;
+      const double* vec = (f & 1) ? P.ops.right : P.ops.left;
+      const int ya = y / NQ, yb = y % NQ;
+      const int sa = (a == 0) ? NQ * NQ : (a == 1) ? NQ : 1;
+      const int xb = (a == 0) ? ya * NQ + yb : (a == 1) ? ya * NQ * NQ + yb : (ya * NQ + yb) * NQ;
+      double qs[M];
+#pragma unroll
+      for (int c = 0; c < M; ++c) {
+        double v = 0.0;
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) v = fma(vec[i], sN[c * NS + xb + i * sa], v);
+        qs[c] = v;
+      }
+      bool adm;
+      const double sp = max_speed_fast<DIM>(qs, a, a + 1, adm);
+      atomicMax(&sSmax[f], (unsigned long long)__double_as_longlong(sp));
+    }
+  }
+  __syncthreads();
+  if (tid < 2 * DIM) {
+    double* rec = P.tr_out + ((long long)tid * P.slots + own_slot) * REC;
+    rec[2 * NF * M] = __longlong_as_double((long long)sSmax[tid]);
+    rec[2 * NF * M + 1] = 0.0;
+  }
+}
+
+}  // namespace adg

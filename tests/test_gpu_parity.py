@@ -58,7 +58,8 @@ def test_gpu_matches_reference_golden(cuda_ok, name):
 
 
 @pytest.mark.parametrize("d,L,p,steps,seed", [(3, 2, 3, 3, 7), (2, 2, 4, 6, 3), (3, 1, 4, 4, 11),
-                                              (2, 2, 7, 3, 5), (3, 2, 5, 2, 1)])
+                                              (2, 2, 7, 3, 5), (3, 2, 5, 2, 1), (3, 1, 6, 3, 2),
+                                              (3, 1, 7, 3, 4), (3, 1, 8, 2, 6), (3, 1, 9, 2, 8)])
 def test_gpu_matches_oracle_random_seeds(cuda_ok, d, L, p, steps, seed):
     Q0 = scenarios.build("bump", d, L, p, seed=seed, noise=1e-2)
     drv = make_driver(Q0, d, L, p)
