@@ -18,6 +18,7 @@
 #include "aderdg_kernels.cuh"
 #include "aderdg_sweep_v2.cuh"
 #include "aderdg_sweep_ho.cuh"
+#include "aderdg_sweep_st.cuh"
 
 using namespace adg;
 
@@ -68,6 +69,20 @@ void launch_sweep_ho(const SweepParams& P, unsigned grid, cudaStream_t s) {
   sweep_kernel_ho<NQ><<<grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
 }
 
+void launch_sweep_st(const SweepParams& P, unsigned grid, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sweep_kernel_st, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ShapeST::SMEM_BYTES);
+    attr = true;
+  }
+  sweep_kernel_st<<<grid, ShapeST::THREADS, ShapeST::SMEM_BYTES, s>>>(P);
+}
+
+Dispatch make_dispatch_st() {
+  static_assert(ShapeST::REC == Shape<3, 4>::REC, "record layout must match");
+  return Dispatch{&launch_sweep_st, ShapeST::REC};
+}
+
 template <int NQ>
 Dispatch make_dispatch_ho() {
   static_assert(ShapeHO<NQ>::REC == Shape<3, NQ>::REC, "record layout must match");
@@ -109,7 +124,8 @@ bool dispatch_for(int d, int p, Dispatch* out) {
       case 4:
         *out = kernel_variant() == 1 ? make_dispatch<3, 4>()
              : kernel_variant() == 2 ? make_dispatch_v2<4, 2, true>()
-             : kernel_variant() == 5 ? make_dispatch_v2<4, 1, true, true>() : make_dispatch_v2<4, 1, true, false>();
+             : kernel_variant() == 5 ? make_dispatch_v2<4, 1, true, true>()
+             : kernel_variant() == 6 ? make_dispatch_st() : make_dispatch_v2<4, 1, true, false>();
         return true;
       case 5: *out = make_dispatch<3, 5>(); return true;
       case 6:
