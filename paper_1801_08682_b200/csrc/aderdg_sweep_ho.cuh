@@ -40,12 +40,16 @@ struct ShapeHO {
   static constexpr int RR = NF * M;                          // GEMM columns per axis
   static constexpr int NT = (RR + 7) / 8;                    // n-tiles
   static constexpr int RP = NT * 8;
-  static constexpr int JS = 12;                              // row stride of the B staging
+  // padded natural node layout [c][SC] (brute-forced: stores, DMMA B loads and
+  // C scatters of every axis are at most 3-way bank conflicted)
+  static constexpr int P1 = (NQ == 10) ? 13 : 11;
+  static constexpr int P0 = (NQ == 7) ? 77 : (NQ == 8) ? 91 : (NQ == 9) ? 107 : 131;
+  static constexpr int SC = (NQ == 7) ? 541 : (NQ == 8) ? 729 : (NQ == 9) ? 965 : 1311;
   static constexpr int REC = 2 * NF * M + 2;
   // shared memory (doubles)
   static constexpr int R_RED = 2 * NW + 2 * DIM + 4;
-  static constexpr int R_FA = RP * JS;                       // B staging of one axis
-  static constexpr int R_DV = M * NS;                        // derivative accumulator
+  static constexpr int R_FA = M * SC;                        // flux of one axis (padded natural layout)
+  static constexpr int R_DV = M * SC;                        // derivative accumulator (same layout)
   static constexpr int R_NODE = M * NS;                      // per-node staging (q_t / qbar / fbar_a / D / Q)
   static constexpr int R_FACE = 2 * DIM * NF * M;
   static constexpr int OFF_RED = 0;
@@ -62,13 +66,13 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
   using S = ShapeHO<NQ>;
   constexpr int DIM = 3, M = 5, NS = S::NS, NF = S::NF, NPT = S::NPT, REC = S::REC;
   constexpr int THREADS = S::THREADS, NW = S::NW, KC = S::KC, MT = S::MT, NT = S::NT;
-  constexpr int RR = S::RR, JS = S::JS;
+  constexpr int RR = S::RR, SC = S::SC, P0 = S::P0, P1 = S::P1;
 
   extern __shared__ __align__(16) double smem[];
   double* sRed = smem + S::OFF_RED;
   unsigned long long* sSmax = reinterpret_cast<unsigned long long*>(sRed + 2 * NW);
-  double* sFA = smem + S::OFF_FA;     // [RP][JS]
-  double* sDv = smem + S::OFF_DV;     // [M][NS]
+  double* sFA = smem + S::OFF_FA;     // [M][SC] flux of the current axis
+  double* sDv = smem + S::OFF_DV;     // [M][SC] spatial divergence of the current slice
   double* sN = smem + S::OFF_NODE;    // [M][NS] node staging
   double* sFace = smem + S::OFF_FACE;
 
@@ -100,6 +104,15 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
   auto idx3 = [](int x, int& i0, int& i1, int& i2) {
     i0 = x / (NQ * NQ); i1 = (x / NQ) % NQ; i2 = x % NQ;
   };
+
+  auto pad = [](int i0, int i1, int i2) { return i0 * P0 + i1 * P1 + i2; };
+  int pn[NPT];
+#pragma unroll
+  for (int n = 0; n < NPT; ++n) {
+    int a0, a1, a2;
+    idx3(xn[n], a0, a1, a2);
+    pn[n] = pad(a0, a1, a2);
+  }
 
   double Qx[NPT][M];
 #pragma unroll
@@ -221,8 +234,6 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
   const double tol = 1e-10 * (1.0 + block_max<NW>(am, sRed));
   const int cap = 2 * NQ;
 
-  // zero the padding of the B staging once (rows >= RR, columns >= NQ)
-  for (int e = tid; e < S::R_FA; e += THREADS) sFA[e] = 0.0;
   // constant A fragments: A[i'][j] = diff[i'][j]; lane holds A[mt*8 + g][kc*4 + t4]
   double afr[MT][KC];
   {
@@ -255,31 +266,35 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
       }
 #pragma unroll 1
       for (int a = 0; a < DIM; ++a) {
-        // stage F_a with the contraction index (i_a) fastest: row r = (ib, ic, c)
+        // stage F_a in the padded natural layout
 #pragma unroll
         for (int n = 0; n < NPT; ++n) {
           if (!an[n]) continue;
-          int i[3];
-          idx3(xn[n], i[0], i[1], i[2]);
-          const int ib = (a == 0) ? i[1] : i[0];
-          const int ic = (a == 2) ? i[1] : i[2];
-          const int ia = i[a];
 #pragma unroll
           for (int c = 0; c < M; ++c) {
             const double v = (a == 0) ? F[n][0][c] : (a == 1) ? F[n][1][c] : F[n][2][c];
-            sFA[((ib * NQ + ic) * M + c) * JS + ia] = v;
+            sFA[c * SC + pn[n]] = v;
           }
         }
         __syncthreads();
+        // strides of the contraction axis and of the two other axes (ib < ic in axis order)
+        const int sa = (a == 0) ? P0 : (a == 1) ? P1 : 1;
+        const int sb = (a == 0) ? P1 : P0;
+        const int sc2 = (a == 2) ? P1 : 1;
         // GEMM tiles: warp w takes n-tiles w, w+NW, ...
         for (int nt = warp; nt < NT; nt += NW) {
           double cacc[MT][2];
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt) { cacc[mt][0] = 0.0; cacc[mt][1] = 0.0; }
-          const double* brow = sFA + (nt * 8 + (lane >> 2)) * JS + (lane & 3);
+          // B[j][r]: r = c*NF + (ib*NQ + ic); columns past RR and rows past NQ read a
+          // finite in-range value (their A entries / outputs are zero / discarded)
+          const int rb = min(nt * 8 + (lane >> 2), RR - 1);
+          const int cb = rb / NF, yb = rb % NF;
+          const double* bbase = sFA + cb * SC + (yb / NQ) * sb + (yb % NQ) * sc2;
 #pragma unroll
           for (int kc = 0; kc < KC; ++kc) {
-            const double b = brow[kc * 4];
+            const int jj = min(kc * 4 + (lane & 3), NQ - 1);
+            const double b = bbase[jj * sa];
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt)
               dmma_8x8x4(cacc[mt][0], cacc[mt][1], afr[mt][kc], b, cacc[mt][0], cacc[mt][1]);
@@ -292,11 +307,10 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
               const int ip = mt * 8 + (lane >> 2);
               const int r = nt * 8 + 2 * (lane & 3) + e2;
               if (ip < NQ && r < RR) {
-                const int c = r % M, bc = r / M, ib = bc / NQ, ic = bc % NQ;
-                const int x = (a == 0) ? (ip * NQ + ib) * NQ + ic
-                            : (a == 1) ? (ib * NQ + ip) * NQ + ic : (ib * NQ + ic) * NQ + ip;
-                if (a == 0) sDv[c * NS + x] = cacc[mt][e2];
-                else sDv[c * NS + x] += cacc[mt][e2];
+                const int c = r / NF, y = r % NF;
+                const int ad = c * SC + ip * sa + (y / NQ) * sb + (y % NQ) * sc2;
+                if (a == 0) sDv[ad] = cacc[mt][e2];
+                else sDv[ad] += cacc[mt][e2];
               }
             }
         }
@@ -305,7 +319,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
 #pragma unroll
       for (int n = 0; n < NPT; ++n)
 #pragma unroll
-        for (int c = 0; c < M; ++c) dh[n][k][c] = sDv[c * NS + xn[n]];
+        for (int c = 0; c < M; ++c) dh[n][k][c] = sDv[c * SC + pn[n]];
     }
     // time contraction + Picard update per node
     double dmax = 0.0, dsum = 0.0;
