@@ -54,7 +54,7 @@ struct ShapeV2 {
   static constexpr int P1T = NQ * NQ + 2;              // its plane stride (odd number of 16-byte chunks)
   static constexpr int REC = 2 * NF * M + 2;
   // shared memory (doubles), all region sizes even (16-byte alignment)
-  static constexpr int R_RED = 2 * NWARPS + 2 * DIM + 4;
+  static constexpr int R_RED = 3 * NWARPS + 2 * DIM + 4;   // block_max | s_max | convergence flags
   static constexpr int R_Q = NS * M;
   static constexpr int R_REC = 4 * DIM * REC;
   static constexpr int R_F = TS * DS * M * PS;
@@ -153,6 +153,7 @@ sweep_kernel_v2(const SweepParams P) {
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR);
   double* sRed = smem + S::OFF_RED;
   unsigned long long* sSmax = reinterpret_cast<unsigned long long*>(sRed + 2 * NW);
+  unsigned* sFlags = reinterpret_cast<unsigned*>(sRed + 2 * NW + 2 * 3);
   double* sQ = smem + S::OFF_Q;
   double* sD = smem + S::OFF_D;
   double* sU = smem + S::OFF_U;
@@ -448,24 +449,23 @@ sweep_kernel_v2(const SweepParams P) {
       }
       // Picard update; max |q_new - q| via the bit patterns of non-negative
       // doubles (NaN/inf patterns sort above every finite value)
-      // max |q_new - q| (fmax drops NaN, so a running sum of the same
-      // differences carries any inf/NaN into the finiteness test)
-      double dmax = 0.0, dsum = 0.0;
+      // converged iff every |q_new - q| <= tol; a running sum carries inf/NaN
+      bool conv = true;
+      double dsum = 0.0;
 #pragma unroll
       for (int t = 0; t < NQ; ++t)
 #pragma unroll
         for (int c = 0; c < M; ++c) {
           const double qn = Qx[c] - scale * acc[t][c];
           const double dd = fabs(qn - q[t][c]);
-          dmax = fmax(dmax, dd);
+          conv = conv && (dd <= tol);
           dsum += dd;
           q[t][c] = qn;
         }
       iters = it + 1;
-      const bool bad = !finite(dsum);
-      if (__syncthreads_or(act && bad)) { failed = true; break; }
-      const double delta = block_max<NW>(act ? dmax : 0.0, sRed);
-      if (delta <= tol) break;
+      const int fl = block_flags<NW>(!act || conv, act && !finite(dsum), sFlags, it & 1);
+      if (fl & 2) { failed = true; break; }
+      if (fl & 1) break;
     }
   } else {
   for (int it = 0; it < cap; ++it) {
@@ -532,7 +532,8 @@ sweep_kernel_v2(const SweepParams P) {
       }
       if (!(TS == 1 && S::DBUF)) __syncthreads();
     }
-    unsigned long long dbits = 0ull;
+    bool conv = true;
+    double dsum = 0.0;
 #pragma unroll
     for (int c = 0; c < M; ++c) {
       double dvk[NQ];
@@ -551,16 +552,16 @@ sweep_kernel_v2(const SweepParams P) {
           for (int k = 0; k < NQ; ++k) acc = fma(P.ops.integ[t][k], dvk[k], acc);
         }
         const double qn = Qx[c] - scale * acc;
-        const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(qn - q[s][c]));
-        dbits = b > dbits ? b : dbits;
+        const double dd = fabs(qn - q[s][c]);
+        conv = conv && (dd <= tol);
+        dsum += dd;
         q[s][c] = qn;
       }
     }
     iters = it + 1;
-    const bool bad = dbits >= 0x7ff0000000000000ull;
-    if (__syncthreads_or(act && bad)) { failed = true; break; }
-    const double delta = block_max<NW>(act ? __longlong_as_double((long long)dbits) : 0.0, sRed);
-    if (delta <= tol) break;
+    const int fl = block_flags<NW>(!act || conv, act && !finite(dsum), sFlags, it & 1);
+    if (fl & 2) { failed = true; break; }
+    if (fl & 1) break;
   }
   }
 
@@ -685,7 +686,11 @@ sweep_kernel_v2(const SweepParams P) {
 
   // ---------------- s_max over the space-time face traces ----------------
   // tasks per face axis a (compile-time): (side, t, face node y), y fastest, so a
-  // warp gathers whole face planes with one address formula
+  // warp gathers whole face planes with one address formula; per-thread maxima
+  // are reduced over the warp and merged with one shared atomic per warp and side
+  double smx[2 * DIM];
+#pragma unroll
+  for (int f = 0; f < 2 * DIM; ++f) smx[f] = 0.0;
 #pragma unroll
   for (int a = 0; a < DIM; ++a) {
     for (int e = tid; e < 2 * NQ * NF; e += THREADS) {
@@ -705,8 +710,20 @@ sweep_kernel_v2(const SweepParams P) {
       }
       bool adm;
       const double sp = max_speed_fast<DIM>(qs, a, a + 1, adm);
-      atomicMax(&sSmax[2 * a + side], (unsigned long long)__double_as_longlong(sp));
+      // NaN must win the max like the reference's np.max: compare bit patterns
+      if (side) smx[2 * a + 1] = (__double_as_longlong(sp) > __double_as_longlong(smx[2 * a + 1])) ? sp : smx[2 * a + 1];
+      else smx[2 * a] = (__double_as_longlong(sp) > __double_as_longlong(smx[2 * a])) ? sp : smx[2 * a];
     }
+  }
+#pragma unroll
+  for (int f = 0; f < 2 * DIM; ++f) {
+    unsigned long long v = (unsigned long long)__double_as_longlong(smx[f]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+      v = w > v ? w : v;
+    }
+    if ((tid & 31) == 0) atomicMax(&sSmax[f], v);
   }
   __syncthreads();
   if (tid == 0) {
