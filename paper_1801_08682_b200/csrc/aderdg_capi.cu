@@ -38,16 +38,16 @@ void launch_sweep(const SweepParams& P, unsigned grid, cudaStream_t s) {
   sweep_kernel<DIM, NQ><<<grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
 }
 
-template <int NQ, int TS, bool DMMA, bool ROLLED = (NQ == 4)>
+template <int NQ, int TS, bool DMMA, bool ROLLED = (NQ == 4), int MB = 0>
 void launch_sweep_v2(const SweepParams& P, unsigned grid, cudaStream_t s) {
-  using S = ShapeV2<NQ, TS, DMMA, ROLLED>;
+  using S = ShapeV2<NQ, TS, DMMA, ROLLED, MB>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(sweep_kernel_v2<NQ, TS, DMMA, ROLLED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(sweep_kernel_v2<NQ, TS, DMMA, ROLLED, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)S::SMEM_BYTES);
     attr = true;
   }
-  sweep_kernel_v2<NQ, TS, DMMA, ROLLED><<<grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
+  sweep_kernel_v2<NQ, TS, DMMA, ROLLED, MB><<<grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
 }
 
 struct Dispatch {
@@ -89,10 +89,10 @@ Dispatch make_dispatch_ho() {
   return Dispatch{&launch_sweep_ho<NQ>, ShapeHO<NQ>::REC};
 }
 
-template <int NQ, int TS, bool DMMA, bool ROLLED = (NQ == 4)>
+template <int NQ, int TS, bool DMMA, bool ROLLED = (NQ == 4), int MB = 0>
 Dispatch make_dispatch_v2() {
-  static_assert(ShapeV2<NQ, TS, DMMA, ROLLED>::REC == Shape<3, NQ>::REC, "record layout must match");
-  return Dispatch{&launch_sweep_v2<NQ, TS, DMMA, ROLLED>, ShapeV2<NQ, TS, DMMA, ROLLED>::REC};
+  static_assert(ShapeV2<NQ, TS, DMMA, ROLLED, MB>::REC == Shape<3, NQ>::REC, "record layout must match");
+  return Dispatch{&launch_sweep_v2<NQ, TS, DMMA, ROLLED, MB>, ShapeV2<NQ, TS, DMMA, ROLLED, MB>::REC};
 }
 
 int kernel_variant() {
@@ -125,12 +125,15 @@ bool dispatch_for(int d, int p, Dispatch* out) {
         *out = kernel_variant() == 1 ? make_dispatch<3, 4>()
              : kernel_variant() == 2 ? make_dispatch_v2<4, 2, true>()
              : kernel_variant() == 5 ? make_dispatch_v2<4, 1, true, true>()
-             : kernel_variant() == 6 ? make_dispatch_st() : make_dispatch_v2<4, 1, true, false>();
+             : kernel_variant() == 6 ? make_dispatch_st()
+             : kernel_variant() == 7 ? make_dispatch_v2<4, 1, true, false, 7>()
+             : kernel_variant() == 8 ? make_dispatch_v2<4, 1, true, false, 8>() : make_dispatch_v2<4, 1, true, false>();
         return true;
       case 5: *out = make_dispatch<3, 5>(); return true;
       case 6:
         *out = kernel_variant() == 1 ? make_dispatch<3, 6>()
-             : kernel_variant() == 2 ? make_dispatch_v2<6, 2, false>() : make_dispatch_v2<6, 1, false>();
+             : kernel_variant() == 2 ? make_dispatch_v2<6, 2, false>()
+             : kernel_variant() == 9 ? make_dispatch_v2<6, 1, false, false, 9>() : make_dispatch_v2<6, 1, false>();
         return true;
       // p >= 6: time line in local memory, spatial derivatives as DMMA GEMMs
       case 7: *out = kernel_variant() == 1 ? make_dispatch<3, 7>() : make_dispatch_ho<7>(); return true;

@@ -32,7 +32,7 @@ __host__ __device__ constexpr int plane_pad(int nq) {
          : (((nq * nq + 6) % 16 >= nq && (nq * nq + 6) % 16 <= 16 - nq) ? 6 : 8)));
 }
 
-template <int NQ, int TS, bool DMMA, bool ROLLED = (NQ == 4)>
+template <int NQ, int TS, bool DMMA, bool ROLLED = (NQ == 4), int MINB_OVERRIDE = 0>
 struct ShapeV2 {
   static constexpr int DIM = 3, M = 5;
   static constexpr int NS = NQ * NQ * NQ;
@@ -42,15 +42,16 @@ struct ShapeV2 {
   static constexpr int NWARPS = THREADS / 32;
   static constexpr int TH = NQ / TS;
   // CTAs/SM the register allocation must allow (TS = 1 at NQ = 6 keeps 60 doubles of Picard state)
-  static constexpr int MINB = (TS == 1 && NQ >= 6) ? 1
+  static constexpr int MINB = (MINB_OVERRIDE && MINB_OVERRIDE != 9) ? MINB_OVERRIDE : (MINB_OVERRIDE == 9) ? 1
+                            : (TS == 1 && NQ >= 6) ? 1
                             : THREADS <= 64 ? 6 : THREADS <= 128 ? 4 : (THREADS <= 256 ? 2 : 1);
   static constexpr int P0 = NQ * NQ + plane_pad(NQ);   // padded axis-0 plane stride
   static constexpr int PS = NQ * P0;                   // padded slice size
   static constexpr int DS = DMMA ? DIM - 1 : DIM;      // axes through shared memory
-  static constexpr bool F1T = (NQ == 4);               // axis-1 flux stored transposed, 16-byte gathers
+  static constexpr bool F1T = (NQ == 4) || (NQ == 6 && MINB_OVERRIDE == 9);  // axis-1 flux stored transposed, 16-byte gathers
   static constexpr bool ROLL = ROLLED;                 // rolled slice loop (i-cache); NQ = 6 stays unrolled
   static constexpr int RR = 1;                         // slices per rolled trip
-  static constexpr bool DBUF = (TS == 1 && NQ == 4);   // double-buffered flux slices (one barrier per slice)
+  static constexpr bool DBUF = (TS == 1 && (NQ == 4 || MINB_OVERRIDE == 9));  // double-buffered flux slices
   static constexpr int P1T = NQ * NQ + 2;              // its plane stride (odd number of 16-byte chunks)
   static constexpr int REC = 2 * NF * M + 2;
   // shared memory (doubles), all region sizes even (16-byte alignment)
@@ -141,10 +142,10 @@ __device__ __forceinline__ int trace_addr(int i0, int i1, int i2) {
   return (i0 * NQ + i1) * NQ + i2;
 }
 
-template <int NQ, int TS, bool DMMA, bool ROLLED = (NQ == 4)>
-__global__ void __launch_bounds__(ShapeV2<NQ, TS, DMMA, ROLLED>::THREADS, ShapeV2<NQ, TS, DMMA, ROLLED>::MINB)
+template <int NQ, int TS, bool DMMA, bool ROLLED = (NQ == 4), int MB = 0>
+__global__ void __launch_bounds__(ShapeV2<NQ, TS, DMMA, ROLLED, MB>::THREADS, ShapeV2<NQ, TS, DMMA, ROLLED, MB>::MINB)
 sweep_kernel_v2(const SweepParams P) {
-  using S = ShapeV2<NQ, TS, DMMA, ROLLED>;
+  using S = ShapeV2<NQ, TS, DMMA, ROLLED, MB>;
   constexpr int DIM = 3, M = 5, NS = S::NS, NF = S::NF, NSP = S::NSP, REC = S::REC;
   constexpr int THREADS = S::THREADS, NW = S::NWARPS, TH = S::TH, P0 = S::P0, PS = S::PS;
   constexpr int DS = S::DS;
