@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
     }
     __syncthreads();
     // ------------- integrate_face + update (kernels.py:183-214) -------------
-    const double scale_old = st->dt_old / P.h;
+    const double scale_old = st->scale_old;
 #pragma unroll
     for (int n = 0; n < NPT; ++n) {
       if (!an[n]) continue;
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
 
   // ---------------- predictor (kernels.py:68-105) ----------------
   const double dt = (mode == MODE_RERUN) ? st->dt_old : st->dt_new;
-  const double scale = dt / P.h;
+  const double scale = (mode == MODE_RERUN) ? st->scale_old : st->scale_new;   // dt / h
   double am = 0.0;
 #pragma unroll
   for (int n = 0; n < NPT; ++n)
@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
     }
   }
   {
-    const double sdt = dt / P.h;
+    const double sdt = scale;
 #pragma unroll
     for (int n = 0; n < NPT; ++n)
       if (an[n])

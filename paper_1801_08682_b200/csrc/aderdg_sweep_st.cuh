@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(256, 3) sweep_kernel_st(const SweepParams P) {
       double Dx[M];
 #pragma unroll
       for (int c = 0; c < M; ++c) Dx[c] = sD[x * M + c];
-      const double scale_old = st->dt_old / P.h;
+      const double scale_old = st->scale_old;
       const int idx[3] = {i0, i1, i2};
 #pragma unroll
       for (int a = 0; a < DIM; ++a) {
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(256, 3) sweep_kernel_st(const SweepParams P) {
 
   // ---------------- predictor (kernels.py:68-105) ----------------
   const double dt = (mode == MODE_RERUN) ? st->dt_old : st->dt_new;
-  const double scale = dt / P.h;
+  const double scale = (mode == MODE_RERUN) ? st->scale_old : st->scale_new;   // dt / h
   double absmax;
   {
     double am = 0.0;
@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(256, 3) sweep_kernel_st(const SweepParams P) {
 
   // ---------------- integrate_volume (kernels.py:130-143): lane t takes components t, t+4 ----------------
   {
-    const double sdt = dt / P.h;
+    const double sdt = scale;
     const int idx[3] = {i0, i1, i2};
     for (int c = t; c < M; c += 4) {
       double s = 0.0;

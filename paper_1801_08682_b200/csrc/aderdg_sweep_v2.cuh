@@ -245,7 +245,7 @@ sweep_kernel_v2(const SweepParams P) {
       double Dx[M];
 #pragma unroll
       for (int c = 0; c < M; ++c) Dx[c] = sD[x * M + c];
-      const double scale_old = st->dt_old / P.h;
+      const double scale_old = st->scale_old;
       const int idx[3] = {i0, i1, i2};
 #pragma unroll
       for (int a = 0; a < DIM; ++a) {
@@ -317,8 +317,7 @@ sweep_kernel_v2(const SweepParams P) {
   }
 
   // ---------------- predictor (kernels.py:68-105) ----------------
-  const double dt = (mode == MODE_RERUN) ? st->dt_old : st->dt_new;
-  const double scale = dt / P.h;
+  const double scale = (mode == MODE_RERUN) ? st->scale_old : st->scale_new;   // dt / h
   double absmax;
   {
     double am = 0.0;
@@ -471,6 +470,7 @@ sweep_kernel_v2(const SweepParams P) {
   } else {
   for (int it = 0; it < cap; ++it) {
     double accr[TS == 1 ? NQ : 1][M];            // register time contraction (TS == 1)
+    double dvp[M];                               // pending slice (DBUF: deferred contraction)
 #pragma unroll
     for (int s = 0; s < TH; ++s) {
       const int k = ts * TH + s;
@@ -485,6 +485,14 @@ sweep_kernel_v2(const SweepParams P) {
 #pragma unroll
           for (int c = 0; c < M; ++c)
             sFs[(a * M + c) * PS + ((S::F1T && a == 1) ? p1t : px)] = F[a][c];
+      }
+      if (TS == 1 && S::DBUF && s > 0) {
+        // time contraction of the previous slice, deferred past its DMMA latency
+#pragma unroll
+        for (int t = 0; t < (TS == 1 ? NQ : 1); ++t)
+#pragma unroll
+          for (int c = 0; c < M; ++c)
+            accr[t][c] = (k == 1) ? P.ops.integ[t][0] * dvp[c] : fma(P.ops.integ[t][k - 1], dvp[c], accr[t][c]);
       }
       __syncthreads();
       double dv[M];
@@ -521,7 +529,10 @@ sweep_kernel_v2(const SweepParams P) {
           dmma_8x8x4(dv[c], d1, F[2][c], bfrag, dv[c], 0.0);
         }
       }
-      if (TS == 1) {
+      if (TS == 1 && S::DBUF) {
+#pragma unroll
+        for (int c = 0; c < M; ++c) dvp[c] = dv[c];
+      } else if (TS == 1) {
 #pragma unroll
         for (int t = 0; t < (TS == 1 ? NQ : 1); ++t)
 #pragma unroll
@@ -532,6 +543,12 @@ sweep_kernel_v2(const SweepParams P) {
         for (int c = 0; c < M; ++c) sDiv[(k * M + c) * NSP + x] = dv[c];
       }
       if (!(TS == 1 && S::DBUF)) __syncthreads();
+    }
+    if (TS == 1 && S::DBUF) {
+#pragma unroll
+      for (int t = 0; t < (TS == 1 ? NQ : 1); ++t)
+#pragma unroll
+        for (int c = 0; c < M; ++c) accr[t][c] = fma(P.ops.integ[t][NQ - 1], dvp[c], accr[t][c]);
     }
     bool conv = true;
     double dsum = 0.0;
@@ -658,7 +675,7 @@ sweep_kernel_v2(const SweepParams P) {
 
   // ---------------- integrate_volume (kernels.py:130-143) ----------------
   if (ts == 0 && act) {
-    const double sdt = dt / P.h;
+    const double sdt = scale;
     const int idx[3] = {i0, i1, i2};
 #pragma unroll
     for (int c = 0; c < M; ++c) {
@@ -718,12 +735,7 @@ sweep_kernel_v2(const SweepParams P) {
   }
 #pragma unroll
   for (int f = 0; f < 2 * DIM; ++f) {
-    unsigned long long v = (unsigned long long)__double_as_longlong(smx[f]);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      const unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
-      v = w > v ? w : v;
-    }
+    const unsigned long long v = warp_max_u64((unsigned long long)__double_as_longlong(smx[f]));
     if ((tid & 31) == 0) atomicMax(&sSmax[f], v);
   }
   __syncthreads();
