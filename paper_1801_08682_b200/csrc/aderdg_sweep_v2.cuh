@@ -219,6 +219,32 @@ sweep_kernel_v2(const SweepParams P) {
       }
     }
   }
+  // predictor setup that needs no cell data, while the bulk copies land
+  // derivative rows of the shared-memory axes; DMMA B fragment for axis 2
+  double drow[DS][NQ];
+  {
+    const int idx[3] = {i0, i1, i2};
+#pragma unroll
+    for (int a = 0; a < DS; ++a)
+#pragma unroll
+      for (int j = 0; j < NQ; ++j) drow[a][j] = P.ops.diff[idx[a]][j];
+  }
+  double bfrag = 0.0;
+  if (DMMA) {
+    const int lane = tid & 31;
+    const int g = lane >> 2, t4 = lane & 3;      // B[k=t4][n=g]: n even -> diff[n/2][k]
+    bfrag = (g & 1) ? 0.0 : P.ops.diff[g >> 1][t4];
+  }
+  // padded gather bases for the shared-memory axes
+  int gbase[DIM], gstr[DIM];
+  gbase[0] = px - i0 * P0; gstr[0] = P0;
+  gbase[1] = px - i1 * NQ; gstr[1] = NQ;
+  gbase[2] = px - i2;      gstr[2] = 1;
+  // F1T: axis-1 flux stored with i1 fastest (plane stride P1T), gathered as
+  // 16-byte pairs; 8 distinct 16-byte chunks per warp -> one wavefront.
+  const int p1t = i0 * S::P1T + i2 * NQ + i1;
+  const int g1t = i0 * S::P1T + i2 * NQ;
+
   mbar_wait(bar, 0);
 
   double Qx[M];
@@ -327,31 +353,6 @@ sweep_kernel_v2(const SweepParams P) {
   }
   const double tol = 1e-10 * (1.0 + absmax);
   const int cap = 2 * NQ;
-
-  // derivative rows of the shared-memory axes; DMMA B fragment for axis 2
-  double drow[DS][NQ];
-  {
-    const int idx[3] = {i0, i1, i2};
-#pragma unroll
-    for (int a = 0; a < DS; ++a)
-#pragma unroll
-      for (int j = 0; j < NQ; ++j) drow[a][j] = P.ops.diff[idx[a]][j];
-  }
-  double bfrag = 0.0;
-  if (DMMA) {
-    const int lane = tid & 31;
-    const int g = lane >> 2, t4 = lane & 3;      // B[k=t4][n=g]: n even -> diff[n/2][k]
-    bfrag = (g & 1) ? 0.0 : P.ops.diff[g >> 1][t4];
-  }
-  // padded gather bases for the shared-memory axes
-  int gbase[DIM], gstr[DIM];
-  gbase[0] = px - i0 * P0; gstr[0] = P0;
-  gbase[1] = px - i1 * NQ; gstr[1] = NQ;
-  gbase[2] = px - i2;      gstr[2] = 1;
-  // F1T: axis-1 flux stored with i1 fastest (plane stride P1T), gathered as
-  // 16-byte pairs; 8 distinct 16-byte chunks per warp -> one wavefront.
-  const int p1t = i0 * S::P1T + i2 * NQ + i1;
-  const int g1t = i0 * S::P1T + i2 * NQ;
 
   double q[TH][M];
 #pragma unroll
