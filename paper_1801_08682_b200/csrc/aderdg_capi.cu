@@ -98,7 +98,7 @@ Dispatch make_dispatch_v2() {
 int kernel_variant() {
   // ADG_KERNEL=1: first-generation kernel; 2: time-split v2; 3 (default): v2 without time split
   const char* v = getenv("ADG_KERNEL");
-  return v ? (v[0] - '0') : 3;
+  return v ? atoi(v) : 3;
 }
 
 bool dispatch_for(int d, int p, Dispatch* out) {
