@@ -52,12 +52,19 @@ struct ShapeHO {
   static constexpr int R_DV = M * SC;                        // derivative accumulator (same layout)
   static constexpr int R_NODE = M * NS;                      // per-node staging (q_t / qbar / fbar_a / D / Q)
   static constexpr int R_FACE = 2 * DIM * NF * M;
+  // divergence history dh[k][c][x] of the Picard iteration: in shared memory when
+  // it fits next to the GEMM buffers (n <= 8), aliasing the corrector (sFace) and
+  // tail (sN) buffers, otherwise in thread-private local memory
+  static constexpr int R_DH = NQ * M * THREADS * NPT;
+  static constexpr bool DH_SMEM = (NQ <= 8);
+  static constexpr int R_ALIAS = DH_SMEM ? R_DH : (R_NODE + R_FACE);
   static constexpr int OFF_RED = 0;
   static constexpr int OFF_FA = (R_RED + 1) & ~1;
   static constexpr int OFF_DV = OFF_FA + R_FA;
   static constexpr int OFF_NODE = OFF_DV + R_DV;
   static constexpr int OFF_FACE = OFF_NODE + R_NODE;
-  static constexpr int TOTAL = OFF_FACE + R_FACE;
+  static constexpr int OFF_DH = OFF_NODE;
+  static constexpr int TOTAL = OFF_NODE + (R_ALIAS > R_NODE + R_FACE ? R_ALIAS : R_NODE + R_FACE);
   static constexpr size_t SMEM_BYTES = sizeof(double) * TOTAL;
 };
 
@@ -75,6 +82,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
   double* sDv = smem + S::OFF_DV;     // [M][SC] spatial divergence of the current slice
   double* sN = smem + S::OFF_NODE;    // [M][NS] node staging
   double* sFace = smem + S::OFF_FACE;
+  double* sDH = smem + S::OFF_DH;     // [k][c][THREADS*NPT] (DH_SMEM)
 
   DevState* st = P.st;
   if (st->status != 0) return;
@@ -248,7 +256,11 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
   }
   // per-node time line in thread-private (local) memory
   double qo[NPT][NQ][M];
-  double dh[NPT][NQ][M];
+  double dh[S::DH_SMEM ? 1 : NPT][S::DH_SMEM ? 1 : NQ][M];
+  auto dhp = [&](int n, int k, int c) -> double& {
+    if constexpr (S::DH_SMEM) return sDH[(k * M + c) * (THREADS * NPT) + n * THREADS + tid];
+    else return dh[n][k][c];
+  };
   int iters = 0;
   bool failed = false;
   __syncthreads();
@@ -319,7 +331,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
 #pragma unroll
       for (int n = 0; n < NPT; ++n)
 #pragma unroll
-        for (int c = 0; c < M; ++c) dh[n][k][c] = sDv[c * SC + pn[n]];
+        for (int c = 0; c < M; ++c) dhp(n, k, c) = sDv[c * SC + pn[n]];
     }
     // time contraction + Picard update per node
     double dmax = 0.0, dsum = 0.0;
@@ -331,7 +343,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
         for (int c = 0; c < M; ++c) {
           double acc = 0.0;
 #pragma unroll
-          for (int k = 0; k < NQ; ++k) acc = fma(P.ops.integ[t][k], dh[n][k][c], acc);
+          for (int k = 0; k < NQ; ++k) acc = fma(P.ops.integ[t][k], dhp(n, k, c), acc);
           const double qn = Qx[n][c] - scale * acc;
           const double qold = (it == 0) ? Qx[n][c] : qo[n][t][c];
           const double dd = fabs(qn - qold);
