@@ -73,6 +73,7 @@ typedef struct {
   int device;            /* CUDA device ordinal                            */
   int rank;              /* slab index (0 for a single GPU)                */
   int world;             /* number of slabs along axis 0 (1 = periodic in place) */
+  int halo_mode;         /* 0: halo slots iff world > 1; 1: always (world = 1 then exchanges with itself) */
 } adg_config;
 
 typedef struct {

@@ -39,7 +39,7 @@ class AdgConfig(ctypes.Structure):
         ("creeping", ctypes.c_int), ("forced_dt", ctypes.c_double),
         ("inject_rerun", ctypes.c_int), ("spike_step", ctypes.c_int),
         ("spike_factor", ctypes.c_double), ("device", ctypes.c_int),
-        ("rank", ctypes.c_int), ("world", ctypes.c_int),
+        ("rank", ctypes.c_int), ("world", ctypes.c_int), ("halo_mode", ctypes.c_int),
     ]
 
 

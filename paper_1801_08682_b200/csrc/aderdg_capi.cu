@@ -216,7 +216,7 @@ static SweepParams sweep_params(adg_handle* h, int mode) {
   P.planes_local = h->planes_local;
   P.plane_cells = h->plane_cells;
   P.cell_offset = (int)(h->plane0 * (long long)h->plane_cells);
-  P.halo = h->cfg.world > 1 ? 1 : 0;
+  P.halo = (h->cfg.world > 1 || h->cfg.halo_mode == 1) ? 1 : 0;
   P.spike_step = h->cfg.spike_step;
   P.p = h->cfg.p;
   P.h = h->h;

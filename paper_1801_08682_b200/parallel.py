@@ -47,6 +47,7 @@ class HaloExchange:
         # staged: device tensors go through host copies (gloo transport; used to
         # test the multi-slab device path with several ranks on one GPU)
         self.staged = staged
+        self.force = False          # exchange even at world = 1 (self send/recv; halo test mode)
 
     def views(self, tr):
         """tr: tensor (2d, slots, REC).  Returns (send_to_prev, recv_from_prev,
@@ -60,7 +61,7 @@ class HaloExchange:
 
     def exchange(self, tr):
         import torch.distributed as dist
-        if self.world == 1:
+        if self.world == 1 and not self.force:
             return
         send_prev, recv_prev, send_next, recv_next = self.views(tr)
         if self.staged:
@@ -102,7 +103,7 @@ class SlabDriver:
 
     def __init__(self, Q_global, d, L, p, rank, world, device, cfl=0.9, c_dt=0.99,
                  averaging="strict", forced_dt=None, inject_rerun=False,
-                 spike_step=None, spike_factor=3.0, group=None, staged=False):
+                 spike_step=None, spike_factor=3.0, group=None, staged=False, halo_mode=0):
         import torch
         from .basis import make_basis
         from .solver import upload_operators
@@ -119,6 +120,7 @@ class SlabDriver:
         cfg.spike_step = -1 if spike_step is None else int(spike_step)
         cfg.spike_factor = float(spike_factor)
         cfg.device, cfg.rank, cfg.world = int(device), int(rank), int(world)
+        cfg.halo_mode = int(halo_mode)
         self.handle = _lib.Handle(cfg)
         self._ops = upload_operators(self.handle, make_basis(p))
         self.lay = lay = self.handle.layout()
@@ -129,6 +131,7 @@ class SlabDriver:
         assert planes == lay.planes_local and plane0 * lay.plane_cells == lay.cell_offset
         self.cell_offset, self.n_local = lay.cell_offset, lay.n_cells_local
         self.halo = HaloExchange(lay.planes_local, lay.plane_cells, rank, world, group, staged)
+        self.halo.force = bool(halo_mode)
         slots = (lay.planes_local + 2) * lay.plane_cells
         shape = (lay.faces_per_cell, slots, lay.record_doubles)
         self.tr = []

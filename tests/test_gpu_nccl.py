@@ -1,0 +1,56 @@
+"""NCCL halo path on ONE GPU: a single-rank NCCL process group with the halo
+slots forced on (halo_mode=1), so every step sends the slab-boundary face
+records to itself with batched NCCL send/recv and all-reduces the
+{lambda, error} pair through NCCL.  The result must equal the periodic
+in-place run bitwise (this is the code path of the x-slab decomposition)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _run(port, out, inject):
+    import torch.distributed as dist
+    from paper_1801_08682_b200 import scenarios
+    from paper_1801_08682_b200.parallel import SlabDriver
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    Q0 = scenarios.build("bump", 3, 2, 3, seed=5, noise=1e-2)
+    a = SlabDriver(Q0, 3, 2, 3, 0, 1, 0, inject_rerun=inject, halo_mode=1)
+    a.run(4)
+    qa = a.local_state()
+    b = SlabDriver(Q0, 3, 2, 3, 0, 1, 0, inject_rerun=inject)
+    b.run(4)
+    qb = b.local_state()
+    np.save(out, np.stack([qa, qb]))
+    a.close()
+    b.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("inject", [False, True])
+def test_nccl_self_halo_equals_periodic(cuda_ok, tmp_path, inject):
+    ctx = mp.get_context("spawn")
+    out = str(tmp_path / "q.npy")
+    p = ctx.Process(target=_run, args=(_port(), out, inject))
+    p.start()
+    p.join(timeout=300)
+    assert p.exitcode == 0
+    qa, qb = np.load(out)
+    assert np.array_equal(qa, qb)
