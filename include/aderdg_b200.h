@@ -74,6 +74,9 @@ typedef struct {
   int rank;              /* slab index (0 for a single GPU)                */
   int world;             /* number of slabs along axis 0 (1 = periodic in place) */
   int halo_mode;         /* 0: halo slots iff world > 1; 1: always (world = 1 then exchanges with itself) */
+  int driver_mode;       /* 0: fused single-touch (scheduler.py:370-449); 1: straightforward
+                            (scheduler.py:230-313: predict pass, then Riemann/corrector pass,
+                            dt = dt_new, no priming, no rerun)                               */
 } adg_config;
 
 typedef struct {
@@ -130,6 +133,9 @@ adg_status adg_run(adg_handle* h, int steps, adg_step_record* out);
 /* records of steps first..first+count-1 (1-based; the last 4096 steps are kept) */
 adg_status adg_step_records(adg_handle* h, int first, int count, adg_step_record* out);
 adg_status adg_sync(adg_handle* h);
+/* tc.dt_new = value before the next step (straightforward run(final_time) clamp,
+ * scheduler.py:223-226) */
+adg_status adg_set_dt_new(adg_handle* h, double value);
 int        adg_step_count(const adg_handle* h);
 int        adg_rerun_count(const adg_handle* h);
 int        adg_sweep_count(const adg_handle* h);

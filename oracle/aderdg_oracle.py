@@ -507,3 +507,40 @@ class FusedDriver:
         for _ in range(steps):
             self.step()
         return self.step_count
+
+
+class StraightforwardDriver(FusedDriver):
+    """Batched restatement of ``Driver(..., mode="straightforward")`` without
+    limiter (src/scheduler.py:230-313): three phase-pure sweeps per step
+    (predict + extrapolate; Riemann; volume + face + update + calc_time_step),
+    step size ``dt = tc.dt_new`` of the previous step, no priming, no rerun."""
+
+    def step(self):
+        k, tc = self.k, self.tc
+        step = self.step_count + 1
+        dt = tc.dt_new
+        q, f, pfail, _ = k.predict(self.Q, dt)                      # sweep 1
+        if np.any(pfail):
+            ci = int(np.nonzero(pfail)[0][0])
+            raise OracleError("PredictorFailureError",
+                              f"predictor produced non-finite values (cell {ci})", ci, step)
+        tr_q, tr_f = k.extrapolate(q, f)
+        fstar = k.solve_riemann(tr_q, tr_f)                         # sweep 2
+        D = k.integrate_volume(f, dt)                               # sweep 3
+        D = k.integrate_face(D, fstar, dt)
+        self.Q += D
+        if self.spike_step is not None and step == self.spike_step:
+            self._apply_spike()
+        dtc, ok, _ = k.calc_time_step(self.Q)
+        if not np.all(ok):
+            ci = int(np.nonzero(~ok)[0][0])
+            raise OracleError("NumericalError", f"inadmissible state in cell {ci} at step {step}", ci, step)
+        self.sweep_count += 3
+        tc.T += dt
+        tc.dt_adm = float(np.min(dtc))
+        update_time_step_sizes(tc)
+        self.step_count = step
+        self.step_records.append({
+            "step": step, "T": tc.T, "dt_old": tc.dt_old, "dt_new": tc.dt_new,
+            "dt_adm": tc.dt_adm, "reruns": 0, "troubled": 0})
+        return step

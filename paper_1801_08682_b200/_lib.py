@@ -28,7 +28,7 @@ EXPORTS = (
     "adg_time_control", "adg_picard_histogram", "adg_error_info",
     "adg_last_error", "adg_layout_info", "adg_buffer", "adg_phase_seed",
     "adg_phase_seed_finish", "adg_phase_rerun", "adg_phase_sweep",
-    "adg_phase_finish", "adg_trace_parity", "adg_flush_l2", "adg_reset",
+    "adg_phase_finish", "adg_trace_parity", "adg_flush_l2", "adg_reset", "adg_set_dt_new",
 )
 
 
@@ -40,6 +40,7 @@ class AdgConfig(ctypes.Structure):
         ("inject_rerun", ctypes.c_int), ("spike_step", ctypes.c_int),
         ("spike_factor", ctypes.c_double), ("device", ctypes.c_int),
         ("rank", ctypes.c_int), ("world", ctypes.c_int), ("halo_mode", ctypes.c_int),
+        ("driver_mode", ctypes.c_int),
     ]
 
 
@@ -109,6 +110,7 @@ def load_library(path=None):
         "adg_trace_parity": (ctypes.c_int, [H]),
         "adg_flush_l2": (ctypes.c_int, [H]),
         "adg_reset": (ctypes.c_int, [H]),
+        "adg_set_dt_new": (ctypes.c_int, [H, ctypes.c_double]),
     }
     for name, (res, args) in proto.items():
         fn = getattr(lib, name)

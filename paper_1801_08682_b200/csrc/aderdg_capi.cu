@@ -209,6 +209,10 @@ static SweepParams sweep_params(adg_handle* h, int mode) {
     P.tr_out = h->tr[par ^ 1];
   }
   if (mode == MODE_PRIMING) P.tr_out = h->tr[1];
+  if (mode == MODE_SF_PREDICT || mode == MODE_SF_CORRECT) {   // straightforward: one record parity
+    P.tr_in = h->tr[0];
+    P.tr_out = h->tr[0];
+  }
   P.st = h->st;
   P.slots = h->slots;
   P.mode = mode;
@@ -240,6 +244,7 @@ static FinishParams finish_params(adg_handle* h, int priming, int seed) {
   F.forced_dt = h->cfg.forced_dt;
   F.creeping = h->cfg.creeping;
   F.inject_rerun = h->cfg.inject_rerun;
+  F.straightforward = (h->cfg.driver_mode == 1 && !seed) ? 1 : 0;
   return F;
 }
 
@@ -298,6 +303,7 @@ adg_status adg_create(const adg_config* cfg, adg_handle** out) {
   if (c.L < 1 || c.L > 4) { snprintf(buf, sizeof buf, "depth L must be in [1, 4], got %d", c.L); h->err = buf; *out = h; return ADG_ERR_CONFIG; }
   if (c.p < 0 || c.p > 9) { snprintf(buf, sizeof buf, "order p must be in [0, 9], got %d", c.p); h->err = buf; *out = h; return ADG_ERR_CONFIG; }
   if (!(c.c_dt > 0.0 && c.c_dt <= 1.0)) { snprintf(buf, sizeof buf, "c_dt must be in (0, 1], got %g", c.c_dt); h->err = buf; *out = h; return ADG_ERR_CONFIG; }
+  if (c.driver_mode != 0 && c.driver_mode != 1) { h->err = "driver_mode must be 0 (fused) or 1 (straightforward)"; *out = h; return ADG_ERR_CONFIG; }
   if (!dispatch_for(c.d, c.p, &h->disp)) {
     snprintf(buf, sizeof buf, "no sm_100a kernel instantiated for d=%d p=%d", c.d, c.p);
     h->err = buf; *out = h; return ADG_ERR_CONFIG;
@@ -454,8 +460,14 @@ adg_status adg_seed(adg_handle* h) {
   return status_from_state(h);
 }
 
+static bool straightforward(const adg_handle* h) { return h->cfg.driver_mode == 1; }
+
 adg_status adg_phase_rerun(adg_handle* h) {
   if (!h) return ADG_ERR_CONFIG;
+  if (straightforward(h)) {                     // the prediction sweep of the step
+    if (!h->seeded) return fail(h, ADG_ERR_CONFIG, "time control not seeded");
+    return launch(h, MODE_SF_PREDICT);
+  }
   if (h->sweep_index == 0) return ADG_OK;       // nothing predicted yet
   return launch(h, MODE_RERUN);
 }
@@ -463,13 +475,14 @@ adg_status adg_phase_rerun(adg_handle* h) {
 adg_status adg_phase_sweep(adg_handle* h) {
   if (!h) return ADG_ERR_CONFIG;
   if (!h->seeded) return fail(h, ADG_ERR_CONFIG, "time control not seeded");
+  if (straightforward(h)) return launch(h, MODE_SF_CORRECT);
   adg_status s = launch(h, h->sweep_index == 0 ? MODE_PRIMING : MODE_NORMAL);
   return s;
 }
 
 adg_status adg_phase_finish(adg_handle* h) {
   if (!h) return ADG_ERR_CONFIG;
-  adg_status s = launch_finish(h, h->sweep_index == 0 ? 1 : 0, 0);
+  adg_status s = launch_finish(h, (!straightforward(h) && h->sweep_index == 0) ? 1 : 0, 0);
   h->sweep_index += 1;
   return s;
 }
@@ -478,7 +491,7 @@ int adg_trace_parity(const adg_handle* h) { return h ? (h->sweep_index & 1) : 0;
 
 static adg_status enqueue_step(adg_handle* h) {
   adg_status s;
-  if (h->sweep_index == 0) {                    // Driver.step: priming sweep first
+  if (!straightforward(h) && h->sweep_index == 0) {   // Driver.step: priming sweep first
     if ((s = adg_phase_sweep(h)) != ADG_OK) return s;
     if ((s = adg_phase_finish(h)) != ADG_OK) return s;
   }
@@ -545,6 +558,21 @@ adg_status adg_step_records(adg_handle* h, int first, int count, adg_step_record
   return fetch_records(h, first - 1, first - 1 + count, out);
 }
 
+namespace {
+__global__ void set_dt_new_kernel(DevState* st, double v, double h) {
+  st->dt_new = v;
+  st->scale_new = __ddiv_rn(v, h);
+}
+}  // namespace
+
+adg_status adg_set_dt_new(adg_handle* h, double value) {
+  if (!h) return ADG_ERR_CONFIG;
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  set_dt_new_kernel<<<1, 1, 0, h->stream>>>(h->st, value, h->h);
+  CUDA_TRY(h, cudaGetLastError());
+  return pull_state(h);
+}
+
 adg_status adg_sync(adg_handle* h) {
   if (!h) return ADG_ERR_CONFIG;
   adg_status s = pull_state(h);
@@ -558,8 +586,10 @@ int adg_rerun_count(const adg_handle* h) {
   return h ? h->hst.reruns_total - h->hst.rerun_next : 0;
 }
 int adg_sweep_count(const adg_handle* h) {
-  // priming + one regular sweep per step + rerun passes (Driver.sweep_count)
+  // priming + one regular sweep per step + rerun passes (Driver.sweep_count);
+  // straightforward: three sweeps per step (scheduler.py:236,255,267)
   if (!h || h->hst.step == 0) return 0;
+  if (h->cfg.driver_mode == 1) return 3 * h->hst.step;
   return 1 + h->hst.step + h->hst.reruns_total - (h->hst.rerun_next ? 1 : 0);
 }
 

@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
   if (st->status != 0) return;
   const int mode = P.mode;
   if (mode == MODE_RERUN && !st->rerun_next) return;
-  if (mode == MODE_NORMAL && st->reduce[1] != 0) return;
+  if (mode_corrects(mode) && st->reduce[1] != 0) return;   // a predict pass already failed
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long cell = blockIdx.x;
@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
   const int plane = (int)(cell / P.plane_cells);
   const int rest = (int)(cell % P.plane_cells);
   const long long own_slot = (long long)(plane + 1) * P.plane_cells + rest;
-  const int step_idx = (mode == MODE_NORMAL) ? st->step + 1 : 0;
+  const int step_idx = mode_corrects(mode) ? st->step + 1 : 0;
   double* Qg = P.Q + cell * (NS * M);
   double* Dg = P.D + cell * (NS * M);
 
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
 #pragma unroll
     for (int c = 0; c < M; ++c) Qx[n][c] = Qg[xn[n] * M + c];
 
-  if (mode == MODE_NORMAL) {
+  if (mode_corrects(mode)) {
     // ------------- Riemann on the 2d faces (kernels.py:147-179), time-collapsed -------------
     long long nb_slot[2 * DIM];
 #pragma unroll
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
     }
     __syncthreads();
     // ------------- integrate_face + update (kernels.py:183-214) -------------
-    const double scale_old = st->scale_old;
+    const double scale_old = (mode == MODE_SF_CORRECT) ? st->scale_new : st->scale_old;
 #pragma unroll
     for (int n = 0; n < NPT; ++n) {
       if (!an[n]) continue;
@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
     }
   }
 
-  if (mode != MODE_RERUN) {
+  if (!mode_predict_only(mode)) {
     // ------------- calc_time_step (kernels.py:216-229) -------------
     bool ok = true;
     double lam = 0.0;
@@ -217,6 +217,10 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
     lam = block_max<NW>(lam, sRed);
     if (tid == 0) atomicMax(&st->reduce[0], __double_as_longlong(lam));
     if (mode == MODE_SEED) return;
+    if (mode == MODE_SF_CORRECT) {                       // straightforward: no predictor in this pass
+      if (tid == 0) bulk_commit_wait_if_any();
+      return;
+    }
   } else {
     bool ok = true;
 #pragma unroll
@@ -232,7 +236,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
 
   // ---------------- predictor (kernels.py:68-105) ----------------
   const double dt = (mode == MODE_RERUN) ? st->dt_old : st->dt_new;
-  const double scale = (mode == MODE_RERUN) ? st->scale_old : st->scale_new;   // dt / h
+  const double scale = (mode == MODE_RERUN) ? st->scale_old : st->scale_new;   // dt / h (SF: dt_new)
   double am = 0.0;
 #pragma unroll
   for (int n = 0; n < NPT; ++n)

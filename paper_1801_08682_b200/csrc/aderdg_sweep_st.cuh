@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(256, 3) sweep_kernel_st(const SweepParams P) {
   if (st->status != 0) return;
   const int mode = P.mode;
   if (mode == MODE_RERUN && !st->rerun_next) return;
-  if (mode == MODE_NORMAL && st->reduce[1] != 0) return;
+  if (mode_corrects(mode) && st->reduce[1] != 0) return;   // a predict pass already failed
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int t = lane & 3;
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(256, 3) sweep_kernel_st(const SweepParams P) {
   const int plane = (int)(cell / P.plane_cells);
   const int rest = (int)(cell % P.plane_cells);
   const long long own_slot = (long long)(plane + 1) * P.plane_cells + rest;
-  const int step_idx = (mode == MODE_NORMAL) ? st->step + 1 : 0;
+  const int step_idx = mode_corrects(mode) ? st->step + 1 : 0;
   double* Qg = P.Q + cell * (NS * M);
   double* Dg = P.D + cell * (NS * M);
 
@@ -99,10 +99,10 @@ __global__ void __launch_bounds__(256, 3) sweep_kernel_st(const SweepParams P) {
   __syncthreads();
   if (tid == 0) {
     uint32_t bytes = NS * M * 8;
-    if (mode == MODE_NORMAL) bytes += NS * M * 8 + 4 * DIM * REC * 8;
+    if (mode_corrects(mode)) bytes += NS * M * 8 + 4 * DIM * REC * 8;
     mbar_arrive_expect_tx(bar, bytes);
     bulk_g2s(sQ, Qg, NS * M * 8, bar);
-    if (mode == MODE_NORMAL) {
+    if (mode_corrects(mode)) {
       bulk_g2s(sD, Dg, NS * M * 8, bar);
       for (int f = 0; f < 2 * DIM; ++f) {
         const int a = f >> 1, dir = (f & 1) ? 1 : -1;
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(256, 3) sweep_kernel_st(const SweepParams P) {
 #pragma unroll
   for (int c = 0; c < M; ++c) Qx[c] = sQ[x * M + c];
 
-  if (mode == MODE_NORMAL) {
+  if (mode_corrects(mode)) {
     // ------------- Riemann (kernels.py:147-179), time-collapsed -------------
     for (int e = tid; e < 2 * DIM * NF * M; e += THREADS) {
       const int f = e / (NF * M), yc = e % (NF * M);
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(256, 3) sweep_kernel_st(const SweepParams P) {
       double Dx[M];
 #pragma unroll
       for (int c = 0; c < M; ++c) Dx[c] = sD[x * M + c];
-      const double scale_old = st->scale_old;
+      const double scale_old = (mode == MODE_SF_CORRECT) ? st->scale_new : st->scale_old;
       const int idx[3] = {i0, i1, i2};
 #pragma unroll
       for (int a = 0; a < DIM; ++a) {
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(256, 3) sweep_kernel_st(const SweepParams P) {
     }
   }
 
-  if (mode != MODE_RERUN) {
+  if (!mode_predict_only(mode)) {
     // ------------- calc_time_step (kernels.py:216-229) -------------
     bool ok = true;
     double lam = 0.0;
@@ -200,13 +200,17 @@ __global__ void __launch_bounds__(256, 3) sweep_kernel_st(const SweepParams P) {
     if (!__syncthreads_and(ok)) {
       if (tid == 0) {
         report_error(st, 2 * gcell + 0);
-        if (mode == MODE_NORMAL) bulk_commit_wait();
+        if (mode_corrects(mode)) bulk_commit_wait();
       }
       return;
     }
     lam = block_max<NW>(lam, sRed);
     if (tid == 0) atomicMax(&st->reduce[0], __double_as_longlong(lam));
     if (mode == MODE_SEED) return;
+    if (mode == MODE_SF_CORRECT) {                       // straightforward: no predictor in this pass
+      if (tid == 0) bulk_commit_wait_if_any();
+      return;
+    }
   } else {
     bool ok = true;
 #pragma unroll
@@ -219,7 +223,7 @@ __global__ void __launch_bounds__(256, 3) sweep_kernel_st(const SweepParams P) {
 
   // ---------------- predictor (kernels.py:68-105) ----------------
   const double dt = (mode == MODE_RERUN) ? st->dt_old : st->dt_new;
-  const double scale = (mode == MODE_RERUN) ? st->scale_old : st->scale_new;   // dt / h
+  const double scale = (mode == MODE_RERUN) ? st->scale_old : st->scale_new;   // dt / h (SF: dt_new)
   double absmax;
   {
     double am = 0.0;
@@ -319,7 +323,7 @@ __global__ void __launch_bounds__(256, 3) sweep_kernel_st(const SweepParams P) {
   if (failed) {
     if (tid == 0) {
       report_error(st, 2 * gcell + 1);
-      if (mode == MODE_NORMAL) bulk_commit_wait();
+      if (mode_corrects(mode)) bulk_commit_wait();
     }
     return;
   }

@@ -103,7 +103,8 @@ class SlabDriver:
 
     def __init__(self, Q_global, d, L, p, rank, world, device, cfl=0.9, c_dt=0.99,
                  averaging="strict", forced_dt=None, inject_rerun=False,
-                 spike_step=None, spike_factor=3.0, group=None, staged=False, halo_mode=0):
+                 spike_step=None, spike_factor=3.0, group=None, staged=False, halo_mode=0,
+                 mode="fused"):
         import torch
         from .basis import make_basis
         from .solver import upload_operators
@@ -121,6 +122,8 @@ class SlabDriver:
         cfg.spike_factor = float(spike_factor)
         cfg.device, cfg.rank, cfg.world = int(device), int(rank), int(world)
         cfg.halo_mode = int(halo_mode)
+        cfg.driver_mode = 1 if mode == "straightforward" else 0
+        self.mode = mode
         self.handle = _lib.Handle(cfg)
         self._ops = upload_operators(self.handle, make_basis(p))
         self.lay = lay = self.handle.layout()
@@ -161,7 +164,7 @@ class SlabDriver:
     def enqueue_step(self):
         """Queue one realisation step without host synchronisation."""
         h = self.handle
-        if not self.primed:
+        if not self.primed and self.mode != "straightforward":
             h.call("adg_phase_sweep")          # priming sweep (no traces read)
             self.halo.reduce(self.red)
             h.call("adg_phase_finish")

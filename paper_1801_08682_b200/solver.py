@@ -25,6 +25,7 @@ Reference citations (``src/`` = ``/root/reference/pkg/src/aderdg/``):
   Driver (fused)             src/scheduler.py:88-226, 370-481
 """
 
+import ctypes
 import math
 from collections import Counter
 
@@ -201,7 +202,8 @@ class TimeControl:
         self.T, self.dt_old, self.dt_new, self.dt_adm = 0.0, 0.0, 0.0, math.inf
 
 
-def _config(grid, kernels, tc, inject_rerun, spike_step, spike_factor, device, rank=0, world=1):
+def _config(grid, kernels, tc, inject_rerun, spike_step, spike_factor, device, rank=0, world=1,
+            mode="fused"):
     cfg = _lib.AdgConfig()
     cfg.d, cfg.p, cfg.L = grid.d, grid.p, grid.L
     cfg.cfl = float(kernels.cfl)
@@ -213,6 +215,7 @@ def _config(grid, kernels, tc, inject_rerun, spike_step, spike_factor, device, r
     cfg.spike_factor = float(spike_factor)
     cfg.device = int(device)
     cfg.rank, cfg.world = int(rank), int(world)
+    cfg.driver_mode = 1 if mode == "straightforward" else 0
     return cfg
 
 
@@ -224,7 +227,9 @@ def upload_operators(handle, basis):
 
 
 class Driver:
-    """Fused single-touch driver on the GPU (src/scheduler.py:88-226).
+    """GPU driver (src/scheduler.py:88-313): the fused single-touch mode (the
+    north-star path) or the straightforward three-sweep mode (predict pass,
+    Riemann + corrector pass; dt = dt_new, no priming, no rerun).
 
     ``host_sync``: "step" copies the state back into ``grid.Q`` after every
     step (reference semantics: ``cell.Q`` is current after ``step()``);
@@ -237,11 +242,14 @@ class Driver:
                  limiter=None, device=0, host_sync="step"):
         if mode not in ("straightforward", "shifted", "fused"):
             raise ConfigurationError(f"unknown scheduler mode {mode!r}")
-        if mode != "fused":
-            raise ConfigurationError(
-                f"the GPU driver implements the fused single-touch mode; {mode!r} is out of scope")
+        if mode == "shifted":
+            raise ConfigurationError("the shifted driver is not implemented on the GPU (out of scope)")
+        if parallel and mode == "shifted":
+            raise ConfigurationError("the shifted driver is sequential only")
         if limiter is not None:
-            raise ConfigurationError("subcell limiting is supported in straightforward mode only")
+            if mode != "straightforward":
+                raise ConfigurationError("subcell limiting is supported in straightforward mode only")
+            raise ConfigurationError("the GPU path has no subcell limiter (out of scope)")
         if isinstance(traversal, np.ndarray):
             if sorted(traversal.tolist()) != list(range(grid.n_cells)):
                 raise ConfigurationError("traversal must be a permutation of the cells")
@@ -262,7 +270,8 @@ class Driver:
         self.step_records = []
         self.picard_iters = 0
         self.predicts = 0
-        cfg = _config(grid, kernels, time_control, inject_rerun, spike_step, spike_factor, device)
+        cfg = _config(grid, kernels, time_control, inject_rerun, spike_step, spike_factor, device,
+                      mode=mode)
         self.handle = _lib.Handle(cfg)
         self._ops = upload_operators(self.handle, kernels.basis)
         self.load_state(grid.Q)
@@ -326,9 +335,11 @@ class Driver:
         if (steps is None) == (final_time is None):
             raise ConfigurationError("specify exactly one of steps / final_time")
         if final_time is not None:
-            raise ConfigurationError(
-                "final-time integration requires the straightforward driver "
-                "(the pipelined modes realise steps one sweep late)")
+            if self.mode != "straightforward":
+                raise ConfigurationError(
+                    "final-time integration requires the straightforward driver "
+                    "(the pipelined modes realise steps one sweep late)")
+            return self._run_to(float(final_time))
         steps = int(steps)
         if steps <= 0:
             return self.step_count
@@ -344,6 +355,17 @@ class Driver:
         if self.host_sync in ("step", "run"):
             self.sync_state()
         self._finish(list(recs)[:done], err)
+        return self.step_count
+
+    def _run_to(self, final_time):
+        """src/scheduler.py:223-226: clamp dt_new so the last step lands on final_time."""
+        while True:
+            T, dt_old, dt_new, dt_adm = self.handle.time_control()
+            if not T < final_time - 1e-14:
+                break
+            if dt_new > final_time - T:
+                self.handle.call("adg_set_dt_new", ctypes.c_double(final_time - T))
+            self.step()
         return self.step_count
 
     def picard_histogram(self):

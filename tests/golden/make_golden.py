@@ -7,8 +7,9 @@ Runs only in the build container, where ``/root/reference`` exists:
 
 For every case it builds the reference grid (``build_grid`` with an explicit
 budget, ``src/mesh.py:167-243``), fills ``cell.Q`` from the seeded scenario in
-``paper_1801_08682_b200/scenarios.py``, runs ``Driver(..., "fused")``
-(``src/scheduler.py:92-226``) and stores under ``tests/golden/<case>.npz``:
+``paper_1801_08682_b200/scenarios.py``, runs ``Driver(..., "fused")`` (or the
+straightforward three-sweep driver for the ``sf_*`` cases, ``storage="spacetime"``)
+(``src/scheduler.py:92-313``) and stores under ``tests/golden/<case>.npz``:
 
 * ``records``: per step (step, T, dt_old, dt_new, dt_adm, reruns);
 * ``Q_final`` (small cases) or ``Q_sample`` + ``sample_cells`` (large cases:
@@ -56,6 +57,12 @@ SMALL = {
     "wave_d2_L2_p3_forced": ("wave", 2, 2, 3, 10, {}, {"forced_dt": 2e-4}, True),
     "wave_d3_L1_p2_creeping": ("wave", 3, 1, 2, 5, {}, {"averaging": "creeping"}, True),
     "uniform_d2_L1_p2": ("uniform", 2, 1, 2, 5, {}, {}, True),
+    # straightforward (three-sweep) driver, src/scheduler.py:230-313
+    "sf_bump_d2_L2_p3": ("bump", 2, 2, 3, 8, {"mode": "straightforward"}, {}, True),
+    "sf_bump_d3_L1_p3": ("bump", 3, 1, 3, 5, {"mode": "straightforward"}, {}, True),
+    "sf_wave_d2_L2_p3_forced": ("wave", 2, 2, 3, 10, {"mode": "straightforward"}, {"forced_dt": 2e-4}, True),
+    "sf_bump_d3_L1_p5_creeping": ("bump", 3, 1, 5, 4, {"mode": "straightforward"}, {"averaging": "creeping"}, True),
+    "sf_wave_d2_L1_p2_spike": ("wave", 2, 1, 2, 8, {"mode": "straightforward", "spike_step": 4}, {}, True),
 }
 BIG = {
     "bump_d3_L3_p3_cfg2": ("bump", 3, 3, 3, 20, {}, {}, False),
@@ -74,7 +81,10 @@ def run_case(name, spec):
     Q0 = scenarios.build(scen, d, L, p)
     system = EulerSystem(d)
     basis = make_basis(p)
-    grid = build_grid(d, L, p, system.m, budget_bytes=1 << 40)
+    dkw = dict(dkw)
+    mode = dkw.pop("mode", "fused")
+    storage = "spacetime" if mode == "straightforward" else "hull"
+    grid = build_grid(d, L, p, system.m, storage=storage, budget_bytes=1 << 40)
     for c in grid.cells:
         c.Q[...] = Q0[c.index]
     kernels = Kernels(system, basis, grid, None, cfl=0.9)
@@ -101,7 +111,7 @@ def run_case(name, spec):
     error = None
     t0 = time.time()
     try:
-        driver = Driver(grid, kernels, tc, "fused", **dkw)
+        driver = Driver(grid, kernels, tc, mode, **dkw)
         for _ in range(steps):
             driver.step()
     except (NumericalError, PredictorFailureError) as e:
@@ -121,7 +131,7 @@ def run_case(name, spec):
         "picard_keys": np.array(sorted(hist), dtype=np.int64),
         "picard_vals": np.array([hist[k] for k in sorted(hist)], dtype=np.int64),
         "meta": np.array(json.dumps({"scenario": scen, "d": d, "L": L, "p": p, "steps": steps,
-                                     "driver_kwargs": dkw, "tc_kwargs": tkw, "error": error,
+                                     "driver_kwargs": dkw, "mode": mode, "tc_kwargs": tkw, "error": error,
                                      "wall_s": wall, "sweep_count": driver.sweep_count if driver else None,
                                      "rerun_count": driver.rerun_count if driver else None,
                                      "reruns_by_step": {str(k): v for k, v in

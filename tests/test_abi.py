@@ -47,7 +47,19 @@ def test_missing_library_fails_loudly(tmp_path):
         _lib.load_library(str(tmp_path / "nope.so"))
 
 
-def test_struct_layouts_match_header():
-    # adg_step_record: 2 ints + 4 doubles + 2 long long = 56 bytes
-    assert ctypes.sizeof(_lib.AdgStepRecord) == 56
-    assert ctypes.sizeof(_lib.AdgConfig) == 80
+def test_struct_layouts_match_header(tmp_path):
+    """ctypes mirrors of the C structs agree with the C compiler's layout."""
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "aderdg_b200.h"\n'
+                   'int main(void){printf("%zu %zu %zu %zu %zu\\n", sizeof(adg_config), sizeof(adg_step_record),'
+                   ' sizeof(adg_layout), offsetof(adg_config, driver_mode), offsetof(adg_step_record, predicts));'
+                   'return 0;}\n')
+    exe = tmp_path / "sz"
+    r = subprocess.run(["gcc", "-I", os.path.join(REPO, "include"), str(src), "-o", str(exe)],
+                       capture_output=True, text=True)
+    if r.returncode != 0:
+        pytest.skip("gcc unavailable: " + r.stderr[:200])
+    vals = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
+    assert vals == [ctypes.sizeof(_lib.AdgConfig), ctypes.sizeof(_lib.AdgStepRecord),
+                    ctypes.sizeof(_lib.AdgLayout), _lib.AdgConfig.driver_mode.offset,
+                    _lib.AdgStepRecord.predicts.offset]

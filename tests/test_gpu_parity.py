@@ -171,3 +171,58 @@ def test_gpu_matches_reference_at_baseline_size(cuda_ok, name):
     if "Q_sample" in g:
         e = rel_linf(drv.grid.Q[g["sample_cells"]], g["Q_sample"])
         assert e <= TOL, f"{name}: rel L-inf {e:.3e}"
+
+
+SF = [n for n in golden_names() if n.startswith("sf_")]
+
+
+@pytest.mark.parametrize("name", SF)
+def test_gpu_straightforward_matches_reference(cuda_ok, name):
+    """Straightforward (three-sweep) driver, src/scheduler.py:230-313: GPU predict pass +
+    Riemann/corrector pass against the reference's own straightforward runs."""
+    g = load_golden(name)
+    meta = g["meta"]
+    d, L, p = meta["d"], meta["L"], meta["p"]
+    Q0 = scenarios.build(meta["scenario"], d, L, p)
+    grid = build_grid(d, L, p, d + 2)
+    grid.Q[...] = Q0
+    kern = Kernels(EulerSystem(d), make_basis(p), grid, None, cfl=0.9)
+    drv = Driver(grid, kern, TimeControl(c_dt=0.99, **meta["tc_kwargs"]), "straightforward",
+                 host_sync="run", **meta["driver_kwargs"])
+    drv.run(steps=meta["steps"])
+    recs = records_array(drv)
+    ref = g["records"]
+    assert recs.shape == ref.shape
+    assert np.max(np.abs(recs[:, 1:5] - ref[:, 1:5]) / np.abs(ref[:, 1:5]).clip(1e-300)) < TOL
+    assert drv.sweep_count == meta["sweep_count"]
+    assert drv.rerun_count == 0
+    assert rel_linf(drv.grid.Q, g["Q_final"]) <= TOL
+
+
+def test_gpu_mode_equivalence_forced_dt(cuda_ok):
+    """tests/test_acceptance.py:104-119 of the reference: under a forced step
+    size the fused and straightforward drivers agree to <= 1e-12."""
+    d, L, p = 2, 2, 3
+    Q0 = scenarios.smooth_density_wave(d, L, p)
+    out = {}
+    for mode in ("straightforward", "fused"):
+        grid = build_grid(d, L, p, d + 2)
+        grid.Q[...] = Q0
+        kern = Kernels(EulerSystem(d), make_basis(p), grid, None)
+        drv = Driver(grid, kern, TimeControl(forced_dt=2e-4), mode, host_sync="run")
+        drv.run(steps=10)
+        out[mode] = (np.array(grid.Q), drv.sweep_count)
+    assert np.max(np.abs(out["fused"][0] - out["straightforward"][0])) <= 1e-12
+    assert out["straightforward"][1] == 30 and out["fused"][1] == 11
+
+
+def test_gpu_straightforward_final_time(cuda_ok):
+    """run(final_time=...) clamps the last step (src/scheduler.py:219-226)."""
+    d, L, p = 2, 1, 2
+    Q0 = scenarios.smooth_density_wave(d, L, p)
+    grid = build_grid(d, L, p, d + 2)
+    grid.Q[...] = Q0
+    kern = Kernels(EulerSystem(d), make_basis(p), grid, None)
+    drv = Driver(grid, kern, TimeControl(), "straightforward", host_sync="run")
+    drv.run(final_time=0.05)
+    assert abs(drv.tc.T - 0.05) < 1e-14

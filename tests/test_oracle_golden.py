@@ -12,14 +12,15 @@ FAST = [n for n in golden_names() if n in (
     "bump_d2_L2_p3", "bump_d2_L1_p0", "bump_d2_L2_p1", "bump_d2_L1_p9", "bump_d2_L2_p6",
     "bump_d3_L1_p3", "bump_d3_L1_p2", "bump_d3_L1_p5", "fourier_d3_L1_p4",
     "wave_d2_L1_p2_spike", "wave_d2_L1_p3_inject", "wave_d2_L2_p3_forced",
-    "wave_d3_L1_p2_creeping", "uniform_d2_L1_p2", "bump_d2_L3_p3_cfg1")]
+    "wave_d3_L1_p2_creeping", "uniform_d2_L1_p2", "bump_d2_L3_p3_cfg1") or n.startswith("sf_")]
 
 
 def run_oracle(meta):
     Q0 = scenarios.build(meta["scenario"], meta["d"], meta["L"], meta["p"])
     dkw = dict(meta["driver_kwargs"])
     tkw = dict(meta["tc_kwargs"])
-    drv = O.FusedDriver(Q0.copy(), meta["d"], meta["p"], meta["L"], **dkw, **tkw)
+    cls = O.StraightforwardDriver if meta.get("mode", "fused") == "straightforward" else O.FusedDriver
+    drv = cls(Q0.copy(), meta["d"], meta["p"], meta["L"], **dkw, **tkw)
     err = None
     try:
         for _ in range(meta["steps"]):
