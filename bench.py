@@ -203,6 +203,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="fused", choices=["fused", "straightforward"],
+                    help="driver: fused single-touch (north star) or the straightforward passes")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -247,7 +249,7 @@ def main():
     # segments.  Default K + W = E: one episode, the first W steps (incl. the
     # priming sweep) untimed.
     E = cfgd["steps"]
-    drv = SlabDriver(Q0, d, L, p, rank, world, local)
+    drv = SlabDriver(Q0, d, L, p, rank, world, local, mode=args.mode)
     h = drv.handle
     K = args.steps
     clocks = ClockSampler(local)
@@ -364,6 +366,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfgd["desc"], "d": d, "p": p, "L": L, "cells": cells,
+                       "driver": args.mode,
                        "nodes": cells * (p + 1) ** d, "dof": dofs,
                        "parallelism": f"x-slab x{world}" if world > 1 else "single GPU",
                        "l2": "no flush: per-step working set (Q,D r/w + 2 trace parities) "
@@ -372,7 +375,7 @@ def main():
                        "reruns_in_timed": reruns, "picard_mean": iters / max(preds, 1)},
             "roofline": {"bound": "fp64", "achieved": achieved_tf, "peak": peak_tf,
                          "unit": "TFLOP/s", "frac": achieved_tf / peak_tf, "traffic": traffic,
-                         "kernel": f"sweep_kernel<{d},{p + 1}> (fused sweep + rerun passes)",
+                         "kernel": f"sweep kernel d={d} n={p + 1} ({args.mode}: all sweep passes of the step)",
                          "kernel_ms_per_step": kern_ms_per_step,
                          "kernel_share_of_step": kern_ms_per_step / ms_per_step,
                          "flops_per_step_per_gpu": flops / K if K else 0,

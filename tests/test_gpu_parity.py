@@ -31,7 +31,7 @@ def records_array(drv):
                      for r in drv.step_records]).reshape(-1, 6)
 
 
-SMALL = [n for n in golden_names() if not any(t in n for t in ("cfg2", "cfg3", "L2_p5"))]
+SMALL = [n for n in golden_names() if not any(t in n for t in ("cfg2", "cfg3", "L2_p5")) and not n.startswith("sf_")]
 
 
 @pytest.mark.parametrize("name", SMALL)
