@@ -69,6 +69,12 @@ void launch_sweep_ho(const SweepParams& P, unsigned grid, cudaStream_t s) {
   sweep_kernel_ho<NQ><<<grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
 }
 
+int kernel_variant() {
+  // ADG_KERNEL=1: first-generation kernel; 2: time-split v2; 3 (default): v2 without time split
+  const char* v = getenv("ADG_KERNEL");
+  return v ? atoi(v) : 3;
+}
+
 void launch_sweep_st(const SweepParams& P, unsigned grid, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
@@ -95,11 +101,6 @@ Dispatch make_dispatch_v2() {
   return Dispatch{&launch_sweep_v2<NQ, TS, DMMA, ROLLED, MB>, ShapeV2<NQ, TS, DMMA, ROLLED, MB>::REC};
 }
 
-int kernel_variant() {
-  // ADG_KERNEL=1: first-generation kernel; 2: time-split v2; 3 (default): v2 without time split
-  const char* v = getenv("ADG_KERNEL");
-  return v ? atoi(v) : 3;
-}
 
 bool dispatch_for(int d, int p, Dispatch* out) {
   const int n = p + 1;

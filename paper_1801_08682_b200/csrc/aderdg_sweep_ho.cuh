@@ -27,7 +27,7 @@
 
 namespace adg {
 
-template <int NQ>
+template <int NQ, bool FA = true>
 struct ShapeHO {
   static constexpr int DIM = 3, M = 5;
   static constexpr int NS = NQ * NQ * NQ;
@@ -56,21 +56,26 @@ struct ShapeHO {
   // it fits next to the GEMM buffers (n <= 8), aliasing the corrector (sFace) and
   // tail (sN) buffers, otherwise in thread-private local memory
   static constexpr int R_DH = NQ * M * THREADS * NPT;
-  static constexpr bool DH_SMEM = (NQ <= 8);
+  // FA (fused axes): the flux of all three axes is staged at once and every
+  // GEMM of the slice runs between one barrier pair, writing D_a F_a in place
+  // (a tile's outputs only depend on its own columns): 2 barriers per slice.
+  // Otherwise one axis at a time (6 barriers) with the history in smem (n <= 8).
+  static constexpr bool DH_SMEM = !FA && (NQ <= 8);
   static constexpr int R_ALIAS = DH_SMEM ? R_DH : (R_NODE + R_FACE);
   static constexpr int OFF_RED = 0;
   static constexpr int OFF_FA = (R_RED + 1) & ~1;
   static constexpr int OFF_DV = OFF_FA + R_FA;
-  static constexpr int OFF_NODE = OFF_DV + R_DV;
+  static constexpr int OFF_NODE = FA ? OFF_FA : OFF_DV + R_DV;   // FA: tail buffers alias the slabs
   static constexpr int OFF_FACE = OFF_NODE + R_NODE;
   static constexpr int OFF_DH = OFF_NODE;
-  static constexpr int TOTAL = OFF_NODE + (R_ALIAS > R_NODE + R_FACE ? R_ALIAS : R_NODE + R_FACE);
+  static constexpr int TOTAL = FA ? OFF_FA + (3 * R_FA > R_NODE + R_FACE ? 3 * R_FA : R_NODE + R_FACE)
+                                  : OFF_NODE + (R_ALIAS > R_NODE + R_FACE ? R_ALIAS : R_NODE + R_FACE);
   static constexpr size_t SMEM_BYTES = sizeof(double) * TOTAL;
 };
 
-template <int NQ>
+template <int NQ, bool FA = true>
 __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
-  using S = ShapeHO<NQ>;
+  using S = ShapeHO<NQ, FA>;
   constexpr int DIM = 3, M = 5, NS = S::NS, NF = S::NF, NPT = S::NPT, REC = S::REC;
   constexpr int THREADS = S::THREADS, NW = S::NW, KC = S::KC, MT = S::MT, NT = S::NT;
   constexpr int RR = S::RR, SC = S::SC, P0 = S::P0, P1 = S::P1;
@@ -280,42 +285,39 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
         for (int c = 0; c < M; ++c) qq[c] = (it == 0) ? Qx[n][c] : qo[n][k][c];
         flux<DIM>(qq, F[n]);
       }
-#pragma unroll 1
-      for (int a = 0; a < DIM; ++a) {
-        // stage F_a in the padded natural layout
+if constexpr (FA) {
+        // stage the flux of all three axes (padded natural layout, one slab per axis)
 #pragma unroll
         for (int n = 0; n < NPT; ++n) {
           if (!an[n]) continue;
 #pragma unroll
-          for (int c = 0; c < M; ++c) {
-            const double v = (a == 0) ? F[n][0][c] : (a == 1) ? F[n][1][c] : F[n][2][c];
-            sFA[c * SC + pn[n]] = v;
-          }
+          for (int a = 0; a < DIM; ++a)
+#pragma unroll
+            for (int c = 0; c < M; ++c) sFA[a * S::R_FA + c * SC + pn[n]] = F[n][a][c];
         }
         __syncthreads();
-        // strides of the contraction axis and of the two other axes (ib < ic in axis order)
-        const int sa = (a == 0) ? P0 : (a == 1) ? P1 : 1;
-        const int sb = (a == 0) ? P1 : P0;
-        const int sc2 = (a == 2) ? P1 : 1;
-        // GEMM tiles: warp w takes n-tiles w, w+NW, ...
-        for (int nt = warp; nt < NT; nt += NW) {
+        // every GEMM tile of the slice: item = (axis, n-tile); outputs overwrite their inputs
+        for (int item = warp; item < DIM * NT; item += NW) {
+          const int a = item / NT, nt = item % NT;
+          const int sa = (a == 0) ? P0 : (a == 1) ? P1 : 1;
+          const int sb = (a == 0) ? P1 : P0;
+          const int sc2 = (a == 2) ? P1 : 1;
+          double* slab = sFA + a * S::R_FA;
           double cacc[MT][2];
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt) { cacc[mt][0] = 0.0; cacc[mt][1] = 0.0; }
-          // B[j][r]: r = c*NF + (ib*NQ + ic); columns past RR and rows past NQ read a
-          // finite in-range value (their A entries / outputs are zero / discarded)
           const int rb = min(nt * 8 + (lane >> 2), RR - 1);
           const int cb = rb / NF, yb = rb % NF;
-          const double* bbase = sFA + cb * SC + (yb / NQ) * sb + (yb % NQ) * sc2;
+          const double* bbase = slab + cb * SC + (yb / NQ) * sb + (yb % NQ) * sc2;
+          double bv[KC];
 #pragma unroll
-          for (int kc = 0; kc < KC; ++kc) {
-            const int jj = min(kc * 4 + (lane & 3), NQ - 1);
-            const double b = bbase[jj * sa];
+          for (int kc = 0; kc < KC; ++kc) bv[kc] = bbase[min(kc * 4 + (lane & 3), NQ - 1) * sa];
+          __syncwarp();
+#pragma unroll
+          for (int kc = 0; kc < KC; ++kc)
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt)
-              dmma_8x8x4(cacc[mt][0], cacc[mt][1], afr[mt][kc], b, cacc[mt][0], cacc[mt][1]);
-          }
-          // C[i'][r]: lane holds rows mt*8 + g, columns nt*8 + 2*t4 + {0,1}
+              dmma_8x8x4(cacc[mt][0], cacc[mt][1], afr[mt][kc], bv[kc], cacc[mt][0], cacc[mt][1]);
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -324,18 +326,76 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
               const int r = nt * 8 + 2 * (lane & 3) + e2;
               if (ip < NQ && r < RR) {
                 const int c = r / NF, y = r % NF;
-                const int ad = c * SC + ip * sa + (y / NQ) * sb + (y % NQ) * sc2;
-                if (a == 0) sDv[ad] = cacc[mt][e2];
-                else sDv[ad] += cacc[mt][e2];
+                slab[c * SC + ip * sa + (y / NQ) * sb + (y % NQ) * sc2] = cacc[mt][e2];
               }
             }
         }
         __syncthreads();
-      }
 #pragma unroll
+        for (int n = 0; n < NPT; ++n)
+#pragma unroll
+          for (int c = 0; c < M; ++c)
+            dhp(n, k, c) = (sFA[c * SC + pn[n]] + sFA[S::R_FA + c * SC + pn[n]]) +
+                           sFA[2 * S::R_FA + c * SC + pn[n]];
+      } else {
+#pragma unroll 1
+        for (int a = 0; a < DIM; ++a) {
+          // stage F_a in the padded natural layout
+  #pragma unroll
+          for (int n = 0; n < NPT; ++n) {
+            if (!an[n]) continue;
+  #pragma unroll
+            for (int c = 0; c < M; ++c) {
+              const double v = (a == 0) ? F[n][0][c] : (a == 1) ? F[n][1][c] : F[n][2][c];
+              sFA[c * SC + pn[n]] = v;
+            }
+          }
+          __syncthreads();
+          // strides of the contraction axis and of the two other axes (ib < ic in axis order)
+          const int sa = (a == 0) ? P0 : (a == 1) ? P1 : 1;
+          const int sb = (a == 0) ? P1 : P0;
+          const int sc2 = (a == 2) ? P1 : 1;
+          // GEMM tiles: warp w takes n-tiles w, w+NW, ...
+          for (int nt = warp; nt < NT; nt += NW) {
+            double cacc[MT][2];
+  #pragma unroll
+            for (int mt = 0; mt < MT; ++mt) { cacc[mt][0] = 0.0; cacc[mt][1] = 0.0; }
+            // B[j][r]: r = c*NF + (ib*NQ + ic); columns past RR and rows past NQ read a
+            // finite in-range value (their A entries / outputs are zero / discarded)
+            const int rb = min(nt * 8 + (lane >> 2), RR - 1);
+            const int cb = rb / NF, yb = rb % NF;
+            const double* bbase = sFA + cb * SC + (yb / NQ) * sb + (yb % NQ) * sc2;
+  #pragma unroll
+            for (int kc = 0; kc < KC; ++kc) {
+              const int jj = min(kc * 4 + (lane & 3), NQ - 1);
+              const double b = bbase[jj * sa];
+  #pragma unroll
+              for (int mt = 0; mt < MT; ++mt)
+                dmma_8x8x4(cacc[mt][0], cacc[mt][1], afr[mt][kc], b, cacc[mt][0], cacc[mt][1]);
+            }
+            // C[i'][r]: lane holds rows mt*8 + g, columns nt*8 + 2*t4 + {0,1}
+  #pragma unroll
+            for (int mt = 0; mt < MT; ++mt)
+  #pragma unroll
+              for (int e2 = 0; e2 < 2; ++e2) {
+                const int ip = mt * 8 + (lane >> 2);
+                const int r = nt * 8 + 2 * (lane & 3) + e2;
+                if (ip < NQ && r < RR) {
+                  const int c = r / NF, y = r % NF;
+                  const int ad = c * SC + ip * sa + (y / NQ) * sb + (y % NQ) * sc2;
+                  if (a == 0) sDv[ad] = cacc[mt][e2];
+                  else sDv[ad] += cacc[mt][e2];
+                }
+              }
+          }
+          __syncthreads();
+        }
+  #pragma unroll
       for (int n = 0; n < NPT; ++n)
 #pragma unroll
         for (int c = 0; c < M; ++c) dhp(n, k, c) = sDv[c * SC + pn[n]];
+      }
+
     }
     // time contraction + Picard update per node
     double dmax = 0.0, dsum = 0.0;
