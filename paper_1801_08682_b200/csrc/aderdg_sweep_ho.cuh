@@ -62,8 +62,10 @@ struct ShapeHO {
   // Otherwise one axis at a time (6 barriers) with the history in smem (n <= 8).
   static constexpr bool DH_SMEM = !FA && (NQ <= 8);
   static constexpr int R_ALIAS = DH_SMEM ? R_DH : (R_NODE + R_FACE);
+  static constexpr int R_OFF = (3 * RP + 1) / 2;            // int column-offset table (3 axes)
   static constexpr int OFF_RED = 0;
-  static constexpr int OFF_FA = (R_RED + 1) & ~1;
+  static constexpr int OFF_TAB = (R_RED + 1) & ~1;
+  static constexpr int OFF_FA = OFF_TAB + ((R_OFF + 1) & ~1);
   static constexpr int OFF_DV = OFF_FA + R_FA;
   static constexpr int OFF_NODE = FA ? OFF_FA : OFF_DV + R_DV;   // FA: tail buffers alias the slabs
   static constexpr int OFF_FACE = OFF_NODE + R_NODE;
@@ -88,6 +90,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
   double* sN = smem + S::OFF_NODE;    // [M][NS] node staging
   double* sFace = smem + S::OFF_FACE;
   double* sDH = smem + S::OFF_DH;     // [k][c][THREADS*NPT] (DH_SMEM)
+  int* sTab = reinterpret_cast<int*>(smem + S::OFF_TAB);   // [axis][RP]: c*SC + ib*sb + ic*sc2
 
   DevState* st = P.st;
   if (st->status != 0) return;
@@ -263,6 +266,15 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
         afr[mt][kc] = (ii < NQ && jj < NQ) ? P.ops.diff[ii][jj] : 0.0;
       }
   }
+  // GEMM column offsets: column r = c*NF + (ib*NQ + ic) of axis a -> padded address
+  // of (c, i_a = 0, ib, ic); padded columns clamp to the last real column
+  for (int e = tid; e < 3 * S::RP; e += THREADS) {
+    const int a = e / S::RP, r = min(e % S::RP, RR - 1);
+    const int sb = (a == 0) ? P1 : P0;
+    const int sc2 = (a == 2) ? P1 : 1;
+    const int c = r / NF, y = r % NF;
+    sTab[e] = c * SC + (y / NQ) * sb + (y % NQ) * sc2;
+  }
   // per-node time line in thread-private (local) memory
   double qo[NPT][NQ][M];
   double dh[S::DH_SMEM ? 1 : NPT][S::DH_SMEM ? 1 : NQ][M];
@@ -298,17 +310,14 @@ if constexpr (FA) {
         __syncthreads();
         // every GEMM tile of the slice: item = (axis, n-tile); outputs overwrite their inputs
         for (int item = warp; item < DIM * NT; item += NW) {
-          const int a = item / NT, nt = item % NT;
+          const int a = item / NT, nt = item - a * NT;
           const int sa = (a == 0) ? P0 : (a == 1) ? P1 : 1;
-          const int sb = (a == 0) ? P1 : P0;
-          const int sc2 = (a == 2) ? P1 : 1;
           double* slab = sFA + a * S::R_FA;
+          const int* tab = sTab + a * S::RP;
           double cacc[MT][2];
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt) { cacc[mt][0] = 0.0; cacc[mt][1] = 0.0; }
-          const int rb = min(nt * 8 + (lane >> 2), RR - 1);
-          const int cb = rb / NF, yb = rb % NF;
-          const double* bbase = slab + cb * SC + (yb / NQ) * sb + (yb % NQ) * sc2;
+          const double* bbase = slab + tab[nt * 8 + (lane >> 2)];
           double bv[KC];
 #pragma unroll
           for (int kc = 0; kc < KC; ++kc) bv[kc] = bbase[min(kc * 4 + (lane & 3), NQ - 1) * sa];
@@ -324,10 +333,7 @@ if constexpr (FA) {
             for (int e2 = 0; e2 < 2; ++e2) {
               const int ip = mt * 8 + (lane >> 2);
               const int r = nt * 8 + 2 * (lane & 3) + e2;
-              if (ip < NQ && r < RR) {
-                const int c = r / NF, y = r % NF;
-                slab[c * SC + ip * sa + (y / NQ) * sb + (y % NQ) * sc2] = cacc[mt][e2];
-              }
+              if (ip < NQ && r < RR) slab[tab[r] + ip * sa] = cacc[mt][e2];
             }
         }
         __syncthreads();
