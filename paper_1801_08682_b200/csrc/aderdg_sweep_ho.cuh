@@ -42,9 +42,9 @@ struct ShapeHO {
   static constexpr int RP = NT * 8;
   // padded natural node layout [c][SC] (brute-forced: stores, DMMA B loads and
   // C scatters of every axis are at most 3-way bank conflicted)
-  static constexpr int P1 = (NQ == 10) ? 13 : 11;
-  static constexpr int P0 = (NQ == 7) ? 77 : (NQ == 8) ? 91 : (NQ == 9) ? 107 : 131;
-  static constexpr int SC = (NQ == 7) ? 541 : (NQ == 8) ? 729 : (NQ == 9) ? 965 : 1311;
+  static constexpr int P1 = (NQ == 10) ? 13 : (NQ == 6) ? 6 : 11;
+  static constexpr int P0 = (NQ == 6) ? 36 : (NQ == 7) ? 77 : (NQ == 8) ? 91 : (NQ == 9) ? 107 : 131;
+  static constexpr int SC = (NQ == 6) ? 217 : (NQ == 7) ? 541 : (NQ == 8) ? 729 : (NQ == 9) ? 965 : 1311;
   static constexpr int REC = 2 * NF * M + 2;
   // shared memory (doubles)
   static constexpr int R_RED = 2 * NW + 2 * DIM + 4;
