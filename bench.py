@@ -26,6 +26,7 @@ its batched restatement) on a bounded sample of the same workload, rank 0 only.
 """
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -265,32 +266,45 @@ def main():
         h.call("adg_sync")
         step0 = h.lib.adg_step_count(h.h)
         n = min(remaining, max(1, E - warm))
-        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n)]
-        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        barrier()
-        torch.cuda.synchronize()
-        if not clocks_started:
-            clocks.start()
-            clocks_started = True
-            time.sleep(0.05)
-        start.record()
-        for i in range(n):
-            e0, e1, e2, e3 = ev[i]
-            e0.record()
-            h.call("adg_phase_rerun")
-            e1.record()
-            drv.halo.exchange(drv.tr[h.lib.adg_trace_parity(h.h)])
-            e2.record()
-            h.call("adg_phase_sweep")
-            e3.record()
-            drv.halo.reduce(drv.red)
-            h.call("adg_phase_finish")
-        stop.record()
-        torch.cuda.synchronize()
-        barrier()
-        h.call("adg_sync")
-        seg_ms.append(start.elapsed_time(stop))
-        kern_ms += sum(e[0].elapsed_time(e[1]) + e[2].elapsed_time(e[3]) for e in ev)
+        if world == 1:
+            # single GPU: the C side enqueues the n steps back to back with CUDA
+            # events around the segment and every sweep-kernel launch
+            torch.cuda.synchronize()
+            if not clocks_started:
+                clocks.start()
+                clocks_started = True
+                time.sleep(0.05)
+            tout = (ctypes.c_double * 2)()
+            h.call("adg_run_timed", n, tout)
+            seg_ms.append(tout[0])
+            kern_ms += tout[1]
+        else:
+            ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n)]
+            start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            barrier()
+            torch.cuda.synchronize()
+            if not clocks_started:
+                clocks.start()
+                clocks_started = True
+                time.sleep(0.05)
+            start.record()
+            for i in range(n):
+                e0, e1, e2, e3 = ev[i]
+                e0.record()
+                h.call("adg_phase_rerun")
+                e1.record()
+                drv.halo.exchange(drv.tr[h.lib.adg_trace_parity(h.h)])
+                e2.record()
+                h.call("adg_phase_sweep")
+                e3.record()
+                drv.halo.reduce(drv.red)
+                h.call("adg_phase_finish")
+            stop.record()
+            torch.cuda.synchronize()
+            barrier()
+            h.call("adg_sync")
+            seg_ms.append(start.elapsed_time(stop))
+            kern_ms += sum(e[0].elapsed_time(e[1]) + e[2].elapsed_time(e[3]) for e in ev)
         recs += h.step_records(step0 + 1, n)
         remaining -= n
         first = False

@@ -160,6 +160,11 @@ int        adg_trace_parity(const adg_handle* h); /* parity the next sweep reads
 
 /* Timing helpers for bench.py: launches on the handle's stream. */
 adg_status adg_flush_l2(adg_handle* h);
+/* Enqueue `steps` realisation steps (single GPU) with CUDA events around the
+ * whole segment and around every sweep-kernel launch; synchronises once.
+ * out[0] = elapsed ms of the segment, out[1] = summed ms of the sweep-kernel
+ * launches (rerun pass + sweep), both measured on the handle's stream. */
+adg_status adg_run_timed(adg_handle* h, int steps, double* out);
 
 #ifdef __cplusplus
 }

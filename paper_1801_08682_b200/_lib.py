@@ -29,6 +29,7 @@ EXPORTS = (
     "adg_last_error", "adg_layout_info", "adg_buffer", "adg_phase_seed",
     "adg_phase_seed_finish", "adg_phase_rerun", "adg_phase_sweep",
     "adg_phase_finish", "adg_trace_parity", "adg_flush_l2", "adg_reset", "adg_set_dt_new",
+    "adg_run_timed",
 )
 
 
@@ -111,6 +112,7 @@ def load_library(path=None):
         "adg_flush_l2": (ctypes.c_int, [H]),
         "adg_reset": (ctypes.c_int, [H]),
         "adg_set_dt_new": (ctypes.c_int, [H, ctypes.c_double]),
+        "adg_run_timed": (ctypes.c_int, [H, ctypes.c_int, dp]),
     }
     for name, (res, args) in proto.items():
         fn = getattr(lib, name)

@@ -648,6 +648,47 @@ adg_status adg_buffer(adg_handle* h, int which, void** ptr, size_t* bytes) {
   return ADG_ERR_CONFIG;
 }
 
+adg_status adg_run_timed(adg_handle* h, int steps, double* out) {
+  if (!h || !out || steps < 1) return ADG_ERR_CONFIG;
+  if (h->hst.status) return status_from_state(h);
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  if (!straightforward(h) && h->sweep_index == 0)
+    return fail(h, ADG_ERR_CONFIG, "adg_run_timed needs a primed driver (run one step first)");
+  std::vector<cudaEvent_t> ev(4 * (size_t)steps + 2);
+  for (auto& e : ev) CUDA_TRY(h, cudaEventCreate(&e));
+  adg_status s = ADG_OK;
+  CUDA_TRY(h, cudaEventRecord(ev[0], h->stream));
+  for (int i = 0; i < steps && s == ADG_OK; ++i) {
+    CUDA_TRY(h, cudaEventRecord(ev[2 + 4 * i], h->stream));
+    s = adg_phase_rerun(h);
+    CUDA_TRY(h, cudaEventRecord(ev[3 + 4 * i], h->stream));
+    if (s != ADG_OK) break;
+    CUDA_TRY(h, cudaEventRecord(ev[4 + 4 * i], h->stream));
+    s = adg_phase_sweep(h);
+    CUDA_TRY(h, cudaEventRecord(ev[5 + 4 * i], h->stream));
+    if (s != ADG_OK) break;
+    s = adg_phase_finish(h);
+  }
+  CUDA_TRY(h, cudaEventRecord(ev[1], h->stream));
+  CUDA_TRY(h, cudaEventSynchronize(ev[1]));
+  float ms = 0.f;
+  CUDA_TRY(h, cudaEventElapsedTime(&ms, ev[0], ev[1]));
+  out[0] = ms;
+  double kern = 0.0;
+  for (int i = 0; i < steps; ++i) {
+    float a = 0.f, b = 0.f;
+    CUDA_TRY(h, cudaEventElapsedTime(&a, ev[2 + 4 * i], ev[3 + 4 * i]));
+    CUDA_TRY(h, cudaEventElapsedTime(&b, ev[4 + 4 * i], ev[5 + 4 * i]));
+    kern += a + b;
+  }
+  out[1] = kern;
+  for (auto& e : ev) cudaEventDestroy(e);
+  if (s != ADG_OK) return s;
+  s = pull_state(h);
+  if (s != ADG_OK) return s;
+  return status_from_state(h);
+}
+
 adg_status adg_flush_l2(adg_handle* h) {
   if (!h) return ADG_ERR_CONFIG;
   if (!h->flush) {
