@@ -77,6 +77,9 @@ typedef struct {
   int driver_mode;       /* 0: fused single-touch (scheduler.py:370-449); 1: straightforward
                             (scheduler.py:230-313: predict pass, then Riemann/corrector pass,
                             dt = dt_new, no priming, no rerun)                               */
+  int system;            /* PDE plug-in (pde.py:16-102): 0 EulerSystem(d), m = d+2;
+                            1 AdvectionSystem(d, velocity), m = 1                            */
+  double velocity[3];    /* AdvectionSystem velocity (first d used)        */
 } adg_config;
 
 typedef struct {

@@ -22,6 +22,7 @@ imports ``/root/reference/pkg/src/aderdg`` in the build container and writes
 Reference citations (``src/`` = ``/root/reference/pkg/src/aderdg/``):
   basis       src/basis.py:31-122         make_basis / Gauss-Legendre / lagrange_eval
   pde         src/pde.py:12-67            EulerSystem pressure / flux / speed / admissible
+              src/pde.py:70-94            AdvectionSystem flux / speed / admissible
   kernels     src/kernels.py:46-229       predict / extrapolate / integrate_volume /
                                           solve_riemann / integrate_face / update /
                                           calc_time_step
@@ -189,6 +190,47 @@ def admissible_per_cell(Q, d):
     return finite & rho_ok & p_ok
 
 
+class EulerPDE:
+    """src/pde.py:16-67 as a plug-in of the batched kernels."""
+
+    name = "euler"
+
+    def __init__(self, d):
+        self.d, self.m = d, d + 2
+
+    def flux(self, Q):
+        return flux(Q, self.d)
+
+    def max_signal_speed(self, Q, axis):
+        return max_signal_speed(Q, axis, self.d)
+
+    def admissible_per_cell(self, Q):
+        return admissible_per_cell(Q, self.d)
+
+
+class AdvectionPDE:
+    """src/pde.py:70-94: F_a = v_a q, speed |v_a|, admissible iff finite."""
+
+    name = "advection"
+
+    def __init__(self, d, velocity):
+        self.d, self.m = d, 1
+        self.velocity = np.asarray(velocity, dtype=float)[:d]
+
+    def flux(self, Q):
+        F = np.empty((self.d,) + Q.shape)
+        for a in range(self.d):
+            F[a] = self.velocity[a] * Q
+        return F
+
+    def max_signal_speed(self, Q, axis):
+        return np.full(Q.shape[:-1], abs(self.velocity[axis]))
+
+    def admissible_per_cell(self, Q):
+        C = Q.shape[0]
+        return np.all(np.isfinite(Q.reshape(C, -1)), axis=1)
+
+
 # ---------------------------------------------------------------------------
 # grid topology (src/mesh.py:167-243, periodic)
 
@@ -208,9 +250,10 @@ def neighbour_tables(d, K):
 class OracleKernels:
     """Batched restatement of ``Kernels`` (src/kernels.py:37-229) for Euler."""
 
-    def __init__(self, d, p, L, cfl=DEFAULT_CFL):
+    def __init__(self, d, p, L, cfl=DEFAULT_CFL, pde=None):
         self.d, self.p, self.L = d, p, L
-        self.m = d + 2
+        self.pde = pde if pde is not None else EulerPDE(d)
+        self.m = self.pde.m
         self.basis = b = make_basis(p)
         self.n = b.n
         self.K = 3 ** L
@@ -243,7 +286,7 @@ class OracleKernels:
                 break
             qa = q[active]
             with np.errstate(all="ignore"):
-                F = flux(qa, d)
+                F = self.pde.flux(qa)
                 div = apply_matrix(b.diff, F[0], axis=1)
                 for a in range(1, d):
                     div += apply_matrix(b.diff, F[a], axis=1 + a)
@@ -258,7 +301,7 @@ class OracleKernels:
             done = bad | (delta <= tol[active])
             active = active[~done]
         with np.errstate(all="ignore"):
-            f = flux(q, d)
+            f = self.pde.flux(q)
         fail |= ~np.all(np.isfinite(f.reshape(d, C, -1)), axis=(0, 2))
         for k, v in Counter(iters[~fail].tolist()).items():
             self.picard_hist[k] += v
@@ -304,8 +347,8 @@ class OracleKernels:
                 continue
             C = qp.shape[0]
             with np.errstate(all="ignore"):
-                sm = np.max(max_signal_speed(qm, a, d).reshape(C, -1), axis=1)
-                sp = np.max(max_signal_speed(qp, a, d).reshape(C, -1), axis=1)
+                sm = np.max(self.pde.max_signal_speed(qm, a).reshape(C, -1), axis=1)
+                sp = np.max(self.pde.max_signal_speed(qp, a).reshape(C, -1), axis=1)
             alpha = np.maximum(sm, sp)   # python max(a, b) == np.maximum for finite inputs
             al = alpha.reshape((-1,) + (1,) * (qp.ndim - 1))
             out.append(0.5 * (fm + fp) - 0.5 * al * (qp - qm))
@@ -331,11 +374,11 @@ class OracleKernels:
     def calc_time_step(self, Q):
         d = self.d
         C = Q.shape[0]
-        ok = admissible_per_cell(Q, d)
+        ok = self.pde.admissible_per_cell(Q)
         lam = np.zeros(C)
         with np.errstate(all="ignore"):
             for a in range(d):
-                lam = np.maximum(lam, np.max(max_signal_speed(Q, a, d).reshape(C, -1), axis=1))
+                lam = np.maximum(lam, np.max(self.pde.max_signal_speed(Q, a).reshape(C, -1), axis=1))
             dt = self.cfl * self.h / (d * (2 * self.p + 1) * lam)
         dt = np.where(lam <= 0.0, np.inf, dt)
         return dt, ok, lam
@@ -393,8 +436,12 @@ class FusedDriver:
 
     def __init__(self, Q, d, p, L, cfl=DEFAULT_CFL, c_dt=DEFAULT_C_DT,
                  averaging="strict", forced_dt=None, inject_rerun=False,
-                 spike_step=None, spike_factor=3.0):
-        self.k = OracleKernels(d, p, L, cfl)
+                 spike_step=None, spike_factor=3.0, velocity=None):
+        """``velocity`` given: AdvectionSystem(d, velocity) (m = 1), else Euler."""
+        pde = AdvectionPDE(d, velocity) if velocity is not None else EulerPDE(d)
+        if velocity is not None and spike_step is not None:
+            raise OracleError("ConfigurationError", "the speed spike is defined for Euler runs")
+        self.k = OracleKernels(d, p, L, cfl, pde)
         self.d, self.p, self.L = d, p, L
         self.Q = Q
         self.D = np.zeros_like(Q)                       # src/mesh.py:238-239

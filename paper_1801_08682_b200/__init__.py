@@ -11,14 +11,14 @@ the in-tree ``libaderdg_b200.so`` and a CUDA device.
 from .basis import Basis1D, make_basis
 from .errors import (ConfigurationError, DeviceError, DomainError, NumericalError,
                      PredictorFailureError, ResourceBudgetError, SchedulingOrderError)
-from .solver import (Driver, EulerSystem, Grid, Kernels, TimeControl, build_grid,
+from .solver import (AdvectionSystem, Driver, EulerSystem, Grid, Kernels, TimeControl, build_grid,
                      device_bytes, gather)
 
 __version__ = "0.1.0"
 
 __all__ = [
     "Basis1D", "ConfigurationError", "DeviceError", "DomainError", "Driver",
-    "EulerSystem", "Grid", "Kernels", "NumericalError", "PredictorFailureError",
+    "AdvectionSystem", "EulerSystem", "Grid", "Kernels", "NumericalError", "PredictorFailureError",
     "ResourceBudgetError", "SchedulingOrderError", "TimeControl", "build_grid",
     "device_bytes", "gather", "make_basis",
 ]

@@ -41,7 +41,8 @@ class AdgConfig(ctypes.Structure):
         ("inject_rerun", ctypes.c_int), ("spike_step", ctypes.c_int),
         ("spike_factor", ctypes.c_double), ("device", ctypes.c_int),
         ("rank", ctypes.c_int), ("world", ctypes.c_int), ("halo_mode", ctypes.c_int),
-        ("driver_mode", ctypes.c_int),
+        ("driver_mode", ctypes.c_int), ("system", ctypes.c_int),
+        ("velocity", ctypes.c_double * 3),
     ]
 
 

@@ -26,16 +26,16 @@ namespace {
 
 typedef void (*launch_fn)(const SweepParams&, unsigned grid, cudaStream_t s);
 
-template <int DIM, int NQ>
+template <class PDE, int DIM, int NQ>
 void launch_sweep(const SweepParams& P, unsigned grid, cudaStream_t s) {
-  using S = Shape<DIM, NQ>;
+  using S = Shape<DIM, NQ, PDE::M>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(sweep_kernel<DIM, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(sweep_kernel<PDE, DIM, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)S::SMEM_BYTES);
     attr = true;
   }
-  sweep_kernel<DIM, NQ><<<grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
+  sweep_kernel<PDE, DIM, NQ><<<grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
 }
 
 template <int NQ, int TS, bool DMMA, bool ROLLED = (NQ == 4), int MB = 0>
@@ -56,7 +56,30 @@ struct Dispatch {
 };
 
 template <int DIM, int NQ>
-Dispatch make_dispatch() { return Dispatch{&launch_sweep<DIM, NQ>, Shape<DIM, NQ>::REC}; }
+Dispatch make_dispatch() { return Dispatch{&launch_sweep<EulerPDE<DIM>, DIM, NQ>, Shape<DIM, NQ>::REC}; }
+
+template <int DIM, int NQ>
+Dispatch make_dispatch_adv() {
+  return Dispatch{&launch_sweep<AdvectionPDE<DIM>, DIM, NQ>, Shape<DIM, NQ, 1>::REC};
+}
+
+// AdvectionSystem: the generic kernel with the advection plug-in, every d and p
+template <int DIM>
+bool dispatch_adv(int n, Dispatch* out) {
+  switch (n) {
+    case 1: *out = make_dispatch_adv<DIM, 1>(); return true;
+    case 2: *out = make_dispatch_adv<DIM, 2>(); return true;
+    case 3: *out = make_dispatch_adv<DIM, 3>(); return true;
+    case 4: *out = make_dispatch_adv<DIM, 4>(); return true;
+    case 5: *out = make_dispatch_adv<DIM, 5>(); return true;
+    case 6: *out = make_dispatch_adv<DIM, 6>(); return true;
+    case 7: *out = make_dispatch_adv<DIM, 7>(); return true;
+    case 8: *out = make_dispatch_adv<DIM, 8>(); return true;
+    case 9: *out = make_dispatch_adv<DIM, 9>(); return true;
+    case 10: *out = make_dispatch_adv<DIM, 10>(); return true;
+  }
+  return false;
+}
 
 template <int NQ>
 void launch_sweep_ho(const SweepParams& P, unsigned grid, cudaStream_t s) {
@@ -102,8 +125,9 @@ Dispatch make_dispatch_v2() {
 }
 
 
-bool dispatch_for(int d, int p, Dispatch* out) {
+bool dispatch_for(int d, int p, int system, Dispatch* out) {
   const int n = p + 1;
+  if (system == 1) return d == 2 ? dispatch_adv<2>(n, out) : d == 3 ? dispatch_adv<3>(n, out) : false;
   if (d == 2) {
     switch (n) {
       case 1: *out = make_dispatch<2, 1>(); return true;
@@ -228,6 +252,7 @@ static SweepParams sweep_params(adg_handle* h, int mode) {
   P.h = h->h;
   P.cfl = h->cfg.cfl;
   P.spike_factor = h->cfg.spike_factor;
+  for (int a = 0; a < 3; ++a) P.vel[a] = h->cfg.velocity[a];
   return P;
 }
 
@@ -306,12 +331,16 @@ adg_status adg_create(const adg_config* cfg, adg_handle** out) {
   if (c.p < 0 || c.p > 9) { snprintf(buf, sizeof buf, "order p must be in [0, 9], got %d", c.p); h->err = buf; *out = h; return ADG_ERR_CONFIG; }
   if (!(c.c_dt > 0.0 && c.c_dt <= 1.0)) { snprintf(buf, sizeof buf, "c_dt must be in (0, 1], got %g", c.c_dt); h->err = buf; *out = h; return ADG_ERR_CONFIG; }
   if (c.driver_mode != 0 && c.driver_mode != 1) { h->err = "driver_mode must be 0 (fused) or 1 (straightforward)"; *out = h; return ADG_ERR_CONFIG; }
-  if (!dispatch_for(c.d, c.p, &h->disp)) {
+  if (c.system != 0 && c.system != 1) { h->err = "system must be 0 (euler) or 1 (advection)"; *out = h; return ADG_ERR_CONFIG; }
+  if (c.system == 1 && c.spike_step >= 0) {                      // scheduler.py:170-171
+    h->err = "the speed spike is defined for Euler runs"; *out = h; return ADG_ERR_CONFIG;
+  }
+  if (!dispatch_for(c.d, c.p, c.system, &h->disp)) {
     snprintf(buf, sizeof buf, "no sm_100a kernel instantiated for d=%d p=%d", c.d, c.p);
     h->err = buf; *out = h; return ADG_ERR_CONFIG;
   }
   h->n = c.p + 1;
-  h->m = c.d + 2;
+  h->m = c.system == 1 ? 1 : c.d + 2;
   h->NS = 1; for (int a = 0; a < c.d; ++a) h->NS *= h->n;
   h->NF = h->NS / h->n;
   h->REC = h->disp.rec;

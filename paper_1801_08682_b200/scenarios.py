@@ -109,11 +109,32 @@ def uniform_state(d, L, p, state=None):
                            (3 ** (d * L),) + (n,) * d + (d + 2,)).copy()
 
 
+GAUSSIAN_SIGMA = 0.25          # src/cli.py:30
+ADVECTION_VELOCITY = (1.0, 0.5, 0.25)   # src/cli.py:31
+
+
+def gaussian_profile(x):
+    """Smooth periodic bump on the unit cube (src/cli.py:96-100)."""
+    return np.exp(-np.sum(np.sin(np.pi * (x - 0.5)) ** 2, axis=-1)
+                  / (2.0 * GAUSSIAN_SIGMA ** 2))
+
+
+def gaussian_advect(d, L, p, noise=0.0, seed=0):
+    """Scenario ``gaussian-advect`` (src/cli.py:139-142): q = gaussian_profile(x),
+    m = 1; optional seeded U(-noise, noise) per node for harder parity cases."""
+    x = node_coordinates(d, L, p)
+    q = gaussian_profile(x)
+    if noise:
+        q = q + np.random.default_rng(seed).uniform(-noise, noise, size=q.shape)
+    return q[..., None]
+
+
 SCENARIOS = {
     "bump": gaussian_bump_noise,
     "fourier": random_fourier,
     "wave": smooth_density_wave,
     "uniform": uniform_state,
+    "gauss": gaussian_advect,
 }
 
 

@@ -27,6 +27,7 @@ Reference citations (``src/`` = ``/root/reference/pkg/src/aderdg/``):
 
 import ctypes
 import math
+import time
 from collections import Counter
 
 import numpy as np
@@ -74,6 +75,38 @@ class EulerSystem:
         return bool(np.all(self.pressure(Q) > 1e-12))
 
 
+class AdvectionSystem:
+    """Scalar linear advection ``q_t + v . grad q = 0`` (src/pde.py:70-102).
+    The flux ``v_a q``, the signal speed ``|v_a|`` and the finiteness test are
+    compiled into the generic sm_100a sweep kernel (``AdvectionPDE``); the
+    velocity travels in ``adg_config.velocity``.  ``exact_solution`` is the
+    analytic oracle of the convergence study (host-side post-processing)."""
+
+    def __init__(self, dim, velocity, profile=None):
+        from .errors import DomainError
+        self.d = dim
+        self.m = 1
+        self.name = "advection"
+        self.velocity = np.asarray(velocity, dtype=float)
+        if self.velocity.shape != (dim,):
+            raise DomainError(f"velocity must have {dim} components")
+        self.profile = profile
+
+    def max_signal_speed(self, Q, axis):
+        Q = np.asarray(Q, dtype=float)
+        return np.full(Q.shape[:-1], abs(self.velocity[axis]))
+
+    def is_admissible(self, Q):
+        return bool(np.all(np.isfinite(np.asarray(Q, dtype=float))))
+
+    def exact_solution(self, x, t):
+        from .errors import DomainError
+        if self.profile is None:
+            raise DomainError("advection system has no initial profile attached")
+        shifted = np.mod(np.asarray(x, dtype=float) - t * self.velocity, 1.0)
+        return self.profile(shifted)[..., None]
+
+
 class Cell:
     """Reference Cell view (src/mesh.py:27-40): ``Q`` is a view into the
     grid's contiguous state array."""
@@ -118,10 +151,10 @@ class Grid:
     ``Q`` holds every cell's coefficients in reference order
     ``(n_cells,) + (p+1,)*d + (m,)``; ``cells[i].Q`` views into it."""
 
-    def __init__(self, d, L, p, m, boundary="periodic"):
+    def __init__(self, d, L, p, m, boundary="periodic", storage="hull"):
         self.d, self.L, self.p, self.m = d, L, p, m
         self.boundary = boundary
-        self.storage = "hull"
+        self.storage = storage
         self.h = 3.0 ** (-L)                       # src/mesh.py:71
         n = p + 1
         self.Q = np.zeros((3 ** (d * L),) + (n,) * d + (m,))
@@ -138,11 +171,18 @@ class Grid:
     def node_block_shape(self):
         return (self.p + 1,) * self.d + (self.m,)
 
+    def persistent_doubles(self, include_limiter=False):
+        """src/mesh.py:124-137: doubles the reference allocates for this grid
+        (its storage layout; the GPU's own HBM is ``device_bytes``)."""
+        from .metrics import estimate_persistent_doubles
+        return estimate_persistent_doubles(self.d, self.L, self.p, self.m, self.boundary, self.storage)
 
-def device_bytes(d, L, p):
+
+def device_bytes(d, L, p, m=None):
     """Persistent HBM of one single-GPU solver: Q, D and two parities of
     time-collapsed face records (2d per cell, 2 n^(d-1) m + 2 doubles each)."""
-    n, m, cells = p + 1, d + 2, 3 ** (d * L)
+    n, cells = p + 1, 3 ** (d * L)
+    m = d + 2 if m is None else m
     rec = 2 * n ** (d - 1) * m + 2
     slots = (3 ** L + 2) * 3 ** (L * (d - 1))
     return 8 * (2 * cells * n ** d * m + 2 * 2 * d * slots * rec)
@@ -163,22 +203,22 @@ def build_grid(d, L, p, m, boundary="periodic", storage="hull",
         raise ConfigurationError("the GPU path implements periodic boundaries only")
     if storage not in ("hull", "spacetime"):
         raise ConfigurationError(f"unknown storage layout {storage!r}")
-    if m != d + 2:
-        raise ConfigurationError(f"the GPU path implements Euler (m = d+2), got m={m}")
+    if m not in (d + 2, 1):
+        raise ConfigurationError(f"the GPU path implements Euler (m = d+2) and advection (m = 1), got m={m}")
     if budget_bytes is not None:
-        req = device_bytes(d, L, p)
+        req = device_bytes(d, L, p, m)
         if req > budget_bytes:
             raise ResourceBudgetError(req, budget_bytes)
-    return Grid(d, L, p, m, boundary)
+    return Grid(d, L, p, m, boundary, storage)
 
 
 class Kernels:
     """Configuration carrier of the reference kernel suite (src/kernels.py:46-60)."""
 
     def __init__(self, system, basis, grid, ledger=None, cfl=DEFAULT_CFL):
-        if getattr(system, "name", None) != "euler":
-            raise ConfigurationError("the GPU kernels are instantiated for the Euler system only")
-        if system.d != grid.d or basis.p != grid.p:
+        if getattr(system, "name", None) not in ("euler", "advection"):
+            raise ConfigurationError("the GPU kernels are instantiated for the Euler and advection systems only")
+        if system.d != grid.d or basis.p != grid.p or system.m != grid.m:
             raise ConfigurationError("system / basis / grid disagree on d or p")
         self.system, self.basis, self.grid = system, basis, grid
         self.ledger = ledger
@@ -216,6 +256,11 @@ def _config(grid, kernels, tc, inject_rerun, spike_step, spike_factor, device, r
     cfg.device = int(device)
     cfg.rank, cfg.world = int(rank), int(world)
     cfg.driver_mode = 1 if mode == "straightforward" else 0
+    system = kernels.system
+    if system.name == "advection":
+        cfg.system = 1
+        for a in range(grid.d):
+            cfg.velocity[a] = float(system.velocity[a])
     return cfg
 
 
@@ -255,6 +300,8 @@ class Driver:
                 raise ConfigurationError("traversal must be a permutation of the cells")
         elif traversal not in ("lexicographic", "peano"):
             raise ConfigurationError(f"unknown traversal kind {traversal!r}")
+        if spike_step is not None and kernels.system.name != "euler":
+            raise ConfigurationError("the speed spike is defined for Euler runs")
         if host_sync not in ("step", "run", "manual"):
             raise ConfigurationError(f"unknown host_sync {host_sync!r}")
         # the fused result is traversal-invariant (tests/test_scheduler.py:111-116):
@@ -295,38 +342,54 @@ class Driver:
         T, dt_old, dt_new, dt_adm = self.handle.time_control()
         self.tc.T, self.tc.dt_old, self.tc.dt_new, self.tc.dt_adm = T, dt_old, dt_new, dt_adm
 
-    def _absorb(self, recs):
+    def _book_ledger(self, r, rec):
+        """Access counts of step ``r.step`` in the reference's ledger units
+        (src/scheduler.py:459-481 with src/metrics.py:157-175); see metrics.py."""
+        from . import metrics
+        led = self.kernels.ledger
+        if led is None or not hasattr(led, "book"):
+            return
+        g = self.grid
+        rec.update(metrics.record_step(led, self.mode, r.step, r.reruns, g.n_cells,
+                                       g.d * g.n_cells))          # periodic: d faces per cell
+
+    def _absorb(self, recs, wall_time=0.0):
         for r in recs:
             if r.reruns:
                 self.reruns_by_step[r.step] += r.reruns
             self.picard_iters += r.picard_iters
             self.predicts += r.predicts
-            self.step_records.append({
+            rec = {
                 "step": r.step, "T": r.T, "dt_old": r.dt_old, "dt_new": r.dt_new,
                 "dt_adm": r.dt_adm, "reruns": r.reruns, "troubled": 0,
+                "wall_time": wall_time / max(1, len(recs)),
                 "picard_iters": r.picard_iters, "predicts": r.predicts,
-            })
+            }
+            self._book_ledger(r, rec)
+            self.step_records.append(rec)
         lib, h = self.handle.lib, self.handle.h
         self.step_count = lib.adg_step_count(h)
         self.rerun_count = lib.adg_rerun_count(h)
         self.sweep_count = lib.adg_sweep_count(h)
         self._pull_tc()
 
-    def _finish(self, recs, err):
-        self._absorb(recs)
+    def _finish(self, recs, err, wall_time=0.0):
+        self._absorb(recs, wall_time)
         if err is not None:
             raise err
 
     # -- public API (src/scheduler.py:190-226) --------------------------------
     def step(self):
         rec = _lib.AdgStepRecord()
+        t0 = time.perf_counter()
         st = self.handle.lib.adg_step(self.handle.h, rec)
+        wall = time.perf_counter() - t0
         err = None
         try:
             self.handle.check(st, "adg_step")
         except Exception as e:  # keep the driver's counters consistent before raising
             err = e
-        self._finish([rec] if st == 0 else [], err)
+        self._finish([rec] if st == 0 else [], err, wall)
         if self.host_sync == "step":
             self.sync_state()
         return self.step_count
@@ -345,7 +408,9 @@ class Driver:
             return self.step_count
         recs = (_lib.AdgStepRecord * steps)()
         before = self.step_count
+        t0 = time.perf_counter()
         st = self.handle.lib.adg_run(self.handle.h, steps, recs)
+        wall = time.perf_counter() - t0
         err = None
         try:
             self.handle.check(st, "adg_run")
@@ -354,7 +419,7 @@ class Driver:
         done = self.handle.lib.adg_step_count(self.handle.h) - before
         if self.host_sync in ("step", "run"):
             self.sync_state()
-        self._finish(list(recs)[:done], err)
+        self._finish(list(recs)[:done], err, wall)
         return self.step_count
 
     def _run_to(self, final_time):
@@ -382,5 +447,5 @@ def gather(grid):
     return np.array(grid.Q)
 
 
-__all__ = ["EulerSystem", "Grid", "Cell", "build_grid", "Kernels", "TimeControl",
+__all__ = ["EulerSystem", "AdvectionSystem", "Grid", "Cell", "build_grid", "Kernels", "TimeControl",
            "Driver", "gather", "make_basis", "device_bytes"]

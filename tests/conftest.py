@@ -27,6 +27,24 @@ def load_golden(name):
     return out
 
 
+def golden_problem(meta):
+    """Initial state and PDE of a golden case: (Q0, velocity or None).  The
+    ``gauss*`` scenarios are AdvectionSystem(d, (1.0, 0.5, 0.25)[:d]) runs
+    (src/cli.py:31,139-142), everything else EulerSystem(d)."""
+    from paper_1801_08682_b200 import scenarios
+    d, L, p = meta["d"], meta["L"], meta["p"]
+    scen = meta["scenario"]
+    if scen.startswith("gauss"):
+        kw = {"noise": 1e-2, "seed": 1} if scen == "gauss_noise" else {}
+        return scenarios.build("gauss", d, L, p, **kw), scenarios.ADVECTION_VELOCITY[:d]
+    return scenarios.build(scen, d, L, p), None
+
+
+def make_system(d, velocity):
+    from paper_1801_08682_b200 import AdvectionSystem, EulerSystem
+    return EulerSystem(d) if velocity is None else AdvectionSystem(d, velocity)
+
+
 def rel_linf(a, b):
     a = np.asarray(a)
     b = np.asarray(b)

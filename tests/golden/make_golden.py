@@ -63,6 +63,16 @@ SMALL = {
     "sf_wave_d2_L2_p3_forced": ("wave", 2, 2, 3, 10, {"mode": "straightforward"}, {"forced_dt": 2e-4}, True),
     "sf_bump_d3_L1_p5_creeping": ("bump", 3, 1, 5, 4, {"mode": "straightforward"}, {"averaging": "creeping"}, True),
     "sf_wave_d2_L1_p2_spike": ("wave", 2, 1, 2, 8, {"mode": "straightforward", "spike_step": 4}, {}, True),
+    # AdvectionSystem(d, (1.0, 0.5, 0.25)[:d]) on the gaussian-advect profile (src/cli.py:139-142)
+    "adv_gauss_d2_L2_p3": ("gauss", 2, 2, 3, 10, {}, {}, True),
+    "adv_gauss_d2_L1_p0": ("gauss", 2, 1, 0, 6, {}, {}, True),
+    "adv_gauss_d2_L2_p2_forced": ("gauss", 2, 2, 2, 10, {}, {"forced_dt": 1e-3}, True),
+    "adv_gauss_d2_L1_p3_inject": ("gauss", 2, 1, 3, 4, {"inject_rerun": True}, {}, True),
+    "adv_gauss_d3_L1_p5": ("gauss", 3, 1, 5, 4, {}, {}, True),
+    "adv_gauss_d3_L1_p9": ("gauss", 3, 1, 9, 3, {}, {}, True),
+    "adv_noise_d3_L2_p3": ("gauss_noise", 3, 2, 3, 5, {}, {}, True),
+    "sf_adv_gauss_d2_L2_p3": ("gauss", 2, 2, 3, 8, {"mode": "straightforward"}, {}, True),
+    "sf_adv_gauss_d3_L1_p4_creeping": ("gauss", 3, 1, 4, 4, {"mode": "straightforward"}, {"averaging": "creeping"}, True),
 }
 BIG = {
     "bump_d3_L3_p3_cfg2": ("bump", 3, 3, 3, 20, {}, {}, False),
@@ -75,11 +85,16 @@ SAMPLE_STRIDE = 97
 
 
 def run_case(name, spec):
-    from aderdg import (Driver, EulerSystem, Kernels, NumericalError,
+    from aderdg import (AdvectionSystem, Driver, EulerSystem, Kernels, NumericalError,
                         PredictorFailureError, TimeControl, build_grid, make_basis)
     scen, d, L, p, steps, dkw, tkw, full = spec
-    Q0 = scenarios.build(scen, d, L, p)
-    system = EulerSystem(d)
+    if scen.startswith("gauss"):
+        from aderdg.cli import gaussian_profile
+        Q0 = scenarios.build("gauss", d, L, p, **({"noise": 1e-2, "seed": 1} if scen == "gauss_noise" else {}))
+        system = AdvectionSystem(d, scenarios.ADVECTION_VELOCITY[:d], profile=gaussian_profile)
+    else:
+        Q0 = scenarios.build(scen, d, L, p)
+        system = EulerSystem(d)
     basis = make_basis(p)
     dkw = dict(dkw)
     mode = dkw.pop("mode", "fused")
@@ -130,7 +145,7 @@ def run_case(name, spec):
         "Q_final_absmax": np.max(np.abs(Qf.reshape(-1, Qf.shape[-1])), axis=0),
         "picard_keys": np.array(sorted(hist), dtype=np.int64),
         "picard_vals": np.array([hist[k] for k in sorted(hist)], dtype=np.int64),
-        "meta": np.array(json.dumps({"scenario": scen, "d": d, "L": L, "p": p, "steps": steps,
+        "meta": np.array(json.dumps({"scenario": scen, "system": system.name, "d": d, "L": L, "p": p, "steps": steps,
                                      "driver_kwargs": dkw, "mode": mode, "tc_kwargs": tkw, "error": error,
                                      "wall_s": wall, "sweep_count": driver.sweep_count if driver else None,
                                      "rerun_count": driver.rerun_count if driver else None,

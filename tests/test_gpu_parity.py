@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import aderdg_oracle as O
-from conftest import golden_names, load_golden, rel_linf
+from conftest import golden_names, golden_problem, load_golden, make_system, rel_linf
 from paper_1801_08682_b200 import (Driver, EulerSystem, Kernels, NumericalError,
                                    PredictorFailureError, TimeControl, build_grid,
                                    make_basis, scenarios)
@@ -18,10 +18,11 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-10   # north_star: rel L-inf in fp64
 
 
-def make_driver(Q0, d, L, p, dkw=None, tkw=None, host_sync="run"):
-    grid = build_grid(d, L, p, d + 2)
+def make_driver(Q0, d, L, p, dkw=None, tkw=None, host_sync="run", velocity=None):
+    system = make_system(d, velocity)
+    grid = build_grid(d, L, p, system.m)
     grid.Q[...] = Q0
-    kern = Kernels(EulerSystem(d), make_basis(p), grid, None, cfl=0.9)
+    kern = Kernels(system, make_basis(p), grid, None, cfl=0.9)
     tc = TimeControl(c_dt=0.99, **(tkw or {}))
     return Driver(grid, kern, tc, "fused", host_sync=host_sync, **(dkw or {}))
 
@@ -39,8 +40,8 @@ def test_gpu_matches_reference_golden(cuda_ok, name):
     g = load_golden(name)
     meta = g["meta"]
     d, L, p = meta["d"], meta["L"], meta["p"]
-    Q0 = scenarios.build(meta["scenario"], d, L, p)
-    drv = make_driver(Q0, d, L, p, meta["driver_kwargs"], meta["tc_kwargs"])
+    Q0, vel = golden_problem(meta)
+    drv = make_driver(Q0, d, L, p, meta["driver_kwargs"], meta["tc_kwargs"], velocity=vel)
     drv.run(steps=meta["steps"])
     recs = records_array(drv)
     ref = g["records"]
@@ -73,6 +74,30 @@ def test_gpu_matches_oracle_random_seeds(cuda_ok, d, L, p, steps, seed):
     oh = dict(ora.k.picard_hist)
     assert sum(gh.values()) == sum(oh.values())
     assert abs(sum(k * v for k, v in gh.items()) - sum(k * v for k, v in oh.items())) <= 0.01 * sum(oh.values())
+
+
+@pytest.mark.parametrize("d,L,p,steps,seed", [(2, 2, 3, 5, 1), (3, 2, 2, 4, 2), (3, 1, 7, 3, 3),
+                                              (2, 1, 9, 3, 4), (3, 2, 4, 3, 5)])
+def test_gpu_advection_matches_oracle(cuda_ok, d, L, p, steps, seed):
+    """AdvectionSystem plug-in of the generic sweep kernel vs the oracle on noisy data."""
+    vel = (1.0, -0.5, 0.25)[:d]
+    Q0 = scenarios.build("gauss", d, L, p, noise=5e-2, seed=seed)
+    drv = make_driver(Q0, d, L, p, velocity=vel)
+    drv.run(steps=steps)
+    ora = O.FusedDriver(Q0.copy(), d, p, L, velocity=vel)
+    ora.run(steps)
+    assert rel_linf(drv.grid.Q, ora.Q) <= TOL
+    ra = records_array(drv)
+    rb = np.array([[r["step"], r["T"], r["dt_old"], r["dt_new"], r["dt_adm"], r["reruns"]]
+                   for r in ora.step_records])
+    assert np.max(np.abs(ra[:, 1:5] - rb[:, 1:5]) / np.abs(rb[:, 1:5])) < TOL
+
+
+def test_gpu_advection_rejects_spike(cuda_ok):
+    from paper_1801_08682_b200 import ConfigurationError
+    Q0 = scenarios.build("gauss", 2, 1, 2)
+    with pytest.raises(ConfigurationError):
+        make_driver(Q0, 2, 1, 2, dkw={"spike_step": 2}, velocity=(1.0, 0.5))
 
 
 def test_uniform_state_is_fixed_point(cuda_ok):
@@ -183,10 +208,11 @@ def test_gpu_straightforward_matches_reference(cuda_ok, name):
     g = load_golden(name)
     meta = g["meta"]
     d, L, p = meta["d"], meta["L"], meta["p"]
-    Q0 = scenarios.build(meta["scenario"], d, L, p)
-    grid = build_grid(d, L, p, d + 2)
+    Q0, vel = golden_problem(meta)
+    system = make_system(d, vel)
+    grid = build_grid(d, L, p, system.m)
     grid.Q[...] = Q0
-    kern = Kernels(EulerSystem(d), make_basis(p), grid, None, cfl=0.9)
+    kern = Kernels(system, make_basis(p), grid, None, cfl=0.9)
     drv = Driver(grid, kern, TimeControl(c_dt=0.99, **meta["tc_kwargs"]), "straightforward",
                  host_sync="run", **meta["driver_kwargs"])
     drv.run(steps=meta["steps"])

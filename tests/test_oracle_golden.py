@@ -5,19 +5,21 @@ import numpy as np
 import pytest
 
 import aderdg_oracle as O
-from conftest import golden_names, load_golden, rel_linf
-from paper_1801_08682_b200 import scenarios
+from conftest import golden_names, golden_problem, load_golden, rel_linf
 
 FAST = [n for n in golden_names() if n in (
     "bump_d2_L2_p3", "bump_d2_L1_p0", "bump_d2_L2_p1", "bump_d2_L1_p9", "bump_d2_L2_p6",
     "bump_d3_L1_p3", "bump_d3_L1_p2", "bump_d3_L1_p5", "fourier_d3_L1_p4",
     "wave_d2_L1_p2_spike", "wave_d2_L1_p3_inject", "wave_d2_L2_p3_forced",
-    "wave_d3_L1_p2_creeping", "uniform_d2_L1_p2", "bump_d2_L3_p3_cfg1") or n.startswith("sf_")]
+    "wave_d3_L1_p2_creeping", "uniform_d2_L1_p2", "bump_d2_L3_p3_cfg1")
+        or n.startswith("sf_") or n.startswith("adv_")]
 
 
 def run_oracle(meta):
-    Q0 = scenarios.build(meta["scenario"], meta["d"], meta["L"], meta["p"])
+    Q0, vel = golden_problem(meta)
     dkw = dict(meta["driver_kwargs"])
+    if vel is not None:
+        dkw["velocity"] = vel
     tkw = dict(meta["tc_kwargs"])
     cls = O.StraightforwardDriver if meta.get("mode", "fused") == "straightforward" else O.FusedDriver
     drv = cls(Q0.copy(), meta["d"], meta["p"], meta["L"], **dkw, **tkw)
