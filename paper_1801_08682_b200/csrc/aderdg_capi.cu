@@ -152,7 +152,9 @@ bool dispatch_for(int d, int p, int system, Dispatch* out) {
              : kernel_variant() == 5 ? make_dispatch_v2<4, 1, true, true>()
              : kernel_variant() == 6 ? make_dispatch_st()
              : kernel_variant() == 7 ? make_dispatch_v2<4, 1, true, false, 7>()
-             : kernel_variant() == 8 ? make_dispatch_v2<4, 1, true, false, 8>() : make_dispatch_v2<4, 1, true, false>();
+             : kernel_variant() == 8 ? make_dispatch_v2<4, 1, true, false, 8>()
+             : kernel_variant() == 14 ? make_dispatch_v2<4, 1, true, false>()      // axis 1 through shared memory
+             : make_dispatch_v2<4, 1, true, false, 10>();   // default: axis 1 via lane transpose + DMMA
         return true;
       case 5: *out = make_dispatch<3, 5>(); return true;
       case 6:

@@ -42,13 +42,15 @@ struct ShapeV2 {
   static constexpr int NWARPS = THREADS / 32;
   static constexpr int TH = NQ / TS;
   // CTAs/SM the register allocation must allow (TS = 1 at NQ = 6 keeps 60 doubles of Picard state)
-  static constexpr int MINB = (MINB_OVERRIDE && MINB_OVERRIDE != 9) ? MINB_OVERRIDE : (MINB_OVERRIDE == 9) ? 1
+  // MINB_OVERRIDE 10: axis-1 derivative on the tensor cores through a lane transpose (A1S)
+  static constexpr bool A1S = (MINB_OVERRIDE == 10);
+  static constexpr int MINB = (MINB_OVERRIDE && MINB_OVERRIDE != 9 && !A1S) ? MINB_OVERRIDE : (MINB_OVERRIDE == 9) ? 1
                             : (TS == 1 && NQ >= 6) ? 1
                             : THREADS <= 64 ? 6 : THREADS <= 128 ? 4 : (THREADS <= 256 ? 2 : 1);
   static constexpr int P0 = NQ * NQ + plane_pad(NQ);   // padded axis-0 plane stride
   static constexpr int PS = NQ * P0;                   // padded slice size
-  static constexpr int DS = DMMA ? DIM - 1 : DIM;      // axes through shared memory
-  static constexpr bool F1T = (NQ == 4) || (NQ == 6 && MINB_OVERRIDE == 9);  // axis-1 flux stored transposed, 16-byte gathers
+  static constexpr int DS = DMMA ? (A1S ? 1 : DIM - 1) : DIM;   // axes through shared memory
+  static constexpr bool F1T = !A1S && ((NQ == 4) || (NQ == 6 && MINB_OVERRIDE == 9));  // axis-1 flux stored transposed, 16-byte gathers
   static constexpr bool ROLL = ROLLED;                 // rolled slice loop (i-cache); NQ = 6 stays unrolled
   static constexpr int RR = 1;                         // slices per rolled trip
   static constexpr bool DBUF = (TS == 1 && (NQ == 4 || MINB_OVERRIDE == 9));  // double-buffered flux slices
@@ -76,6 +78,7 @@ struct ShapeV2 {
   static_assert((NS * M) % 2 == 0, "bulk copies need 16-byte sizes");
   static_assert(NQ % TS == 0, "time split must divide NQ");
   static_assert(!DMMA || NQ == 4, "DMMA axis-2 path needs i2 in lane bits 0-1");
+  static_assert(!A1S || (DMMA && TS == 1 && DBUF), "A1S runs in the double-buffered DMMA slice loop");
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -235,6 +238,11 @@ sweep_kernel_v2(const SweepParams P) {
     const int g = lane >> 2, t4 = lane & 3;      // B[k=t4][n=g]: n even -> diff[n/2][k]
     bfrag = (g & 1) ? 0.0 : P.ops.diff[g >> 1][t4];
   }
+  // A1S: lane sigma(L) swaps lane bits 0-1 (i2) with bits 2-3 (i1).  The DMMA
+  // A operand taken from lane sigma(L) has the i1 line in k; the product lands
+  // in lane sigma(owner), so one shuffle in and one out replace the axis-1
+  // shared-memory gather.
+  const int sig = (tid & 16) | ((tid & 3) << 2) | ((tid >> 2) & 3);
   // padded gather bases for the shared-memory axes
   int gbase[DIM], gstr[DIM];
   gbase[0] = px - i0 * P0; gstr[0] = P0;
@@ -491,6 +499,15 @@ sweep_kernel_v2(const SweepParams P) {
           for (int c = 0; c < M; ++c)
             sFs[(a * M + c) * PS + ((S::F1T && a == 1) ? p1t : px)] = F[a][c];
       }
+      double d1t[M];                             // A1S: axis-1 derivative, transposed lane
+      if (S::A1S) {
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          const double a1 = __shfl_sync(0xffffffffu, F[1][c], sig);
+          double z1;
+          dmma_8x8x4(d1t[c], z1, a1, bfrag, 0.0, 0.0);
+        }
+      }
       if (TS == 1 && S::DBUF && s > 0) {
         // time contraction of the previous slice, deferred past its DMMA latency
 #pragma unroll
@@ -525,6 +542,7 @@ sweep_kernel_v2(const SweepParams P) {
         double sum = part[0];
 #pragma unroll
         for (int a = 1; a < DS; ++a) sum += part[a];
+        if (S::A1S) sum += __shfl_sync(0xffffffffu, d1t[c], sig);
         dv[c] = sum;
       }
       if (DMMA) {
