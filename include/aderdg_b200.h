@@ -159,6 +159,15 @@ adg_status adg_phase_seed_finish(adg_handle* h);
 adg_status adg_phase_rerun(adg_handle* h);     /* device-conditional rerun predict  */
 adg_status adg_phase_sweep(adg_handle* h);     /* priming on the first call          */
 adg_status adg_phase_finish(adg_handle* h);    /* time control + step record         */
+/* Overlapped slab step (the paper's transfer hiding):
+ * rerun -> { halo exchange  ||  sweep_part(INTERIOR) } -> sweep_part(BOUNDARY)
+ * -> all-reduce -> finish.  Interior planes (1..P-2) read no halo slot and
+ * write no record a neighbour receives, so they run while the exchange of the
+ * parity the sweep reads is in flight; the two boundary planes follow.  Both
+ * parts (or ALL) must be enqueued before adg_phase_finish; the priming sweep
+ * is ALL only.  The cells are independent, so split = whole sweep bitwise. */
+typedef enum { ADG_PART_ALL = 0, ADG_PART_INTERIOR = 1, ADG_PART_BOUNDARY = 2 } adg_sweep_part;
+adg_status adg_phase_sweep_part(adg_handle* h, int part);
 int        adg_trace_parity(const adg_handle* h); /* parity the next sweep reads      */
 
 /* Timing helpers for bench.py: launches on the handle's stream. */

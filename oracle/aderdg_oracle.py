@@ -349,7 +349,8 @@ class OracleKernels:
             with np.errstate(all="ignore"):
                 sm = np.max(self.pde.max_signal_speed(qm, a).reshape(C, -1), axis=1)
                 sp = np.max(self.pde.max_signal_speed(qp, a).reshape(C, -1), axis=1)
-            alpha = np.maximum(sm, sp)   # python max(a, b) == np.maximum for finite inputs
+            # python max(sm, sp): a NaN on the minus side wins, one on the plus side is ignored
+            alpha = np.where(np.isnan(sp), sm, np.maximum(sm, sp))
             al = alpha.reshape((-1,) + (1,) * (qp.ndim - 1))
             out.append(0.5 * (fm + fp) - 0.5 * al * (qp - qm))
         return out

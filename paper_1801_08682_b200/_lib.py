@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 ADG_OK, ADG_ERR_CONFIG, ADG_ERR_NUMERICAL, ADG_ERR_RUNTIME, ADG_ERR_PREDICTOR = 0, 2, 3, 4, 5
 ADG_BUF_Q, ADG_BUF_D, ADG_BUF_TRACE0, ADG_BUF_TRACE1, ADG_BUF_REDUCE = range(5)
+ADG_PART_ALL, ADG_PART_INTERIOR, ADG_PART_BOUNDARY = range(3)
 
 #: every symbol the header declares (checked by tests/test_abi.py)
 EXPORTS = (
@@ -29,7 +30,7 @@ EXPORTS = (
     "adg_last_error", "adg_layout_info", "adg_buffer", "adg_phase_seed",
     "adg_phase_seed_finish", "adg_phase_rerun", "adg_phase_sweep",
     "adg_phase_finish", "adg_trace_parity", "adg_flush_l2", "adg_reset", "adg_set_dt_new",
-    "adg_run_timed",
+    "adg_run_timed", "adg_phase_sweep_part",
 )
 
 
@@ -108,6 +109,7 @@ def load_library(path=None):
         "adg_phase_seed_finish": (ctypes.c_int, [H]),
         "adg_phase_rerun": (ctypes.c_int, [H]),
         "adg_phase_sweep": (ctypes.c_int, [H]),
+        "adg_phase_sweep_part": (ctypes.c_int, [H, ctypes.c_int]),
         "adg_phase_finish": (ctypes.c_int, [H]),
         "adg_trace_parity": (ctypes.c_int, [H]),
         "adg_flush_l2": (ctypes.c_int, [H]),

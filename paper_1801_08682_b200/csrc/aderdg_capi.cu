@@ -10,6 +10,7 @@
 #include <stdio.h>
 #include <string.h>
 #include <math.h>
+#include <limits.h>
 #include <stdlib.h>
 #include <string>
 #include <vector>
@@ -249,6 +250,9 @@ static SweepParams sweep_params(adg_handle* h, int mode) {
   P.plane_cells = h->plane_cells;
   P.cell_offset = (int)(h->plane0 * (long long)h->plane_cells);
   P.halo = (h->cfg.world > 1 || h->cfg.halo_mode == 1) ? 1 : 0;
+  P.cell_a = 0;
+  P.blk_split = INT_MAX;
+  P.cell_jump = 0;
   P.spike_step = h->cfg.spike_step;
   P.p = h->cfg.p;
   P.h = h->h;
@@ -277,9 +281,29 @@ static FinishParams finish_params(adg_handle* h, int priming, int seed) {
   return F;
 }
 
-static adg_status launch(adg_handle* h, int mode) {
+// part: ADG_PART_ALL = every local cell; ADG_PART_INTERIOR = slab planes
+// 1..P-2 (read no halo slot, write no record a neighbour needs);
+// ADG_PART_BOUNDARY = planes 0 and P-1 (the halo readers / record producers).
+static adg_status launch(adg_handle* h, int mode, int part = ADG_PART_ALL) {
   SweepParams P = sweep_params(h, mode);
-  h->disp.sweep(P, (unsigned)h->cells_local, h->stream);
+  const int Pl = h->planes_local, pc = h->plane_cells;
+  unsigned blocks = (unsigned)h->cells_local;
+  if (part == ADG_PART_INTERIOR) {
+    if (Pl <= 2) return ADG_OK;                       // no interior plane
+    P.cell_a = pc;
+    blocks = (unsigned)((Pl - 2) * (long long)pc);
+  } else if (part == ADG_PART_BOUNDARY) {
+    if (Pl >= 2) {
+      P.blk_split = pc;
+      P.cell_jump = (Pl - 2) * pc;                    // block pc -> first cell of plane P-1
+      blocks = (unsigned)(2 * pc);
+    } else {
+      blocks = (unsigned)pc;
+    }
+  } else if (part != ADG_PART_ALL) {
+    return fail(h, ADG_ERR_CONFIG, "unknown sweep part");
+  }
+  h->disp.sweep(P, blocks, h->stream);
   return cuda_check(h, cudaGetLastError(), "sweep launch");
 }
 
@@ -505,13 +529,16 @@ adg_status adg_phase_rerun(adg_handle* h) {
   return launch(h, MODE_RERUN);
 }
 
-adg_status adg_phase_sweep(adg_handle* h) {
+adg_status adg_phase_sweep_part(adg_handle* h, int part) {
   if (!h) return ADG_ERR_CONFIG;
   if (!h->seeded) return fail(h, ADG_ERR_CONFIG, "time control not seeded");
-  if (straightforward(h)) return launch(h, MODE_SF_CORRECT);
-  adg_status s = launch(h, h->sweep_index == 0 ? MODE_PRIMING : MODE_NORMAL);
-  return s;
+  if (straightforward(h)) return launch(h, MODE_SF_CORRECT, part);
+  if (h->sweep_index == 0 && part != ADG_PART_ALL)
+    return fail(h, ADG_ERR_CONFIG, "the priming sweep is not split");
+  return launch(h, h->sweep_index == 0 ? MODE_PRIMING : MODE_NORMAL, part);
 }
+
+adg_status adg_phase_sweep(adg_handle* h) { return adg_phase_sweep_part(h, ADG_PART_ALL); }
 
 adg_status adg_phase_finish(adg_handle* h) {
   if (!h) return ADG_ERR_CONFIG;
@@ -520,7 +547,10 @@ adg_status adg_phase_finish(adg_handle* h) {
   return s;
 }
 
-int adg_trace_parity(const adg_handle* h) { return h ? (h->sweep_index & 1) : 0; }
+int adg_trace_parity(const adg_handle* h) {
+  if (!h) return 0;
+  return straightforward(h) ? 0 : (h->sweep_index & 1);   // SF passes share parity 0
+}
 
 static adg_status enqueue_step(adg_handle* h) {
   adg_status s;

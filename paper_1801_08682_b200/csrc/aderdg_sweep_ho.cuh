@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
   if (mode_corrects(mode) && st->reduce[1] != 0) return;   // a predict pass already failed
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const long long cell = blockIdx.x;
+  const long long cell = sweep_cell(P);
   const long long gcell = cell + P.cell_offset;
   const int plane = (int)(cell / P.plane_cells);
   const int rest = (int)(cell % P.plane_cells);
@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
       const double* nb = P.tr_in + ((long long)(f ^ 1) * P.slots + nb_slot[f]) * REC;
       const double* mr = (f & 1) ? own : nb;
       const double* pr = (f & 1) ? nb : own;
-      const double alpha = fmax(mr[2 * NF * M], pr[2 * NF * M]);
+      const double alpha = rusanov_alpha(mr[2 * NF * M], pr[2 * NF * M]);
       const double fs = __dsub_rn(__dmul_rn(0.5, __dadd_rn(mr[NF * M + yc], pr[NF * M + yc])),
                                   __dmul_rn(__dmul_rn(0.5, alpha), __dsub_rn(pr[yc], mr[yc])));
       sFace[e] = (f & 1) ? fs : -fs;

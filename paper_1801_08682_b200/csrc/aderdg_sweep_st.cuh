@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(256, 3) sweep_kernel_st(const SweepParams P) {
   const int i2 = 2 * (warp & 1) + ((lane >> 4) & 1);
   const int x = (i0 * NQ + i1) * NQ + i2;
   const bool lead = (t == 0);          // one lane per spatial node for the per-node work
-  const long long cell = blockIdx.x;
+  const long long cell = sweep_cell(P);
   const long long gcell = cell + P.cell_offset;
   const int plane = (int)(cell / P.plane_cells);
   const int rest = (int)(cell % P.plane_cells);
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(256, 3) sweep_kernel_st(const SweepParams P) {
       const double* nb = sRec + (2 * DIM + f) * REC;
       const double* mr = (f & 1) ? own : nb;
       const double* pr = (f & 1) ? nb : own;
-      const double alpha = fmax(mr[2 * NF * M], pr[2 * NF * M]);
+      const double alpha = rusanov_alpha(mr[2 * NF * M], pr[2 * NF * M]);
       const double fs = __dsub_rn(__dmul_rn(0.5, __dadd_rn(mr[NF * M + yc], pr[NF * M + yc])),
                                   __dmul_rn(__dmul_rn(0.5, alpha), __dsub_rn(pr[yc], mr[yc])));
       sFace[e] = (f & 1) ? fs : -fs;

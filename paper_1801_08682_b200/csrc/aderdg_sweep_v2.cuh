@@ -177,7 +177,7 @@ sweep_kernel_v2(const SweepParams P) {
   const int x0 = tid % NSP;
   const bool act = x0 < NS;
   const int x = act ? x0 : 0;
-  const long long cell = blockIdx.x;
+  const long long cell = sweep_cell(P);
   const long long gcell = cell + P.cell_offset;
   const int i0 = x / (NQ * NQ), i1 = (x / NQ) % NQ, i2 = x % NQ;
   const int px = i0 * P0 + i1 * NQ + i2;              // padded slice index
@@ -268,7 +268,7 @@ sweep_kernel_v2(const SweepParams P) {
       const double* nb = sRec + (2 * DIM + f) * REC;
       const double* mr = (f & 1) ? own : nb;
       const double* pr = (f & 1) ? nb : own;
-      const double alpha = fmax(mr[2 * NF * M], pr[2 * NF * M]);
+      const double alpha = rusanov_alpha(mr[2 * NF * M], pr[2 * NF * M]);
       const double fs = __dsub_rn(__dmul_rn(0.5, __dadd_rn(mr[NF * M + yc], pr[NF * M + yc])),
                                   __dmul_rn(__dmul_rn(0.5, alpha), __dsub_rn(pr[yc], mr[yc])));
       sFace[e] = (f & 1) ? fs : -fs;

@@ -7,9 +7,13 @@ two ring neighbours once per realisation step, boundary Riemann problems
 solved redundantly on both sides, and one global reduction of the admissible
 step (here: max of lambda, which gives dt_adm bitwise).
 
-Per step and rank:  rerun (device-conditional)  ->  halo exchange of the
-trace parity the sweep will read  ->  fused sweep  ->  all-reduce MAX of
-{lambda bits, INT64_MAX - error key}  ->  time control.
+Per step and rank:  rerun (device-conditional)  ->  { halo exchange of the
+trace parity the sweep will read  ||  sweep of the interior planes }  ->
+sweep of the two boundary planes  ->  all-reduce MAX of {lambda bits,
+INT64_MAX - error key}  ->  time control.  The exchange runs on NCCL's stream
+while the interior planes (which read no halo slot and produce no record a
+neighbour receives) run on the compute stream: the paper's transfer hiding
+(``PAPER.md:1591-1597``).
 
 Layout of the trace records (``include/aderdg_b200.h``): ``[2d faces][slots][REC]``
 with ``slots = (planes_local + 2) * plane_cells``; slot plane 0 and
@@ -60,9 +64,20 @@ class HaloExchange:
         return send_prev, recv_prev, send_next, recv_next
 
     def exchange(self, tr):
+        self.wait(self.start(tr))
+
+    def active(self):
+        return self.world > 1 or self.force
+
+    def start(self, tr):
+        """Issue the ring exchange of ``tr``'s boundary records and return the
+        pending works.  With NCCL the transfers run on NCCL's stream, ordered
+        after the work already queued on the current stream; the caller keeps
+        queueing independent kernels (the interior planes) and calls wait()
+        before the halo readers.  The gloo-staged transport completes here."""
         import torch.distributed as dist
-        if self.world == 1 and not self.force:
-            return
+        if not self.active():
+            return []
         send_prev, recv_prev, send_next, recv_next = self.views(tr)
         if self.staged:
             dev_recv = (recv_prev, recv_next)
@@ -74,11 +89,20 @@ class HaloExchange:
                dist.P2POp(dist.irecv, recv_prev, self.prev, self.group),
                dist.P2POp(dist.isend, send_prev, self.prev, self.group),
                dist.P2POp(dist.irecv, recv_next, self.next, self.group)]
-        for r in dist.batch_isend_irecv(ops):
-            r.wait()
+        works = dist.batch_isend_irecv(ops)
         if self.staged:
+            for r in works:
+                r.wait()
             dev_recv[0].copy_(recv_prev)
             dev_recv[1].copy_(recv_next)
+            return []
+        return works
+
+    @staticmethod
+    def wait(works):
+        """NCCL: the current stream waits for the transfers (no host block)."""
+        for r in works:
+            r.wait()
 
     def reduce(self, red):
         """red: int64[2] = {lambda bits, INT64_MAX - error key}; MAX over ranks."""
@@ -104,7 +128,7 @@ class SlabDriver:
     def __init__(self, Q_global, d, L, p, rank, world, device, cfl=0.9, c_dt=0.99,
                  averaging="strict", forced_dt=None, inject_rerun=False,
                  spike_step=None, spike_factor=3.0, group=None, staged=False, halo_mode=0,
-                 mode="fused"):
+                 mode="fused", overlap=True):
         import torch
         from .basis import make_basis
         from .solver import upload_operators
@@ -124,6 +148,7 @@ class SlabDriver:
         cfg.halo_mode = int(halo_mode)
         cfg.driver_mode = 1 if mode == "straightforward" else 0
         self.mode = mode
+        self.overlap = bool(overlap)
         self.handle = _lib.Handle(cfg)
         self._ops = upload_operators(self.handle, make_basis(p))
         self.lay = lay = self.handle.layout()
@@ -170,8 +195,16 @@ class SlabDriver:
             h.call("adg_phase_finish")
             self.primed = True
         h.call("adg_phase_rerun")
-        self.halo.exchange(self.tr[h.lib.adg_trace_parity(h.h)])
-        h.call("adg_phase_sweep")
+        tr = self.tr[h.lib.adg_trace_parity(h.h)]
+        if self.overlap and self.halo.active():
+            # the interior planes hide the face-record transfer
+            pending = self.halo.start(tr)
+            h.call("adg_phase_sweep_part", _lib.ADG_PART_INTERIOR)
+            self.halo.wait(pending)
+            h.call("adg_phase_sweep_part", _lib.ADG_PART_BOUNDARY)
+        else:
+            self.halo.exchange(tr)
+            h.call("adg_phase_sweep")
         self.halo.reduce(self.red)
         h.call("adg_phase_finish")
 

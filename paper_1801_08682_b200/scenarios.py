@@ -129,7 +129,23 @@ def gaussian_advect(d, L, p, noise=0.0, seed=0):
     return q[..., None]
 
 
+def shock_tube(d, L, p, seed=0, noise=0.0, pressure_ratio=10.0):
+    """Periodic two-shock tube along x_0 (the reference's Sod states,
+    ``src/cli.py`` "sod" / ``tests/test_limiter.py:104-109``, made periodic):
+    rho = 1, p = 1 for |x_0 - 0.5| < 0.25, else rho = 0.125, p = 1/ratio;
+    at rest, optional seeded U(-noise, noise) on the density.  Drives the
+    subcell limiter (troubled cells at both discontinuities)."""
+    x = node_coordinates(d, L, p)
+    inside = np.abs(x[..., 0] - 0.5) < 0.25
+    rho = np.where(inside, 1.0, 0.125)
+    if noise:
+        rho = rho + np.random.default_rng(seed).uniform(-noise, noise, size=rho.shape)
+    pr = np.where(inside, 1.0, 1.0 / pressure_ratio)
+    return conserved(rho, np.zeros(x.shape[:-1] + (d,)), pr)
+
+
 SCENARIOS = {
+    "shocktube": shock_tube,
     "bump": gaussian_bump_noise,
     "fourier": random_fourier,
     "wave": smooth_density_wave,

@@ -23,7 +23,7 @@ def _port():
     return p
 
 
-def _run(port, out, inject):
+def _run(port, out, inject, overlap, mode):
     import torch.distributed as dist
     from paper_1801_08682_b200 import scenarios
     from paper_1801_08682_b200.parallel import SlabDriver
@@ -32,10 +32,11 @@ def _run(port, out, inject):
     torch.cuda.set_device(0)
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     Q0 = scenarios.build("bump", 3, 2, 3, seed=5, noise=1e-2)
-    a = SlabDriver(Q0, 3, 2, 3, 0, 1, 0, inject_rerun=inject, halo_mode=1)
+    a = SlabDriver(Q0, 3, 2, 3, 0, 1, 0, inject_rerun=inject, halo_mode=1, overlap=overlap,
+                   mode=mode)
     a.run(4)
     qa = a.local_state()
-    b = SlabDriver(Q0, 3, 2, 3, 0, 1, 0, inject_rerun=inject)
+    b = SlabDriver(Q0, 3, 2, 3, 0, 1, 0, inject_rerun=inject, mode=mode)
     b.run(4)
     qb = b.local_state()
     np.save(out, np.stack([qa, qb]))
@@ -44,11 +45,13 @@ def _run(port, out, inject):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("inject", [False, True])
-def test_nccl_self_halo_equals_periodic(cuda_ok, tmp_path, inject):
+@pytest.mark.parametrize("inject,overlap,mode", [(False, False, "fused"), (True, False, "fused"),
+                                                 (False, True, "fused"), (True, True, "fused"),
+                                                 (False, True, "straightforward")])
+def test_nccl_self_halo_equals_periodic(cuda_ok, tmp_path, inject, overlap, mode):
     ctx = mp.get_context("spawn")
     out = str(tmp_path / "q.npy")
-    p = ctx.Process(target=_run, args=(_port(), out, inject))
+    p = ctx.Process(target=_run, args=(_port(), out, inject, overlap, mode))
     p.start()
     p.join(timeout=300)
     assert p.exitcode == 0

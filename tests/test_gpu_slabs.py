@@ -74,9 +74,10 @@ def single(d, L, p, steps, **kw):
     return out
 
 
+@pytest.mark.parametrize("overlap", [True, False])
 @pytest.mark.parametrize("world,d,L,p,steps", [(2, 3, 2, 3, 4), (3, 3, 2, 5, 3), (2, 2, 3, 3, 6)])
-def test_slabs_equal_single_gpu_bitwise(cuda_ok, tmp_path, world, d, L, p, steps):
-    Q, tcs, errs = run_slabs(world, d, L, p, steps, tmp_path)
+def test_slabs_equal_single_gpu_bitwise(cuda_ok, tmp_path, world, d, L, p, steps, overlap):
+    Q, tcs, errs = run_slabs(world, d, L, p, steps, tmp_path, overlap=overlap)
     assert errs == [""] * world
     Q1, tc1 = single(d, L, p, steps)
     assert np.array_equal(Q, Q1)
@@ -88,4 +89,25 @@ def test_slabs_inject_rerun(cuda_ok, tmp_path):
     Q, tcs, errs = run_slabs(2, 3, 2, 3, 3, tmp_path, inject_rerun=True)
     Q1, tc1 = single(3, 2, 3, 3, inject_rerun=True)
     assert errs == ["", ""]
+    assert np.array_equal(Q, Q1)
+
+
+@pytest.mark.parametrize("world,L", [(2, 1), (3, 1)])
+def test_slabs_of_one_and_two_planes(cuda_ok, tmp_path, world, L):
+    """Slabs without interior planes (P = 1, 2): the overlapped step is the
+    boundary pass alone."""
+    Q, tcs, errs = run_slabs(world, 3, L, 3, 4, tmp_path)
+    assert errs == [""] * world
+    Q1, tc1 = single(3, L, 3, 4)
+    assert np.array_equal(Q, Q1)
+    for tc in tcs:
+        assert np.array_equal(tc, tc1)
+
+
+def test_slabs_straightforward_overlapped(cuda_ok, tmp_path):
+    """Straightforward driver over slabs: predict pass -> {exchange || interior
+    corrector} -> boundary corrector."""
+    Q, tcs, errs = run_slabs(3, 3, 2, 3, 4, tmp_path, mode="straightforward")
+    assert errs == [""] * 3
+    Q1, tc1 = single(3, 2, 3, 4, mode="straightforward")
     assert np.array_equal(Q, Q1)
