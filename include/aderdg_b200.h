@@ -56,7 +56,8 @@ typedef enum {
   ADG_EK_NO_INITIAL_STEP = 2,   /* "no admissible initial step (got {adm})"  scheduler.py:153-154 */
   ADG_EK_INADMISSIBLE = 3,      /* "inadmissible state in cell {c} at step {s}" scheduler.py:429-432 */
   ADG_EK_PREDICTOR = 4,         /* PredictorFailureError(c)                   kernels.py:80-100 */
-  ADG_EK_DEGENERATE = 5         /* "admissible step degenerated to {dt_adm}"  scheduler.py:81-82 */
+  ADG_EK_DEGENERATE = 5,        /* "admissible step degenerated to {dt_adm}"  scheduler.py:81-82 */
+  ADG_EK_SUBCELL = 6            /* "subcell update left cell {c} inadmissible" limiter.py:214-216 */
 } adg_error_kind;
 
 typedef struct {
@@ -91,6 +92,8 @@ typedef struct {
   double dt_adm;
   long long picard_iters;  /* Picard iterations summed over all predicts of the step */
   long long predicts;      /* number of cell predictions in the step        */
+  long long troubled;      /* cells handed to the subcell limiter (Driver.troubled_by_step,
+                              scheduler.py:301-305); 0 without limiter      */
 } adg_step_record;
 
 typedef struct adg_handle adg_handle;
@@ -148,6 +151,17 @@ adg_status adg_picard_histogram(const adg_handle* h, long long* hist, int n_bins
 adg_status adg_error_info(const adg_handle* h, int* kind, long long* cell, int* step, double* value);
 const char* adg_last_error(const adg_handle* h);
 adg_status adg_layout_info(const adg_handle* h, adg_layout* out);
+
+/* SubcellLimiter(system, basis, grid, cfl) attached to a straightforward driver
+ * (limiter.py:87-108, scheduler.py:100-102,239-309), one slab.  P [ns][n] =
+ * subcell_average_matrix(basis), R [n][ns] = solve(P^T P, P^T), nearest [ns] =
+ * node nearest to each subcell centre, sample [n] = min(int(nodes*ns), ns-1),
+ * ns = 2p+1; traversal = the driver's cell order (NULL = lexicographic), which
+ * fixes whose prev_Q the DMP test sees.  Call before the first step. */
+adg_status adg_set_limiter(adg_handle* h, const double* P, const double* R, const int* nearest,
+                           const int* sample, const long long* traversal, double cfl);
+/* Cell.troubled of every local cell (mesh.py:39). */
+adg_status adg_troubled_flags(adg_handle* h, unsigned char* out, size_t n);
 adg_status adg_buffer(adg_handle* h, int which, void** dev_ptr, size_t* bytes);
 
 /* Phase API (one process per GPU; the host drives NCCL between phases).

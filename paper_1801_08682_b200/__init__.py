@@ -12,7 +12,8 @@ from .basis import Basis1D, make_basis
 from .errors import (ConfigurationError, DeviceError, DomainError, NumericalError,
                      PredictorFailureError, ResourceBudgetError, SchedulingOrderError)
 from .solver import (AdvectionSystem, Driver, EulerSystem, Grid, Kernels, TimeControl, build_grid,
-                     device_bytes, gather)
+                     device_bytes, gather, traversal_order)
+from .limiter import SubcellLimiter, subcell_average_matrix
 
 __version__ = "0.1.0"
 
@@ -20,5 +21,6 @@ __all__ = [
     "Basis1D", "ConfigurationError", "DeviceError", "DomainError", "Driver",
     "AdvectionSystem", "EulerSystem", "Grid", "Kernels", "NumericalError", "PredictorFailureError",
     "ResourceBudgetError", "SchedulingOrderError", "TimeControl", "build_grid",
-    "device_bytes", "gather", "make_basis",
+    "device_bytes", "gather", "make_basis", "SubcellLimiter", "subcell_average_matrix",
+    "traversal_order",
 ]

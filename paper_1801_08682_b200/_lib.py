@@ -30,7 +30,7 @@ EXPORTS = (
     "adg_last_error", "adg_layout_info", "adg_buffer", "adg_phase_seed",
     "adg_phase_seed_finish", "adg_phase_rerun", "adg_phase_sweep",
     "adg_phase_finish", "adg_trace_parity", "adg_flush_l2", "adg_reset", "adg_set_dt_new",
-    "adg_run_timed", "adg_phase_sweep_part",
+    "adg_run_timed", "adg_phase_sweep_part", "adg_set_limiter", "adg_troubled_flags",
 )
 
 
@@ -53,6 +53,7 @@ class AdgStepRecord(ctypes.Structure):
         ("T", ctypes.c_double), ("dt_old", ctypes.c_double),
         ("dt_new", ctypes.c_double), ("dt_adm", ctypes.c_double),
         ("picard_iters", ctypes.c_longlong), ("predicts", ctypes.c_longlong),
+        ("troubled", ctypes.c_longlong),
     ]
 
 
@@ -110,6 +111,10 @@ def load_library(path=None):
         "adg_phase_rerun": (ctypes.c_int, [H]),
         "adg_phase_sweep": (ctypes.c_int, [H]),
         "adg_phase_sweep_part": (ctypes.c_int, [H, ctypes.c_int]),
+        "adg_set_limiter": (ctypes.c_int, [H, dp, dp, ctypes.POINTER(ctypes.c_int),
+                                           ctypes.POINTER(ctypes.c_int),
+                                           ctypes.POINTER(ctypes.c_longlong), ctypes.c_double]),
+        "adg_troubled_flags": (ctypes.c_int, [H, ctypes.POINTER(ctypes.c_ubyte), ctypes.c_size_t]),
         "adg_phase_finish": (ctypes.c_int, [H]),
         "adg_trace_parity": (ctypes.c_int, [H]),
         "adg_flush_l2": (ctypes.c_int, [H]),

@@ -20,6 +20,7 @@
 #include "aderdg_sweep_v2.cuh"
 #include "aderdg_sweep_ho.cuh"
 #include "aderdg_sweep_st.cuh"
+#include "aderdg_limiter.cuh"
 
 using namespace adg;
 
@@ -126,6 +127,68 @@ Dispatch make_dispatch_v2() {
 }
 
 
+// subcell limiter kernels (aderdg_limiter.cuh), per PDE plug-in and dimension
+struct LimDispatch {
+  void (*detect)(const LimParams&, unsigned, size_t, cudaStream_t);
+  void (*apply)(const LimParams&, unsigned, cudaStream_t);
+};
+
+template <class PDE, int DIM>
+void launch_lim_detect(const LimParams& L, unsigned grid, size_t smem, cudaStream_t s) {
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(lim_detect_kernel<PDE, DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
+  lim_detect_kernel<PDE, DIM><<<grid, 256, smem, s>>>(L);
+}
+
+template <class PDE, int DIM>
+void launch_lim_apply(const LimParams& L, unsigned grid, cudaStream_t s) {
+  lim_apply_kernel<PDE, DIM><<<grid, 256, 0, s>>>(L);
+}
+
+template <class PDE, int DIM>
+LimDispatch make_lim_dispatch() { return LimDispatch{&launch_lim_detect<PDE, DIM>, &launch_lim_apply<PDE, DIM>}; }
+
+LimDispatch lim_dispatch_for(int d, int system) {
+  if (system == 1) return d == 2 ? make_lim_dispatch<AdvectionPDE<2>, 2>() : make_lim_dispatch<AdvectionPDE<3>, 3>();
+  return d == 2 ? make_lim_dispatch<EulerPDE<2>, 2>() : make_lim_dispatch<EulerPDE<3>, 3>();
+}
+
+// the generic kernel (the one with the limiter hooks) for every Euler (d, p)
+bool dispatch_generic(int d, int p, Dispatch* out) {
+  const int n = p + 1;
+  if (d == 2) {
+    switch (n) {
+      case 1: *out = make_dispatch<2, 1>(); return true;
+      case 2: *out = make_dispatch<2, 2>(); return true;
+      case 3: *out = make_dispatch<2, 3>(); return true;
+      case 4: *out = make_dispatch<2, 4>(); return true;
+      case 5: *out = make_dispatch<2, 5>(); return true;
+      case 6: *out = make_dispatch<2, 6>(); return true;
+      case 7: *out = make_dispatch<2, 7>(); return true;
+      case 8: *out = make_dispatch<2, 8>(); return true;
+      case 9: *out = make_dispatch<2, 9>(); return true;
+      case 10: *out = make_dispatch<2, 10>(); return true;
+    }
+  } else if (d == 3) {
+    switch (n) {
+      case 1: *out = make_dispatch<3, 1>(); return true;
+      case 2: *out = make_dispatch<3, 2>(); return true;
+      case 3: *out = make_dispatch<3, 3>(); return true;
+      case 4: *out = make_dispatch<3, 4>(); return true;
+      case 5: *out = make_dispatch<3, 5>(); return true;
+      case 6: *out = make_dispatch<3, 6>(); return true;
+      case 7: *out = make_dispatch<3, 7>(); return true;
+      case 8: *out = make_dispatch<3, 8>(); return true;
+      case 9: *out = make_dispatch<3, 9>(); return true;
+      case 10: *out = make_dispatch<3, 10>(); return true;
+    }
+  }
+  return false;
+}
+
 bool dispatch_for(int d, int p, int system, Dispatch* out) {
   const int n = p + 1;
   if (system == 1) return d == 2 ? dispatch_adv<2>(n, out) : d == 3 ? dispatch_adv<3>(n, out) : false;
@@ -202,6 +265,24 @@ struct adg_handle {
   int host_steps = 0;        // steps whose records were fetched
   DevState hst;              // host mirror after the last sync
   std::string err;
+  // subcell limiter (adg_set_limiter; straightforward mode, one slab)
+  bool lim = false;
+  LimDispatch ldisp;
+  int lim_ns = 0;
+  double* lim_P = nullptr;
+  double* lim_R = nullptr;
+  int* lim_nearest = nullptr;
+  int* lim_sample = nullptr;
+  int* lim_rank = nullptr;
+  double* lim_prev[2] = {nullptr, nullptr};
+  unsigned char* lim_troubled = nullptr;
+  int* lim_list = nullptr;
+  double* lim_lam = nullptr;
+  double* lim_scratch = nullptr;
+  long long lim_scratch_cta = 0;
+  unsigned lim_grid = 0;
+  size_t lim_detect_smem = 0;
+  double lim_cfl = 0.9;
 };
 
 static adg_status fail(adg_handle* h, adg_status code, const std::string& msg) {
@@ -253,6 +334,10 @@ static SweepParams sweep_params(adg_handle* h, int mode) {
   P.cell_a = 0;
   P.blk_split = INT_MAX;
   P.cell_jump = 0;
+  // limiter hooks: the corrector of step s snapshots prev_Q into lim_prev[s & 1]
+  P.lim_troubled = h->lim ? h->lim_troubled : nullptr;
+  P.lim_cur = h->lim ? h->lim_prev[h->sweep_index & 1] : nullptr;
+  P.lim_lam = h->lim ? h->lim_lam : nullptr;
   P.spike_step = h->cfg.spike_step;
   P.p = h->cfg.p;
   P.h = h->h;
@@ -307,6 +392,41 @@ static adg_status launch(adg_handle* h, int mode, int part = ADG_PART_ALL) {
   return cuda_check(h, cudaGetLastError(), "sweep launch");
 }
 
+// subcell limiter pass after the straightforward corrector (scheduler.py:282-309):
+// detect (one CTA per cell) -> apply (persistent CTAs over the troubled list)
+// -> max lambda.  prev_Q of this step is lim_prev[sweep_index & 1].
+static adg_status launch_limiter(adg_handle* h) {
+  LimParams L;
+  L.sp = sweep_params(h, MODE_SF_CORRECT);
+  L.P = h->lim_P;
+  L.R = h->lim_R;
+  L.nearest = h->lim_nearest;
+  L.sample = h->lim_sample;
+  L.rank = h->lim_rank;
+  L.Q = h->Q;
+  L.cur = h->lim_prev[h->sweep_index & 1];
+  L.old = h->lim_prev[(h->sweep_index & 1) ^ 1];
+  L.troubled = h->lim_troubled;
+  L.list = h->lim_list;
+  L.lam = h->lim_lam;
+  L.scratch = h->lim_scratch;
+  L.scratch_cta = h->lim_scratch_cta;
+  L.st = h->st;
+  L.n = h->n;
+  L.ns = h->lim_ns;
+  L.K = h->K;
+  L.n_cells = (int)h->cells_local;
+  L.h_sub = h->h / (double)h->lim_ns;          // limiter.py:96  grid.h / ns
+  L.cfl = h->lim_cfl;
+  h->ldisp.detect(L, (unsigned)h->cells_local, h->lim_detect_smem, h->stream);
+  adg_status s = cuda_check(h, cudaGetLastError(), "limiter detect launch");
+  if (s != ADG_OK) return s;
+  h->ldisp.apply(L, h->lim_grid, h->stream);
+  if ((s = cuda_check(h, cudaGetLastError(), "limiter apply launch")) != ADG_OK) return s;
+  lim_lambda_kernel<<<148, 256, 0, h->stream>>>(h->lim_lam, (int)h->cells_local, h->st);
+  return cuda_check(h, cudaGetLastError(), "limiter lambda launch");
+}
+
 static adg_status launch_finish(adg_handle* h, int priming, int seed) {
   FinishParams F = finish_params(h, priming, seed);
   finish_kernel<<<1, 1, 0, h->stream>>>(F);
@@ -338,6 +458,9 @@ static adg_status status_from_state(adg_handle* h) {
       return fail(h, ADG_ERR_PREDICTOR, buf);
     case ADG_EK_DEGENERATE:
       snprintf(buf, sizeof buf, "admissible step degenerated to %.17g", s.err_value);
+      return fail(h, ADG_ERR_NUMERICAL, buf);
+    case ADG_EK_SUBCELL:
+      snprintf(buf, sizeof buf, "subcell update left cell %lld inadmissible", s.err_cell);
       return fail(h, ADG_ERR_NUMERICAL, buf);
   }
   return fail(h, ADG_ERR_RUNTIME, "unknown device status");
@@ -417,6 +540,10 @@ void adg_destroy(adg_handle* h) {
   if (h->st) cudaFree(h->st);
   if (h->recs) cudaFree(h->recs);
   if (h->flush) cudaFree(h->flush);
+  void* lim_bufs[] = {h->lim_P, h->lim_R, h->lim_nearest, h->lim_sample, h->lim_rank, h->lim_prev[0],
+                      h->lim_prev[1], h->lim_troubled, h->lim_list, h->lim_lam, h->lim_scratch};
+  for (void* b : lim_bufs)
+    if (b) cudaFree(b);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   delete h;
 }
@@ -459,6 +586,11 @@ adg_status adg_reset(adg_handle* h) {
   CUDA_TRY(h, cudaMemsetAsync(h->D, 0, state_bytes, h->stream));
   CUDA_TRY(h, cudaMemsetAsync(h->tr[0], 0, tr_bytes, h->stream));
   CUDA_TRY(h, cudaMemsetAsync(h->tr[1], 0, tr_bytes, h->stream));
+  if (h->lim) {
+    CUDA_TRY(h, cudaMemsetAsync(h->lim_prev[0], 0, state_bytes, h->stream));   // mesh.py:90-96
+    CUDA_TRY(h, cudaMemsetAsync(h->lim_prev[1], 0, state_bytes, h->stream));
+    CUDA_TRY(h, cudaMemsetAsync(h->lim_troubled, 0, (size_t)h->cells_local, h->stream));
+  }
   DevState s0;
   memset(&s0, 0, sizeof s0);
   s0.dt_adm = INFINITY;
@@ -532,7 +664,11 @@ adg_status adg_phase_rerun(adg_handle* h) {
 adg_status adg_phase_sweep_part(adg_handle* h, int part) {
   if (!h) return ADG_ERR_CONFIG;
   if (!h->seeded) return fail(h, ADG_ERR_CONFIG, "time control not seeded");
-  if (straightforward(h)) return launch(h, MODE_SF_CORRECT, part);
+  if (straightforward(h)) {
+    adg_status s = launch(h, MODE_SF_CORRECT, part);
+    if (s != ADG_OK || !h->lim) return s;
+    return launch_limiter(h);
+  }
   if (h->sweep_index == 0 && part != ADG_PART_ALL)
     return fail(h, ADG_ERR_CONFIG, "the priming sweep is not split");
   return launch(h, h->sweep_index == 0 ? MODE_PRIMING : MODE_NORMAL, part);
@@ -573,6 +709,7 @@ static adg_status fetch_records(adg_handle* h, int from_step, int to_step, adg_s
     adg_step_record& o = out[s - from_step - 1];
     o.step = r.step; o.reruns = r.reruns; o.T = r.T; o.dt_old = r.dt_old;
     o.dt_new = r.dt_new; o.dt_adm = r.dt_adm; o.picard_iters = r.picard_iters; o.predicts = r.predicts;
+    o.troubled = r.troubled;
   }
   return ADG_OK;
 }
@@ -681,6 +818,88 @@ adg_status adg_error_info(const adg_handle* h, int* kind, long long* cell, int* 
 }
 
 const char* adg_last_error(const adg_handle* h) { return h ? h->err.c_str() : "null handle"; }
+
+adg_status adg_set_limiter(adg_handle* h, const double* P, const double* R, const int* nearest,
+                           const int* sample, const long long* traversal, double cfl) {
+  if (!h || !P || !R || !nearest || !sample) return ADG_ERR_CONFIG;
+  if (h->cfg.driver_mode != 1)                     // scheduler.py:100-102
+    return fail(h, ADG_ERR_CONFIG, "subcell limiting is supported in straightforward mode only");
+  if (h->cfg.world != 1 || h->cfg.halo_mode != 0)
+    return fail(h, ADG_ERR_CONFIG, "the subcell limiter runs on a single slab (world = 1)");
+  if (h->lim) return fail(h, ADG_ERR_CONFIG, "limiter already attached");
+  if (h->sweep_index != 0) return fail(h, ADG_ERR_CONFIG, "attach the limiter before the first step");
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  const int d = h->cfg.d, n = h->n, m = h->m, ns = 2 * h->cfg.p + 1;
+  long long nsub = 1;
+  for (int a = 0; a < d; ++a) nsub *= ns;
+  const long long nlay = nsub / ns;
+  if (h->cfg.system == 0 && !dispatch_generic(d, h->cfg.p, &h->disp))
+    return fail(h, ADG_ERR_CONFIG, "no generic kernel for this order");
+  h->ldisp = lim_dispatch_for(d, h->cfg.system);
+  h->lim_ns = ns;
+  h->lim_cfl = cfl;
+  const long long cells = h->cells_local;
+  const size_t state_bytes = sizeof(double) * (size_t)cells * h->NS * m;
+  CUDA_TRY(h, cudaMalloc(&h->lim_P, sizeof(double) * ns * n));
+  CUDA_TRY(h, cudaMalloc(&h->lim_R, sizeof(double) * n * ns));
+  CUDA_TRY(h, cudaMalloc(&h->lim_nearest, sizeof(int) * ns));
+  CUDA_TRY(h, cudaMalloc(&h->lim_sample, sizeof(int) * n));
+  CUDA_TRY(h, cudaMalloc(&h->lim_rank, sizeof(int) * cells));
+  CUDA_TRY(h, cudaMalloc(&h->lim_prev[0], state_bytes));
+  CUDA_TRY(h, cudaMalloc(&h->lim_prev[1], state_bytes));
+  CUDA_TRY(h, cudaMalloc(&h->lim_troubled, (size_t)cells));
+  CUDA_TRY(h, cudaMalloc(&h->lim_list, sizeof(int) * cells));
+  CUDA_TRY(h, cudaMalloc(&h->lim_lam, sizeof(double) * cells));
+  // apply scratch: 5 patches + the frozen halo per CTA; up to 2 CTAs per SM
+  h->lim_scratch_cta = LIM_SCRATCH_PATCHES * nsub * m + 2LL * d * nlay * m;
+  h->lim_grid = (unsigned)(cells < 296 ? cells : 296);
+  CUDA_TRY(h, cudaMalloc(&h->lim_scratch, sizeof(double) * (size_t)h->lim_scratch_cta * h->lim_grid));
+  // detection shared memory (aderdg_limiter.cuh lim_detect_kernel)
+  long long szA = ns, szB = (d == 3) ? (long long)ns * ns * n : (long long)n * n;
+  for (int a = 1; a < d; ++a) szA *= n;
+  szA *= m;
+  szB *= m;
+  const long long NM = (long long)h->NS * m;
+  h->lim_detect_smem = sizeof(double) * (size_t)(szA + (NM > szB ? NM : szB) + 2 * m * 8 + 4 * m);
+  if (h->lim_detect_smem > 227 * 1024) return fail(h, ADG_ERR_CONFIG, "limiter detection does not fit shared memory");
+  std::vector<int> rank(cells);
+  if (traversal) {
+    std::vector<char> seen(cells, 0);
+    for (long long i = 0; i < cells; ++i) {
+      const long long c = traversal[i];
+      if (c < 0 || c >= cells || seen[c]) return fail(h, ADG_ERR_CONFIG, "traversal must be a permutation of the cells");
+      seen[c] = 1;
+      rank[c] = (int)i;
+    }
+  } else {
+    for (long long i = 0; i < cells; ++i) rank[i] = (int)i;     // lexicographic (mesh.py:279-282)
+  }
+  CUDA_TRY(h, cudaMemcpyAsync(h->lim_P, P, sizeof(double) * ns * n, cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(h, cudaMemcpyAsync(h->lim_R, R, sizeof(double) * n * ns, cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(h, cudaMemcpyAsync(h->lim_nearest, nearest, sizeof(int) * ns, cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(h, cudaMemcpyAsync(h->lim_sample, sample, sizeof(int) * n, cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(h, cudaMemcpyAsync(h->lim_rank, rank.data(), sizeof(int) * cells, cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(h, cudaMemsetAsync(h->lim_prev[0], 0, state_bytes, h->stream));     // mesh.py:90-96
+  CUDA_TRY(h, cudaMemsetAsync(h->lim_prev[1], 0, state_bytes, h->stream));
+  CUDA_TRY(h, cudaMemsetAsync(h->lim_troubled, 0, (size_t)cells, h->stream));
+  CUDA_TRY(h, cudaMemsetAsync(h->lim_lam, 0, sizeof(double) * cells, h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  h->lim = true;
+  return ADG_OK;
+}
+
+adg_status adg_troubled_flags(adg_handle* h, unsigned char* out, size_t n) {
+  if (!h || !out) return ADG_ERR_CONFIG;
+  if (n != (size_t)h->cells_local) return fail(h, ADG_ERR_CONFIG, "troubled flag count mismatch");
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  if (!h->lim) {
+    memset(out, 0, n);
+    return ADG_OK;
+  }
+  CUDA_TRY(h, cudaMemcpyAsync(out, h->lim_troubled, n, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  return ADG_OK;
+}
 
 adg_status adg_layout_info(const adg_handle* h, adg_layout* o) {
   if (!h || !o) return ADG_ERR_CONFIG;

@@ -271,6 +271,36 @@ def upload_operators(handle, basis):
     return ops
 
 
+def _peano_order(d, L):
+    """Cells along the d-dimensional Peano curve of depth L (src/mesh.py:246-275):
+    base-3 digits of the curve parameter go round-robin to the axes, coarsest
+    first; a digit is mirrored when the digits seen so far on the other axes
+    sum to an odd number."""
+    K = 3 ** L
+    out = np.empty(K ** d, dtype=np.int64)
+    for t in range(K ** d):
+        digits = np.base_repr(t, 3).rjust(d * L, "0") if t else "0" * (d * L)
+        coords = [0] * d
+        others = [0] * d
+        for i, ch in enumerate(digits):
+            a, dig = i % d, int(ch)
+            coords[a] = coords[a] * 3 + (2 - dig if others[a] % 2 else dig)
+            for b in range(d):
+                if b != a:
+                    others[b] += dig
+        out[t] = np.ravel_multi_index(coords, (K,) * d)
+    return out
+
+
+def traversal_order(grid, kind):
+    """src/mesh.py:278-286: cell order of a sweep ("lexicographic" or "peano")."""
+    if kind == "lexicographic":
+        return np.arange(grid.n_cells, dtype=np.int64)
+    if kind == "peano":
+        return _peano_order(grid.d, grid.L)
+    raise ConfigurationError(f"unknown traversal kind {kind!r}")
+
+
 class Driver:
     """GPU driver (src/scheduler.py:88-313): the fused single-touch mode (the
     north-star path) or the straightforward three-sweep mode (predict pass,
@@ -291,10 +321,8 @@ class Driver:
             raise ConfigurationError("the shifted driver is not implemented on the GPU (out of scope)")
         if parallel and mode == "shifted":
             raise ConfigurationError("the shifted driver is sequential only")
-        if limiter is not None:
-            if mode != "straightforward":
-                raise ConfigurationError("subcell limiting is supported in straightforward mode only")
-            raise ConfigurationError("the GPU path has no subcell limiter (out of scope)")
+        if limiter is not None and mode != "straightforward":       # src/scheduler.py:100-102
+            raise ConfigurationError("subcell limiting is supported in straightforward mode only")
         if isinstance(traversal, np.ndarray):
             if sorted(traversal.tolist()) != list(range(grid.n_cells)):
                 raise ConfigurationError("traversal must be a permutation of the cells")
@@ -309,7 +337,8 @@ class Driver:
         self.grid, self.kernels, self.tc, self.mode = grid, kernels, time_control, mode
         self.traversal, self.parallel, self.n_workers = traversal, parallel, n_workers
         self.inject_rerun, self.spike_step, self.spike_factor = inject_rerun, spike_step, spike_factor
-        self.limiter = None
+        self.limiter = limiter
+        self.order = traversal if isinstance(traversal, np.ndarray) else traversal_order(grid, traversal)
         self.host_sync = host_sync
         self.sweep_count = self.step_count = self.rerun_count = 0
         self.reruns_by_step = Counter()
@@ -321,6 +350,17 @@ class Driver:
                       mode=mode)
         self.handle = _lib.Handle(cfg)
         self._ops = upload_operators(self.handle, kernels.basis)
+        if limiter is not None:
+            # SubcellLimiter operators + the traversal that fixes whose prev_Q the
+            # DMP test sees (src/limiter.py:138-160, src/kernels.py:208-214)
+            P, R, nearest, sample = limiter.device_arrays()
+            order = np.ascontiguousarray(self.order, dtype=np.int64)
+            self._lim_arrays = (P, R, nearest, sample, order)
+            self.handle.call("adg_set_limiter", _lib.dptr(P), _lib.dptr(R),
+                             nearest.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                             sample.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                             order.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong)),
+                             ctypes.c_double(float(limiter.cfl)))
         self.load_state(grid.Q)
         self.handle.call("adg_seed")                       # Driver._seed_time_control
         self._pull_tc()
@@ -357,11 +397,13 @@ class Driver:
         for r in recs:
             if r.reruns:
                 self.reruns_by_step[r.step] += r.reruns
+            if r.troubled:
+                self.troubled_by_step[r.step] = int(r.troubled)
             self.picard_iters += r.picard_iters
             self.predicts += r.predicts
             rec = {
                 "step": r.step, "T": r.T, "dt_old": r.dt_old, "dt_new": r.dt_new,
-                "dt_adm": r.dt_adm, "reruns": r.reruns, "troubled": 0,
+                "dt_adm": r.dt_adm, "reruns": r.reruns, "troubled": int(r.troubled),
                 "wall_time": wall_time / max(1, len(recs)),
                 "picard_iters": r.picard_iters, "predicts": r.predicts,
             }
@@ -432,6 +474,14 @@ class Driver:
                 self.handle.call("adg_set_dt_new", ctypes.c_double(final_time - T))
             self.step()
         return self.step_count
+
+    def troubled_flags(self):
+        """``[cell.troubled for cell in grid.cells]`` (src/mesh.py:39): set by the
+        limiter pipeline, cleared by a successful reconstruction."""
+        out = np.zeros(self.grid.n_cells, dtype=np.uint8)
+        self.handle.call("adg_troubled_flags", out.ctypes.data_as(ctypes.POINTER(ctypes.c_ubyte)),
+                         out.size)
+        return out.astype(bool)
 
     def picard_histogram(self):
         """Picard iterations per predict, summed over every predict so far."""

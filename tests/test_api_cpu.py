@@ -105,3 +105,30 @@ def test_product_never_imports_oracle():
                 if isinstance(node, (ast.Import, ast.ImportFrom)):
                     names = [a.name for a in node.names] + [getattr(node, "module", "") or ""]
                     assert not any("oracle" in n for n in names), fn
+
+
+def test_limiter_mode_restriction():
+    """reference tests/test_limiter.py:170-176 (raised before any device work)."""
+    from paper_1801_08682_b200 import (ConfigurationError, Driver, EulerSystem, Kernels, SubcellLimiter,
+                                       TimeControl, build_grid, make_basis, scenarios)
+    grid = build_grid(2, 1, 2, 4)
+    grid.Q[...] = scenarios.build("wave", 2, 1, 2)
+    basis = make_basis(2)
+    lim = SubcellLimiter(EulerSystem(2), basis, grid)
+    with pytest.raises(ConfigurationError, match="straightforward mode only"):
+        Driver(grid, Kernels(EulerSystem(2), basis, grid, None), TimeControl(), "fused", limiter=lim)
+
+
+def test_limiter_operators_match_reference_construction():
+    """SubcellLimiter operators (src/limiter.py:26-34,96-108) against the oracle's restatement."""
+    import limiter_oracle as LO
+    import aderdg_oracle as O
+    from paper_1801_08682_b200 import EulerSystem, SubcellLimiter, build_grid, make_basis
+    for d, p in ((2, 0), (2, 3), (3, 5), (3, 9)):
+        grid = build_grid(d, 1, p, d + 2)
+        lim = SubcellLimiter(EulerSystem(d), make_basis(p), grid)
+        ora = LO.OracleLimiter(O.OracleKernels(d, p, 1))
+        P, R, nearest, sample = lim.device_arrays()
+        assert np.array_equal(P, ora.P) and np.array_equal(R, ora.R)
+        assert np.array_equal(nearest, ora.nearest) and np.array_equal(sample, ora.sample)
+        assert lim.h_sub == ora.h_sub

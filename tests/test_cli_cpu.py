@@ -63,7 +63,6 @@ def test_config_file_parsing(tmp_path):
     (dict(scenario="sod"), "periodic"),
     (dict(mode="shifted"), "shifted"),
     (dict(limiter=True), "straightforward mode only"),
-    (dict(limiter=True, mode="straightforward"), "limiter"),
     (dict(trace=True), "trace"),
 ])
 def test_outside_gpu_path_is_a_configuration_error(kw, msg):
