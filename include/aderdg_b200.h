@@ -81,6 +81,8 @@ typedef struct {
   int system;            /* PDE plug-in (pde.py:16-102): 0 EulerSystem(d), m = d+2;
                             1 AdvectionSystem(d, velocity), m = 1                            */
   double velocity[3];    /* AdvectionSystem velocity (first d used)        */
+  int boundary;          /* build_grid(boundary=...) (mesh.py:167-231): 0 periodic; 1 outflow
+                            (zero-gradient ghost traces, kernels.py:124-127; one slab)     */
 } adg_config;
 
 typedef struct {

@@ -234,13 +234,19 @@ class AdvectionPDE:
 # ---------------------------------------------------------------------------
 # grid topology (src/mesh.py:167-243, periodic)
 
-def neighbour_tables(d, K):
-    """minus[a][c] / plus[a][c]: periodic neighbour cell of c along axis a
-    (src/mesh.py:202-215; cell index = C-order ravel, src/mesh.py:191-200)."""
+def neighbour_tables(d, K, outflow=False):
+    """minus[a][c] / plus[a][c]: neighbour cell of c along axis a (src/mesh.py:202-231;
+    cell index = C-order ravel, src/mesh.py:191-200); periodic wrap, or -1 across
+    an outflow boundary."""
     shape = (K,) * d
     idx = np.arange(K ** d).reshape(shape)
     minus = [np.roll(idx, 1, axis=a).ravel() for a in range(d)]
     plus = [np.roll(idx, -1, axis=a).ravel() for a in range(d)]
+    if outflow:
+        for a in range(d):
+            ia = np.unravel_index(np.arange(K ** d), shape)[a]
+            minus[a] = np.where(ia == 0, -1, minus[a])
+            plus[a] = np.where(ia == K - 1, -1, plus[a])
     return minus, plus
 
 
@@ -250,8 +256,9 @@ def neighbour_tables(d, K):
 class OracleKernels:
     """Batched restatement of ``Kernels`` (src/kernels.py:37-229) for Euler."""
 
-    def __init__(self, d, p, L, cfl=DEFAULT_CFL, pde=None):
+    def __init__(self, d, p, L, cfl=DEFAULT_CFL, pde=None, boundary="periodic"):
         self.d, self.p, self.L = d, p, L
+        self.outflow = boundary == "outflow"
         self.pde = pde if pde is not None else EulerPDE(d)
         self.m = self.pde.m
         self.basis = b = make_basis(p)
@@ -264,7 +271,7 @@ class OracleKernels:
         self.lift_low = b.left / w                          # src/kernels.py:58
         self.lift_high = b.right / w                        # src/kernels.py:59
         self.picard_cap = max(1, 2 * b.n)                   # src/kernels.py:60
-        self.minus, self.plus = neighbour_tables(d, self.K)
+        self.minus, self.plus = neighbour_tables(d, self.K, self.outflow)
         self.picard_hist = Counter()
 
     # src/kernels.py:68-105
@@ -334,26 +341,41 @@ class OracleKernels:
 
     # src/kernels.py:147-179: one Rusanov solve per face (face = low face of cell c)
     def solve_riemann(self, tr_q, tr_f, populated=True):
-        """Returns fstar[a] with shape (C, ...): F* of the low face of each
-        cell along axis a (minus side = low neighbour's high trace)."""
+        """Returns fstar[a] = (low, high) with shape (C, ...): F* of the low and
+        the high face of each cell along axis a (low face: minus side = low
+        neighbour's high trace).  At an outflow boundary face the ghost side
+        holds the cell's own trace (src/kernels.py:124-127)."""
         d = self.d
         out = []
         for a in range(d):
             qp, fp = tr_q[a][0], tr_f[a][0]                 # plus side: own low trace
             qm = tr_q[a][1][self.minus[a]]                  # minus side: neighbour high
             fm = tr_f[a][1][self.minus[a]]
+            if self.outflow:
+                lo = (self.minus[a] < 0).reshape((-1,) + (1,) * (qp.ndim - 1))
+                qm, fm = np.where(lo, qp, qm), np.where(lo, fp, fm)
             if not populated:
-                out.append(np.zeros_like(qp))
+                out.append((np.zeros_like(qp), np.zeros_like(qp)))
                 continue
-            C = qp.shape[0]
-            with np.errstate(all="ignore"):
-                sm = np.max(self.pde.max_signal_speed(qm, a).reshape(C, -1), axis=1)
-                sp = np.max(self.pde.max_signal_speed(qp, a).reshape(C, -1), axis=1)
-            # python max(sm, sp): a NaN on the minus side wins, one on the plus side is ignored
-            alpha = np.where(np.isnan(sp), sm, np.maximum(sm, sp))
-            al = alpha.reshape((-1,) + (1,) * (qp.ndim - 1))
-            out.append(0.5 * (fm + fp) - 0.5 * al * (qp - qm))
+            low = self._rusanov(qm, fm, qp, fp, a)
+            high = low[self.plus[a]]
+            if self.outflow:
+                hi = (self.plus[a] < 0).reshape((-1,) + (1,) * (qp.ndim - 1))
+                qh, fh = tr_q[a][1], tr_f[a][1]             # own high trace on both sides
+                high = np.where(hi, self._rusanov(qh, fh, qh, fh, a), high)
+            out.append((low, high))
         return out
+
+    def _rusanov(self, qm, fm, qp, fp, a):
+        """src/kernels.py:173-177 for one batch of faces."""
+        C = qp.shape[0]
+        with np.errstate(all="ignore"):
+            sm = np.max(self.pde.max_signal_speed(qm, a).reshape(C, -1), axis=1)
+            sp = np.max(self.pde.max_signal_speed(qp, a).reshape(C, -1), axis=1)
+        # python max(sm, sp): a NaN on the minus side wins, one on the plus side is ignored
+        alpha = np.where(np.isnan(sp), sm, np.maximum(sm, sp))
+        al = alpha.reshape((-1,) + (1,) * (qp.ndim - 1))
+        return 0.5 * (fm + fp) - 0.5 * al * (qp - qm)
 
     # src/kernels.py:183-206 (fixed order: axis ascending, low then high)
     def integrate_face(self, D, fstar, dt):
@@ -362,9 +384,9 @@ class OracleKernels:
         for a in range(d):
             for side_local, lift in ((0, self.lift_low), (1, self.lift_high)):
                 if side_local == 0:
-                    blk = -fstar[a]                       # PLUS side stores -F*
+                    blk = -fstar[a][0]                    # PLUS side stores -F*
                 else:
-                    blk = fstar[a][self.plus[a]]          # MINUS side stores +F*
+                    blk = fstar[a][1]                     # MINUS side stores +F*
                 fbar = np.tensordot(blk, b.weights, axes=(d, 0))   # (C, n^(d-1)..., m)
                 shape = [1] * (d + 2)
                 shape[1 + a] = b.n
@@ -437,12 +459,12 @@ class FusedDriver:
 
     def __init__(self, Q, d, p, L, cfl=DEFAULT_CFL, c_dt=DEFAULT_C_DT,
                  averaging="strict", forced_dt=None, inject_rerun=False,
-                 spike_step=None, spike_factor=3.0, velocity=None):
+                 spike_step=None, spike_factor=3.0, velocity=None, boundary="periodic"):
         """``velocity`` given: AdvectionSystem(d, velocity) (m = 1), else Euler."""
         pde = AdvectionPDE(d, velocity) if velocity is not None else EulerPDE(d)
         if velocity is not None and spike_step is not None:
             raise OracleError("ConfigurationError", "the speed spike is defined for Euler runs")
-        self.k = OracleKernels(d, p, L, cfl, pde)
+        self.k = OracleKernels(d, p, L, cfl, pde, boundary)
         self.d, self.p, self.L = d, p, L
         self.Q = Q
         self.D = np.zeros_like(Q)                       # src/mesh.py:238-239

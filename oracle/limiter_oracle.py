@@ -140,9 +140,11 @@ class OracleLimiter:
             me = np.arange(C)
             for a in range(d):
                 for nb in (k.minus[a], k.plus[a]):
-                    before = (rank[nb] <= rank[me])[:, None]
-                    lo = np.minimum(lo, np.where(before, cmin[nb], omin[nb]))
-                    hi = np.maximum(hi, np.where(before, cmax[nb], omax[nb]))
+                    there = (nb >= 0)[:, None]           # outflow: no neighbour (limiter.py:150-151)
+                    nbc = np.where(nb >= 0, nb, me)
+                    before = (rank[nbc] <= rank[me])[:, None]
+                    lo = np.where(there, np.minimum(lo, np.where(before, cmin[nbc], omin[nbc])), lo)
+                    hi = np.where(there, np.maximum(hi, np.where(before, cmax[nbc], omax[nbc])), hi)
             delta = DMP_ABS + DMP_REL * (hi - lo)
             cand_lo = np.minimum(Q.min(axis=sp), patch.min(axis=sp))
             cand_hi = np.maximum(Q.max(axis=sp), patch.max(axis=sp))
@@ -164,8 +166,12 @@ class OracleLimiter:
         patch = self.start_patch(prev[ci])
         halo = []
         for a in range(d):
-            low = _take_layer(self.start_patch(prev[k.minus[a][ci]]), a, -1)
-            high = _take_layer(self.start_patch(prev[k.plus[a][ci]]), a, 0)
+            lo_nb, hi_nb = k.minus[a][ci], k.plus[a][ci]
+            # outflow boundary: zero-gradient copy of the own edge (limiter.py:185-187)
+            low = (_take_layer(self.start_patch(prev[lo_nb]), a, -1) if lo_nb >= 0
+                   else _take_layer(patch, a, 0))
+            high = (_take_layer(self.start_patch(prev[hi_nb]), a, 0) if hi_nb >= 0
+                    else _take_layer(patch, a, -1))
             halo.append((low, high))
         remaining = dt
         while remaining > 1e-15 * dt:

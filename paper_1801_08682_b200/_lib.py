@@ -43,7 +43,7 @@ class AdgConfig(ctypes.Structure):
         ("spike_factor", ctypes.c_double), ("device", ctypes.c_int),
         ("rank", ctypes.c_int), ("world", ctypes.c_int), ("halo_mode", ctypes.c_int),
         ("driver_mode", ctypes.c_int), ("system", ctypes.c_int),
-        ("velocity", ctypes.c_double * 3),
+        ("velocity", ctypes.c_double * 3), ("boundary", ctypes.c_int),
     ]
 
 

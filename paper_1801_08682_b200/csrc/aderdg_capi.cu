@@ -334,6 +334,7 @@ static SweepParams sweep_params(adg_handle* h, int mode) {
   P.cell_a = 0;
   P.blk_split = INT_MAX;
   P.cell_jump = 0;
+  P.outflow = h->cfg.boundary == 1 ? 1 : 0;
   // limiter hooks: the corrector of step s snapshots prev_Q into lim_prev[s & 1]
   P.lim_troubled = h->lim ? h->lim_troubled : nullptr;
   P.lim_cur = h->lim ? h->lim_prev[h->sweep_index & 1] : nullptr;
@@ -416,6 +417,7 @@ static adg_status launch_limiter(adg_handle* h) {
   L.ns = h->lim_ns;
   L.K = h->K;
   L.n_cells = (int)h->cells_local;
+  L.outflow = h->cfg.boundary == 1 ? 1 : 0;
   L.h_sub = h->h / (double)h->lim_ns;          // limiter.py:96  grid.h / ns
   L.cfl = h->lim_cfl;
   h->ldisp.detect(L, (unsigned)h->cells_local, h->lim_detect_smem, h->stream);
@@ -484,7 +486,13 @@ adg_status adg_create(const adg_config* cfg, adg_handle** out) {
   if (c.system == 1 && c.spike_step >= 0) {                      // scheduler.py:170-171
     h->err = "the speed spike is defined for Euler runs"; *out = h; return ADG_ERR_CONFIG;
   }
-  if (!dispatch_for(c.d, c.p, c.system, &h->disp)) {
+  if (c.boundary != 0 && c.boundary != 1) { h->err = "boundary must be 0 (periodic) or 1 (outflow)"; *out = h; return ADG_ERR_CONFIG; }
+  if (c.boundary == 1 && (c.world > 1 || c.halo_mode != 0)) {
+    h->err = "outflow boundaries run on a single slab (world = 1)"; *out = h; return ADG_ERR_CONFIG;
+  }
+  if (c.boundary == 1 && c.system == 0) {        // ghost faces live in the generic kernel
+    if (!dispatch_generic(c.d, c.p, &h->disp)) { h->err = "no generic kernel for this order"; *out = h; return ADG_ERR_CONFIG; }
+  } else if (!dispatch_for(c.d, c.p, c.system, &h->disp)) {
     snprintf(buf, sizeof buf, "no sm_100a kernel instantiated for d=%d p=%d", c.d, c.p);
     h->err = buf; *out = h; return ADG_ERR_CONFIG;
   }

@@ -50,6 +50,7 @@ struct LimParams {
   long long scratch_cta;     // doubles per CTA
   DevState* st;
   int n, ns, K, n_cells;
+  int outflow;               // boundary faces have no neighbour (mesh.py:139-146 -> None)
   double h_sub, cfl;
 };
 
@@ -59,13 +60,15 @@ __device__ __forceinline__ long long ipow_ll(int b, int e) {
   return r;
 }
 
-// neighbour of `cell` across face f (axis f/2, low side for even f), periodic
+// neighbour of `cell` across face f (axis f/2, low side for even f): periodic,
+// or -1 across an outflow boundary (Grid.cell_neighbors -> None)
 template <int DIM>
-__device__ __forceinline__ int face_neighbour(int cell, int f, int K) {
+__device__ __forceinline__ int face_neighbour(int cell, int f, int K, int outflow) {
   const int a = f >> 1;
   int st = 1;
   for (int b = DIM - 1; b > a; --b) st *= K;
   const int ia = (cell / st) % K;
+  if (outflow && ((f & 1) ? ia == K - 1 : ia == 0)) return -1;
   const int ja = (f & 1) ? (ia + 1) % K : (ia + K - 1) % K;
   return cell + (ja - ia) * st;
 }
@@ -263,7 +266,8 @@ __global__ void __launch_bounds__(256) lim_detect_kernel(const LimParams L) {
       block_minmax<M>(L.cur + (long long)cell * NM, N, lo, hi, red);
       const int r0 = L.rank[cell];
       for (int f = 0; f < 2 * DIM; ++f) {
-        const int nb = face_neighbour<DIM>(cell, f, L.K);
+        const int nb = face_neighbour<DIM>(cell, f, L.K, L.outflow);
+        if (nb < 0) continue;                    // limiter.py:150-151
         const double* src = (L.rank[nb] <= r0) ? L.cur : L.old;
         block_minmax<M>(src + (long long)nb * NM, N, lo, hi, red);
       }
@@ -369,16 +373,20 @@ __global__ void __launch_bounds__(256) lim_apply_kernel(const LimParams L) {
     start_patch<PDE, DIM>(L.cur + (long long)cell * NM, A, T1, T2, L);
     for (int f = 0; f < 2 * DIM; ++f) {
       const int a = f >> 1;
-      const int nb = face_neighbour<DIM>(cell, f, L.K);
-      start_patch<PDE, DIM>(L.cur + (long long)nb * NM, Y, T1, T2, L);
-      // low face: the neighbour's last layer along a; high face: its first
-      const int lay = (f & 1) ? 0 : ns - 1;
+      const int nb = face_neighbour<DIM>(cell, f, L.K, L.outflow);
+      const double* Ysrc = A;                    // boundary: zero-gradient copy of the own edge
+      int lay = (f & 1) ? ns - 1 : 0;
+      if (nb >= 0) {
+        start_patch<PDE, DIM>(L.cur + (long long)nb * NM, Y, T1, T2, L);
+        Ysrc = Y;
+        lay = (f & 1) ? 0 : ns - 1;              // low face: neighbour's last layer; high: its first
+      }
       int inner = 1;
       for (int b = DIM - 1; b > a; --b) inner *= ns;
       for (int e = threadIdx.x; e < nlay * M; e += blockDim.x) {
         const int c = e % M, t = e / M;
         const int i = t % inner, o = t / inner;
-        H[(long long)f * nlay * M + e] = Y[(((long long)o * ns + lay) * inner + i) * M + c];
+        H[(long long)f * nlay * M + e] = Ysrc[(((long long)o * ns + lay) * inner + i) * M + c];
       }
       __syncthreads();
     }

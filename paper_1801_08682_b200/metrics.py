@@ -148,8 +148,10 @@ def book_rerun_pass(ledger, sweep, step, cells):
         ledger.book(t, cells)
 
 
-def book_straightforward_step(ledger, sweep, step, cells, faces):
-    """The three sweeps of a straightforward step (src/scheduler.py:230-313)."""
+def book_straightforward_step(ledger, sweep, step, cells, faces, troubled=0):
+    """The three sweeps of a straightforward step (src/scheduler.py:230-313); with a
+    limiter every troubled cell books one more calcTimeStep after its subcell
+    pass (src/scheduler.py:307-309; the limiter itself records nothing)."""
     ledger.begin_sweep(sweep, step, step)
     ledger.book("predict", cells)
     ledger.book("extrapolate", cells)
@@ -158,15 +160,17 @@ def book_straightforward_step(ledger, sweep, step, cells, faces):
     ledger.begin_sweep(sweep + 2, step, step)
     for t in ("integrateVolume", "integrateFace", "update", "calcTimeStep"):
         ledger.book(t, cells)
+    if troubled:
+        ledger.book("calcTimeStep", troubled)
 
 
-def record_step(ledger, mode, step, reruns, cells, faces):
+def record_step(ledger, mode, step, reruns, cells, faces, troubled=0):
     """Book realisation step ``step`` of a GPU run (priming sweep inside step 1,
     the rerun pass when ``reruns``) and return the ledger columns of its
     metrics record, as ``Driver._record_step`` does (src/scheduler.py:459-481)."""
     reads0, writes0 = Counter(ledger.task_reads), Counter(ledger.task_writes)
     if mode == "straightforward":
-        book_straightforward_step(ledger, 3 * (step - 1), step, cells, faces)
+        book_straightforward_step(ledger, 3 * (step - 1), step, cells, faces, troubled)
     else:
         if step == 1:
             book_fused_sweep(ledger, 0, 0, cells, faces)

@@ -144,7 +144,23 @@ def shock_tube(d, L, p, seed=0, noise=0.0, pressure_ratio=10.0):
     return conserved(rho, np.zeros(x.shape[:-1] + (d,)), pr)
 
 
+def sod(d, L, p):
+    """The reference's Sod tube (``src/cli.py:145-155``, ``tests/test_limiter.py:104-109``):
+    rho = 1 / 0.125 and E = 1/0.4 / 0.1/0.4 left / right of x_0 = 0.5, at rest;
+    run with outflow boundaries."""
+    x = node_coordinates(d, L, p)
+    left = x[..., 0] < 0.5
+    Q = np.zeros(x.shape[:-1] + (d + 2,))
+    Q[..., 0] = np.where(left, 1.0, 0.125)
+    Q[..., -1] = np.where(left, 1.0, 0.1) / 0.4
+    return Q
+
+
+#: scenarios whose grid has outflow boundaries (src/cli.py:155)
+OUTFLOW = ("sod",)
+
 SCENARIOS = {
+    "sod": sod,
     "shocktube": shock_tube,
     "bump": gaussian_bump_noise,
     "fourier": random_fourier,

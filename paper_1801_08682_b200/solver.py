@@ -190,7 +190,8 @@ def device_bytes(d, L, p, m=None):
 
 def build_grid(d, L, p, m, boundary="periodic", storage="hull",
                budget_bytes=DEFAULT_BUDGET_BYTES):
-    """src/mesh.py:167-243 (periodic, hull storage)."""
+    """src/mesh.py:167-243 (periodic or outflow boundaries; the device layout
+    is the same for both storage kinds)."""
     if d not in (2, 3):
         raise ConfigurationError(f"dimension must be 2 or 3, got {d}")
     if not 1 <= L <= 4:
@@ -199,8 +200,6 @@ def build_grid(d, L, p, m, boundary="periodic", storage="hull",
         raise ConfigurationError(f"order p must be in [0, 9], got {p}")
     if boundary not in ("periodic", "outflow"):
         raise ConfigurationError(f"unknown boundary kind {boundary!r}")
-    if boundary != "periodic":
-        raise ConfigurationError("the GPU path implements periodic boundaries only")
     if storage not in ("hull", "spacetime"):
         raise ConfigurationError(f"unknown storage layout {storage!r}")
     if m not in (d + 2, 1):
@@ -256,6 +255,7 @@ def _config(grid, kernels, tc, inject_rerun, spike_step, spike_factor, device, r
     cfg.device = int(device)
     cfg.rank, cfg.world = int(rank), int(world)
     cfg.driver_mode = 1 if mode == "straightforward" else 0
+    cfg.boundary = 1 if grid.boundary == "outflow" else 0
     system = kernels.system
     if system.name == "advection":
         cfg.system = 1
@@ -390,8 +390,10 @@ class Driver:
         if led is None or not hasattr(led, "book"):
             return
         g = self.grid
-        rec.update(metrics.record_step(led, self.mode, r.step, r.reruns, g.n_cells,
-                                       g.d * g.n_cells))          # periodic: d faces per cell
+        K = g.cells_per_axis
+        n_faces = g.d * g.n_cells if g.boundary == "periodic" else g.d * (K + 1) * K ** (g.d - 1)
+        rec.update(metrics.record_step(led, self.mode, r.step, r.reruns, g.n_cells, n_faces,
+                                       int(r.troubled)))
 
     def _absorb(self, recs, wall_time=0.0):
         for r in recs:

@@ -41,6 +41,11 @@ def golden_problem(meta):
     return scenarios.build(scen, d, L, p), None
 
 
+def golden_boundary(meta):
+    """Grid boundary of a golden case (the sod scenario runs with outflow, src/cli.py:155)."""
+    return meta.get("boundary", "periodic")
+
+
 def make_system(d, velocity):
     from paper_1801_08682_b200 import AdvectionSystem, EulerSystem
     return EulerSystem(d) if velocity is None else AdvectionSystem(d, velocity)

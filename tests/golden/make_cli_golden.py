@@ -28,6 +28,7 @@ CASES = {
     "uniform_fused": dict(scenario="uniform", mode="fused", steps=2),
     "wave_forced_creeping": dict(scenario="smooth-density-wave", mode="fused", steps=6,
                                  forced_dt=2e-4, averaging="creeping", L=2, p=2),
+    "sod_limiter": dict(scenario="sod", mode="straightforward", steps=20, limiter=True, L=2, p=3),
 }
 CONVERGENCE = {"conv_p2": (dict(scenario="gaussian-advect", d=2, p=2), (1, 2), 0.02)}
 
@@ -35,7 +36,10 @@ CONVERGENCE = {"conv_p2": (dict(scenario="gaussian-advect", d=2, p=2), (1, 2), 0
 def main():
     from aderdg.cli import RunConfig, convergence_study, run_simulation, write_convergence_csv
     tmp = tempfile.mkdtemp()
+    only = sys.argv[1:]
     for name, kw in CASES.items():
+        if only and name not in only:
+            continue
         out = os.path.join(tmp, name)
         cfg = RunConfig(out=out, **kw)
         run_simulation(cfg)
@@ -47,6 +51,8 @@ def main():
             json.dump(kw, fh, indent=1)
         print(name, "ok")
     for name, (kw, levels, tf) in CONVERGENCE.items():
+        if only and name not in only:
+            continue
         rows = convergence_study(RunConfig(**kw), levels, final_time=tf)
         dst = os.path.join(HERE, "cli", name)
         os.makedirs(dst, exist_ok=True)

@@ -73,6 +73,11 @@ SMALL = {
     "adv_noise_d3_L2_p3": ("gauss_noise", 3, 2, 3, 5, {}, {}, True),
     "sf_adv_gauss_d2_L2_p3": ("gauss", 2, 2, 3, 8, {"mode": "straightforward"}, {}, True),
     "sf_adv_gauss_d3_L1_p4_creeping": ("gauss", 3, 1, 4, 4, {"mode": "straightforward"}, {"averaging": "creeping"}, True),
+    # outflow boundaries (src/mesh.py:216-231, kernels.py:124-127), Sod without limiter
+    "sod_d2_L2_p0": ("sod", 2, 2, 0, 12, {}, {}, True),
+    "sod_d2_L2_p1": ("sod", 2, 2, 1, 6, {}, {}, True),
+    "sod_d3_L1_p2": ("sod", 3, 1, 2, 4, {}, {}, True),
+    "sf_sod_d2_L2_p1": ("sod", 2, 2, 1, 6, {"mode": "straightforward"}, {}, True),
 }
 BIG = {
     "bump_d3_L3_p3_cfg2": ("bump", 3, 3, 3, 20, {}, {}, False),
@@ -99,7 +104,8 @@ def run_case(name, spec):
     dkw = dict(dkw)
     mode = dkw.pop("mode", "fused")
     storage = "spacetime" if mode == "straightforward" else "hull"
-    grid = build_grid(d, L, p, system.m, storage=storage, budget_bytes=1 << 40)
+    boundary = "outflow" if scen in scenarios.OUTFLOW else "periodic"
+    grid = build_grid(d, L, p, system.m, boundary=boundary, storage=storage, budget_bytes=1 << 40)
     for c in grid.cells:
         c.Q[...] = Q0[c.index]
     kernels = Kernels(system, basis, grid, None, cfl=0.9)
@@ -145,7 +151,8 @@ def run_case(name, spec):
         "Q_final_absmax": np.max(np.abs(Qf.reshape(-1, Qf.shape[-1])), axis=0),
         "picard_keys": np.array(sorted(hist), dtype=np.int64),
         "picard_vals": np.array([hist[k] for k in sorted(hist)], dtype=np.int64),
-        "meta": np.array(json.dumps({"scenario": scen, "system": system.name, "d": d, "L": L, "p": p, "steps": steps,
+        "meta": np.array(json.dumps({"scenario": scen, "system": system.name, "boundary": boundary,
+                                     "d": d, "L": L, "p": p, "steps": steps,
                                      "driver_kwargs": dkw, "mode": mode, "tc_kwargs": tkw, "error": error,
                                      "wall_s": wall, "sweep_count": driver.sweep_count if driver else None,
                                      "rerun_count": driver.rerun_count if driver else None,

@@ -41,6 +41,13 @@ CASES = {
                                {"averaging": "creeping"}),
     "bump_d3_L1_p7_noisy": ("bump", {"noise": 5e-2, "seed": 2}, 3, 1, 7, 4, {}, {}),
     "tube_d2_L1_p9": ("shocktube", {}, 2, 1, 9, 5, {}, {}),
+    # outflow Sod, the reference's own limiter tests (tests/test_limiter.py:130-151,
+    # tests/test_acceptance.py:202-229)
+    "sod_d2_L2_p2": ("sod", {}, 2, 2, 2, 30, {}, {}),
+    "sod_d2_L2_p3": ("sod", {}, 2, 2, 3, 30, {}, {}),
+    "sod_d2_L2_p3_100": ("sod", {}, 2, 2, 3, 100, {}, {}),
+    "sod_d3_L1_p2": ("sod", {}, 3, 1, 2, 10, {}, {}),
+    "sod_d2_L2_p4_peano": ("sod", {}, 2, 2, 4, 12, {"traversal": "peano"}, {}),
 }
 
 
@@ -52,7 +59,8 @@ def run_case(name, spec):
     Q0 = scenarios.build(scen, d, L, p, **skw)
     system = EulerSystem(d)
     basis = make_basis(p)
-    grid = build_grid(d, L, p, system.m, storage="spacetime", budget_bytes=1 << 40)
+    boundary = "outflow" if scen in scenarios.OUTFLOW else "periodic"
+    grid = build_grid(d, L, p, system.m, boundary=boundary, storage="spacetime", budget_bytes=1 << 40)
     for c in grid.cells:
         c.Q[...] = Q0[c.index]
     lim = SubcellLimiter(system, basis, grid, cfl=0.9)
@@ -77,7 +85,8 @@ def run_case(name, spec):
         "Q0_sum": np.array([np.sum(Q0), np.sum(np.abs(Q0))]),
         "Q_final": np.stack([c.Q for c in grid.cells]),
         "troubled_final": np.array([bool(c.troubled) for c in grid.cells]),
-        "meta": np.array(json.dumps({"scenario": scen, "scenario_kwargs": skw, "d": d, "L": L,
+        "meta": np.array(json.dumps({"scenario": scen, "scenario_kwargs": skw, "boundary": boundary,
+                                     "d": d, "L": L,
                                      "p": p, "steps": steps, "driver_kwargs": dkw,
                                      "tc_kwargs": tkw, "error": error, "wall_s": wall})),
     }

@@ -35,7 +35,8 @@ def test_build_grid_validation():
     with pytest.raises(ConfigurationError):
         build_grid(2, 1, 10, 4)
     with pytest.raises(ConfigurationError):
-        build_grid(2, 1, 1, 4, boundary="outflow")
+        build_grid(2, 1, 1, 4, boundary="reflective")
+    assert build_grid(2, 1, 1, 4, boundary="outflow").boundary == "outflow"
     with pytest.raises(ResourceBudgetError):
         build_grid(3, 3, 3, 5, budget_bytes=1 << 20)
     g = build_grid(3, 2, 3, 5)

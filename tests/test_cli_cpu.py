@@ -60,7 +60,6 @@ def test_config_file_parsing(tmp_path):
 
 
 @pytest.mark.parametrize("kw,msg", [
-    (dict(scenario="sod"), "periodic"),
     (dict(mode="shifted"), "shifted"),
     (dict(limiter=True), "straightforward mode only"),
     (dict(trace=True), "trace"),
@@ -84,13 +83,15 @@ def test_closed_form_ledger_matches_reference_metrics(case):
     the reference's integer ledger columns and run.json audit figures."""
     kw = json.load(open(os.path.join(CLI, case, "case.json")))
     cfg = RunConfig(**kw)
-    system, _, _ = scenario(cfg.scenario, cfg.d)
+    system, _, boundary = scenario(cfg.scenario, cfg.d)
     rows = read_metrics(os.path.join(CLI, case, "metrics.csv"))
     led = metrics.AccessLedger(cfg.mode, cfg.d, cfg.p, system.m)
-    cells = 3 ** (cfg.d * cfg.L)
+    K = 3 ** cfg.L
+    cells = K ** cfg.d
+    faces = cfg.d * cells if boundary == "periodic" else cfg.d * (K + 1) * K ** (cfg.d - 1)
     for row in rows:
         rec = metrics.record_step(led, cfg.mode, int(row["step"]), int(row["reruns"]), cells,
-                                  cfg.d * cells)
+                                  faces, int(row["troubled"]))
         for col in METRIC_COLUMNS:
             if col in ("step", "T", "dt_old", "dt_new", "dt_adm", "reruns", "troubled", "wall_time"):
                 continue
@@ -99,7 +100,7 @@ def test_closed_form_ledger_matches_reference_metrics(case):
     audit = metrics.single_touch_audit(led, cells, len(rows))
     assert audit["amortised"] == man["q_reads_per_cell_step"]
     storage = "spacetime" if cfg.mode == "straightforward" else "hull"
-    assert metrics.estimate_persistent_doubles(cfg.d, cfg.L, cfg.p, system.m, "periodic",
+    assert metrics.estimate_persistent_doubles(cfg.d, cfg.L, cfg.p, system.m, boundary,
                                                storage) == man["persistent_doubles"]
 
 

@@ -24,11 +24,12 @@ CASES = sorted(f[4:-4] for f in os.listdir(GOLDEN) if f.startswith("lim_") and f
 TOL = 1e-10
 
 
-def gpu_run(Q0, d, L, p, steps, velocity=None, traversal="lexicographic", tc_kwargs=None):
+def gpu_run(Q0, d, L, p, steps, velocity=None, traversal="lexicographic", tc_kwargs=None,
+            boundary="periodic"):
     from paper_1801_08682_b200 import (AdvectionSystem, Driver, EulerSystem, Kernels, SubcellLimiter,
                                        TimeControl, build_grid, make_basis)
     system = EulerSystem(d) if velocity is None else AdvectionSystem(d, velocity)
-    grid = build_grid(d, L, p, system.m)
+    grid = build_grid(d, L, p, system.m, boundary=boundary)
     grid.Q[...] = Q0
     basis = make_basis(p)
     lim = SubcellLimiter(system, basis, grid, cfl=0.9)
@@ -46,7 +47,8 @@ def test_limiter_matches_reference(cuda_ok, name):
     d, L, p = meta["d"], meta["L"], meta["p"]
     Q0 = scenarios.build(meta["scenario"], d, L, p, **meta["scenario_kwargs"])
     trav = g["order"] if "order" in g else meta["driver_kwargs"].get("traversal", "lexicographic")
-    drv, grid = gpu_run(Q0, d, L, p, meta["steps"], traversal=trav, tc_kwargs=meta["tc_kwargs"])
+    drv, grid = gpu_run(Q0, d, L, p, meta["steps"], traversal=trav, tc_kwargs=meta["tc_kwargs"],
+                        boundary=meta.get("boundary", "periodic"))
     assert rel_linf(grid.Q, g["Q_final"]) <= TOL
     rec = np.array([[r["step"], r["T"], r["dt_old"], r["dt_new"], r["dt_adm"], r["troubled"]]
                     for r in drv.step_records])
@@ -63,28 +65,32 @@ def test_limiter_matches_reference(cuda_ok, name):
     ("shocktube", {"pressure_ratio": 50.0}, 2, 2, 1, 12, None),
     ("shocktube", {}, 2, 2, 0, 10, None),
     ("gauss", {"noise": 0.3, "seed": 2}, 2, 2, 3, 6, (1.0, 0.5)),
+    ("sod", {}, 3, 2, 2, 4, None),
 ])
 def test_limiter_matches_oracle(cuda_ok, scen, kw, d, L, p, steps, vel):
     import aderdg_oracle as O  # noqa: F401  (sys.path set by conftest)
     import limiter_oracle as LO
     from paper_1801_08682_b200 import scenarios
     Q0 = scenarios.build(scen, d, L, p, **kw)
-    ora = LO.LimitedStraightforwardDriver(Q0.copy(), d, p, L, velocity=vel)
+    bnd = "outflow" if scen in scenarios.OUTFLOW else "periodic"
+    ora = LO.LimitedStraightforwardDriver(Q0.copy(), d, p, L, velocity=vel, boundary=bnd)
     with np.errstate(all="ignore"):
         ora.run(steps)
-    drv, grid = gpu_run(Q0, d, L, p, steps, velocity=vel)
+    drv, grid = gpu_run(Q0, d, L, p, steps, velocity=vel, boundary=bnd)
     assert rel_linf(grid.Q, ora.Q) <= TOL
     assert [r["troubled"] for r in drv.step_records] == [r["troubled"] for r in ora.step_records]
     assert np.array_equal(drv.troubled_flags(), ora.troubled)
     drv.close()
 
 
-def test_limiter_keeps_shock_tube_admissible(cuda_ok):
-    """reference tests/test_limiter.py:130-151 / test_acceptance.py:202-229 on the
-    periodic tube: limiting happens and every final state is admissible."""
+@pytest.mark.parametrize("p,steps", [(2, 30), (3, 30), (3, 100)])
+def test_limited_sod_stays_admissible(cuda_ok, p, steps):
+    """reference tests/test_limiter.py:130-151 and test_acceptance.py:202-229:
+    outflow Sod with the limiter; limiting happens and every final state is
+    admissible."""
     from paper_1801_08682_b200 import EulerSystem, scenarios
-    Q0 = scenarios.build("shocktube", 2, 2, 3)
-    drv, grid = gpu_run(Q0, 2, 2, 3, 40)
+    Q0 = scenarios.build("sod", 2, 2, p)
+    drv, grid = gpu_run(Q0, 2, 2, p, steps, boundary="outflow")
     assert sum(drv.troubled_by_step.values()) >= 1
     assert EulerSystem(2).is_admissible(grid.Q)
     drv.close()

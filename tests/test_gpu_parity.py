@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import aderdg_oracle as O
-from conftest import golden_names, golden_problem, load_golden, make_system, rel_linf
+from conftest import golden_boundary, golden_names, golden_problem, load_golden, make_system, rel_linf
 from paper_1801_08682_b200 import (Driver, EulerSystem, Kernels, NumericalError,
                                    PredictorFailureError, TimeControl, build_grid,
                                    make_basis, scenarios)
@@ -18,9 +18,9 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-10   # north_star: rel L-inf in fp64
 
 
-def make_driver(Q0, d, L, p, dkw=None, tkw=None, host_sync="run", velocity=None):
+def make_driver(Q0, d, L, p, dkw=None, tkw=None, host_sync="run", velocity=None, boundary="periodic"):
     system = make_system(d, velocity)
-    grid = build_grid(d, L, p, system.m)
+    grid = build_grid(d, L, p, system.m, boundary=boundary)
     grid.Q[...] = Q0
     kern = Kernels(system, make_basis(p), grid, None, cfl=0.9)
     tc = TimeControl(c_dt=0.99, **(tkw or {}))
@@ -32,6 +32,20 @@ def records_array(drv):
                      for r in drv.step_records]).reshape(-1, 6)
 
 
+def run_or_match_error(drv, meta):
+    """Run the golden's steps; when the reference aborted, the GPU must abort with
+    the same class and message (step and cell included).  True if it aborted."""
+    try:
+        drv.run(steps=meta["steps"])
+    except (NumericalError, PredictorFailureError) as e:
+        assert meta["error"] is not None, f"GPU aborted, reference did not: {e}"
+        assert type(e).__name__ == meta["error"]["class"]
+        assert str(e) == meta["error"]["message"]
+        return True
+    assert meta["error"] is None, "reference aborted, GPU did not"
+    return False
+
+
 SMALL = [n for n in golden_names() if not any(t in n for t in ("cfg2", "cfg3", "L2_p5")) and not n.startswith("sf_")]
 
 
@@ -41,8 +55,10 @@ def test_gpu_matches_reference_golden(cuda_ok, name):
     meta = g["meta"]
     d, L, p = meta["d"], meta["L"], meta["p"]
     Q0, vel = golden_problem(meta)
-    drv = make_driver(Q0, d, L, p, meta["driver_kwargs"], meta["tc_kwargs"], velocity=vel)
-    drv.run(steps=meta["steps"])
+    drv = make_driver(Q0, d, L, p, meta["driver_kwargs"], meta["tc_kwargs"], velocity=vel,
+                      boundary=golden_boundary(meta))
+    if run_or_match_error(drv, meta):
+        return
     recs = records_array(drv)
     ref = g["records"]
     assert np.array_equal(recs[:, 0], ref[:, 0])
@@ -210,12 +226,13 @@ def test_gpu_straightforward_matches_reference(cuda_ok, name):
     d, L, p = meta["d"], meta["L"], meta["p"]
     Q0, vel = golden_problem(meta)
     system = make_system(d, vel)
-    grid = build_grid(d, L, p, system.m)
+    grid = build_grid(d, L, p, system.m, boundary=golden_boundary(meta))
     grid.Q[...] = Q0
     kern = Kernels(system, make_basis(p), grid, None, cfl=0.9)
     drv = Driver(grid, kern, TimeControl(c_dt=0.99, **meta["tc_kwargs"]), "straightforward",
                  host_sync="run", **meta["driver_kwargs"])
-    drv.run(steps=meta["steps"])
+    if run_or_match_error(drv, meta):
+        return
     recs = records_array(drv)
     ref = g["records"]
     assert recs.shape == ref.shape

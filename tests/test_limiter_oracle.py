@@ -37,7 +37,7 @@ def load_case(name):
 
 def run_oracle(meta, Q0, order=None):
     drv = LO.LimitedStraightforwardDriver(Q0.copy(), meta["d"], meta["p"], meta["L"], order=order,
-                                          **meta["tc_kwargs"])
+                                          boundary=meta.get("boundary", "periodic"), **meta["tc_kwargs"])
     with np.errstate(all="ignore"):
         drv.run(meta["steps"])
     return drv
