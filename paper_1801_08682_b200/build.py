@@ -13,6 +13,7 @@ OUT = os.path.join(HERE, "libaderdg_b200.so")
 SOURCES = [os.path.join(CSRC, "aderdg_capi.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, "aderdg_kernels.cuh"), os.path.join(CSRC, "aderdg_sweep_v2.cuh"),
                   os.path.join(CSRC, "aderdg_sweep_ho.cuh"), os.path.join(CSRC, "aderdg_sweep_st.cuh"),
+                  os.path.join(CSRC, "aderdg_limiter.cuh"),
                   os.path.join(os.path.dirname(HERE), "include", "aderdg_b200.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",

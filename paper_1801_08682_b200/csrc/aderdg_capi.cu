@@ -83,15 +83,16 @@ bool dispatch_adv(int n, Dispatch* out) {
   return false;
 }
 
-template <int NQ>
+template <int NQ, int LN = 2>
 void launch_sweep_ho(const SweepParams& P, unsigned grid, cudaStream_t s) {
   using S = ShapeHO<NQ>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(sweep_kernel_ho<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM_BYTES);
+    cudaFuncSetAttribute(sweep_kernel_ho<NQ, true, LN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)S::SMEM_BYTES);
     attr = true;
   }
-  sweep_kernel_ho<NQ><<<grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
+  sweep_kernel_ho<NQ, true, LN><<<grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
 }
 
 int kernel_variant() {
@@ -114,10 +115,19 @@ Dispatch make_dispatch_st() {
   return Dispatch{&launch_sweep_st, ShapeST::REC};
 }
 
+// ADG_KERNEL=15 / 18 / 19: DMMA-tile / constant-bank line / lane-group line
+// derivative engines of the high-order kernel (A/B)
 template <int NQ>
 Dispatch make_dispatch_ho() {
   static_assert(ShapeHO<NQ>::REC == Shape<3, NQ>::REC, "record layout must match");
-  return Dispatch{&launch_sweep_ho<NQ>, ShapeHO<NQ>::REC};
+  const char* v = getenv("ADG_KERNEL");
+  const int var = v ? atoi(v) : 0;
+  if (var == 15) return Dispatch{&launch_sweep_ho<NQ, 0>, ShapeHO<NQ>::REC};
+  if (var == 18) return Dispatch{&launch_sweep_ho<NQ, 1>, ShapeHO<NQ>::REC};
+  if (var == 19) return Dispatch{&launch_sweep_ho<NQ, 2>, ShapeHO<NQ>::REC};
+  // measured (cfg3, one B200): DMMA tiles win at n <= 9 (p=7: 6.55 vs 4.74 / 6.18 TF/s),
+  // the constant-bank lines at n = 10 (p=9: 6.89 vs 6.54 / 2.24 TF/s)
+  return Dispatch{&launch_sweep_ho<NQ, (NQ == 10 ? 1 : 0)>, ShapeHO<NQ>::REC};
 }
 
 template <int NQ, int TS, bool DMMA, bool ROLLED = (NQ == 4), int MB = 0>
@@ -218,6 +228,8 @@ bool dispatch_for(int d, int p, int system, Dispatch* out) {
              : kernel_variant() == 7 ? make_dispatch_v2<4, 1, true, false, 7>()
              : kernel_variant() == 8 ? make_dispatch_v2<4, 1, true, false, 8>()
              : kernel_variant() == 14 ? make_dispatch_v2<4, 1, true, false>()      // axis 1 through shared memory
+             : kernel_variant() == 16 ? make_dispatch_v2<4, 1, true, false, 16>()  // A1S, 8 CTAs/SM
+             : kernel_variant() == 17 ? make_dispatch_v2<4, 1, true, false, 17>()  // A1S, 7 CTAs/SM
              : make_dispatch_v2<4, 1, true, false, 10>();   // default: axis 1 via lane transpose + DMMA
         return true;
       case 5: *out = make_dispatch<3, 5>(); return true;

@@ -15,6 +15,12 @@
 //     of a warp touches every 8-byte bank exactly twice).  At p = 7 (n = 8) the
 //     m8n8k4 tiles fit exactly (no padding); at p = 9, M pads 10 -> 16 and
 //     K 10 -> 12.
+//   * derivative engines (template LN): DMMA tiles (default, n <= 9), or one
+//     line per thread with diff from the constant bank (n = 10: no M/K
+//     padding; measured 6.89 vs 6.54 TF/s at p = 9), or lane groups with
+//     diff rows in registers (A/B only: register pressure at n = 10);
+//   * the time contraction reads each node's divergence history once per
+//     component and forms every time level from registers;
 //   * everything else (Riemann, corrector, calc_time_step, final flux, volume
 //     integral, face traces, s_max) follows sweep_kernel, staged per axis /
 //     per time level through one shared node buffer.
@@ -75,7 +81,31 @@ struct ShapeHO {
   static constexpr size_t SMEM_BYTES = sizeof(double) * TOTAL;
 };
 
-template <int NQ, bool FA = true>
+// One derivative line of axis A on the FP64 pipe: the NQ inputs of the line
+// into registers, out[i] = sum_j diff[i][j] in[j] with diff from the constant
+// bank (kernel parameters), NQ independent accumulators, written back in place.
+template <int NQ, int SA>
+__device__ __forceinline__ void deriv_line(double* ln, const SweepParams& P) {
+  double in[NQ];
+#pragma unroll
+  for (int j = 0; j < NQ; ++j) in[j] = ln[j * SA];
+  double out[NQ];
+#pragma unroll
+  for (int i = 0; i < NQ; ++i) {
+    double s = P.ops.diff[i][0] * in[0];
+#pragma unroll
+    for (int j = 1; j < NQ; ++j) s = fma(P.ops.diff[i][j], in[j], s);
+    out[i] = s;
+  }
+#pragma unroll
+  for (int i = 0; i < NQ; ++i) ln[i * SA] = out[i];
+}
+
+// LN (derivative engine): 0 = m8n8k4 DMMA tiles (padded to 16 x 12 at n = 10);
+// 1 = one line per thread, diff from the constant bank; 2 = a line per group of
+// ceil(n/2) lanes, each lane two outputs with its two diff rows in registers,
+// the line's inputs broadcast to the group (DFMA-bound, no padding waste).
+template <int NQ, bool FA = true, int LN = 0>
 __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
   using S = ShapeHO<NQ, FA>;
   constexpr int DIM = 3, M = 5, NS = S::NS, NF = S::NF, NPT = S::NPT, REC = S::REC;
@@ -266,6 +296,16 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
         afr[mt][kc] = (ii < NQ && jj < NQ) ? P.ops.diff[ii][jj] : 0.0;
       }
   }
+  // LN 2: this lane's two output rows of diff (rows >= NQ are zero dummies)
+  constexpr int TPL = (NQ + 1) / 2;          // lanes per line
+  constexpr int LPW = 32 / TPL;              // lines per warp task
+  const int lrow = 2 * (lane % TPL);
+  double drw0[NQ], drw1[NQ];
+#pragma unroll
+  for (int j = 0; j < NQ; ++j) {
+    drw0[j] = (LN == 2 && lrow < NQ) ? P.ops.diff[lrow][j] : 0.0;
+    drw1[j] = (LN == 2 && lrow + 1 < NQ) ? P.ops.diff[lrow + 1][j] : 0.0;
+  }
   // GEMM column offsets: column r = c*NF + (ib*NQ + ic) of axis a -> padded address
   // of (c, i_a = 0, ib, ic); padded columns clamp to the last real column
   for (int e = tid; e < 3 * S::RP; e += THREADS) {
@@ -308,7 +348,41 @@ if constexpr (FA) {
             for (int c = 0; c < M; ++c) sFA[a * S::R_FA + c * SC + pn[n]] = F[n][a][c];
         }
         __syncthreads();
-        // every GEMM tile of the slice: item = (axis, n-tile); outputs overwrite their inputs
+        if constexpr (LN == 2) {
+          // warp task = LPW lines of the slice (any axis); lane group g owns line
+          // task*LPW + g, lane r of the group outputs rows 2r, 2r+1; outputs
+          // overwrite the line after the whole warp has read its inputs
+          constexpr int NTASK = (DIM * RR + LPW - 1) / LPW;
+          const int g = lane / TPL;
+          for (int task = warp; task < NTASK; task += NW) {
+            const int l = task * LPW + g;
+            const bool lv = (g < LPW) && (l < DIM * RR);
+            const int a = (l >= 2 * RR) ? 2 : (l >= RR) ? 1 : 0;
+            const int sa = (a == 0) ? P0 : (a == 1) ? P1 : 1;
+            double* ln = sFA + a * S::R_FA + (lv ? sTab[a * S::RP + l - a * RR] : 0);
+            double o0 = 0.0, o1 = 0.0;
+#pragma unroll
+            for (int j = 0; j < NQ; ++j) {
+              const double v = ln[j * sa];
+              o0 = fma(drw0[j], v, o0);
+              o1 = fma(drw1[j], v, o1);
+            }
+            __syncwarp();
+            if (lv) {
+              ln[lrow * sa] = o0;
+              if (lrow + 1 < NQ) ln[(lrow + 1) * sa] = o1;
+            }
+            __syncwarp();
+          }
+        } else if constexpr (LN == 1) {
+          // every derivative line of the slice: l = (axis, column); a line's outputs
+          // overwrite its inputs (lines are disjoint)
+          for (int l = tid; l < DIM * RR; l += THREADS) {
+            if (l < RR) deriv_line<NQ, P0>(sFA + sTab[l], P);
+            else if (l < 2 * RR) deriv_line<NQ, P1>(sFA + S::R_FA + sTab[S::RP + l - RR], P);
+            else deriv_line<NQ, 1>(sFA + 2 * S::R_FA + sTab[2 * S::RP + l - 2 * RR], P);
+          }
+        } else
         for (int item = warp; item < DIM * NT; item += NW) {
           const int a = item / NT, nt = item - a * NT;
           const int sa = (a == 0) ? P0 : (a == 1) ? P1 : 1;
@@ -405,6 +479,10 @@ if constexpr (FA) {
     }
     // time contraction + Picard update per node
     double dmax = 0.0, dsum = 0.0;
+#ifndef ADG_HO_CR
+#define ADG_HO_CR 1
+#endif
+#if ADG_HO_CR == 0
 #pragma unroll
     for (int n = 0; n < NPT; ++n) {
 #pragma unroll 1
@@ -422,6 +500,29 @@ if constexpr (FA) {
         }
       }
     }
+#else
+#pragma unroll
+    for (int n = 0; n < NPT; ++n) {
+#pragma unroll 1
+      for (int c = 0; c < M; ++c) {
+        // the divergence history of (n, c) is read once; every time level from registers
+        double dk[NQ];
+#pragma unroll
+        for (int k = 0; k < NQ; ++k) dk[k] = dhp(n, k, c);
+#pragma unroll
+        for (int t = 0; t < NQ; ++t) {
+          double acc = 0.0;
+#pragma unroll
+          for (int k = 0; k < NQ; ++k) acc = fma(P.ops.integ[t][k], dk[k], acc);
+          const double qn = Qx[n][c] - scale * acc;
+          const double qold = (it == 0) ? Qx[n][c] : qo[n][t][c];
+          const double dd = fabs(qn - qold);
+          if (an[n]) { dmax = fmax(dmax, dd); dsum += dd; }
+          qo[n][t][c] = qn;
+        }
+      }
+    }
+#endif
     iters = it + 1;
     if (__syncthreads_or(!finite(dsum))) { failed = true; break; }
     const double delta = block_max<NW>(dmax, sRed);

@@ -43,8 +43,10 @@ struct ShapeV2 {
   static constexpr int TH = NQ / TS;
   // CTAs/SM the register allocation must allow (TS = 1 at NQ = 6 keeps 60 doubles of Picard state)
   // MINB_OVERRIDE 10: axis-1 derivative on the tensor cores through a lane transpose (A1S)
-  static constexpr bool A1S = (MINB_OVERRIDE == 10);
-  static constexpr int MINB = (MINB_OVERRIDE && MINB_OVERRIDE != 9 && !A1S) ? MINB_OVERRIDE : (MINB_OVERRIDE == 9) ? 1
+  // MINB_OVERRIDE 16 / 17: A1S with 8 / 7 CTAs per SM forced (<= 128 / 144 registers)
+  static constexpr bool A1S = (MINB_OVERRIDE == 10 || MINB_OVERRIDE == 16 || MINB_OVERRIDE == 17);
+  static constexpr int MINB = (MINB_OVERRIDE == 16) ? 8 : (MINB_OVERRIDE == 17) ? 7
+                            : (MINB_OVERRIDE && MINB_OVERRIDE != 9 && !A1S) ? MINB_OVERRIDE : (MINB_OVERRIDE == 9) ? 1
                             : (TS == 1 && NQ >= 6) ? 1
                             : THREADS <= 64 ? 6 : THREADS <= 128 ? 4 : (THREADS <= 256 ? 2 : 1);
   static constexpr int P0 = NQ * NQ + plane_pad(NQ);   // padded axis-0 plane stride
