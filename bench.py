@@ -349,9 +349,14 @@ def main():
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             for _ in range(n):
-                h.call("adg_load_state", ptr, n_state)       # H2D of the step's input state
-                drv.enqueue_step()
-                h.call("adg_store_state", ptr, n_state)      # D2H of the step's result (synchronous)
+                if world == 1:
+                    # H2D of the step's input, the step, D2H of its result, pipelined
+                    # over plane chunks inside one C-ABI call (adg_step_host)
+                    h.call("adg_step_host", ptr, ptr, None)
+                else:
+                    h.call("adg_load_state", ptr, n_state)   # H2D of the step's input state
+                    drv.enqueue_step()
+                    h.call("adg_store_state", ptr, n_state)  # D2H of the step's result (synchronous)
             t1 = time.perf_counter()
             barrier()
             e2e_s += t1 - t0
@@ -362,7 +367,9 @@ def main():
         e2e = {"value": dofs * K / e2e_s, "unit": "DoF-updates/s",
                "h2d_bytes_per_step": 8 * n_state * world, "d2h_bytes_per_step": 8 * n_state * world,
                "ms_per_step": 1e3 * e2e_s / K,
-               "path": "adg_load_state (pinned H2D) + phase step + adg_store_state (D2H), per step"}
+               "path": ("adg_step_host: pinned H2D + fused step + D2H per step, pipelined over "
+                        "9 plane chunks" if world == 1 else
+                        "adg_load_state (pinned H2D) + phase step + adg_store_state (D2H), per step")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

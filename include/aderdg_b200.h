@@ -186,6 +186,14 @@ typedef enum { ADG_PART_ALL = 0, ADG_PART_INTERIOR = 1, ADG_PART_BOUNDARY = 2 } 
 adg_status adg_phase_sweep_part(adg_handle* h, int part);
 int        adg_trace_parity(const adg_handle* h); /* parity the next sweep reads      */
 
+/* Driver.step with the state in host memory: uploads Q_in, advances one
+ * realisation step (fused driver, one slab), downloads the result into Q_out
+ * (both [cells][nodes][m]; Q_in == Q_out allowed; pin them for overlap).  The
+ * H2D, the sweep and the D2H are pipelined over chunks of cell planes, so the
+ * transfers overlap the compute (a step with the priming sweep or a rerun
+ * uploads all of Q first).  Synchronous at return. */
+adg_status adg_step_host(adg_handle* h, const double* Q_in, double* Q_out, adg_step_record* out);
+
 /* Timing helpers for bench.py: launches on the handle's stream. */
 adg_status adg_flush_l2(adg_handle* h);
 /* Enqueue `steps` realisation steps (single GPU) with CUDA events around the

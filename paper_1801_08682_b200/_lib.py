@@ -31,6 +31,7 @@ EXPORTS = (
     "adg_phase_seed_finish", "adg_phase_rerun", "adg_phase_sweep",
     "adg_phase_finish", "adg_trace_parity", "adg_flush_l2", "adg_reset", "adg_set_dt_new",
     "adg_run_timed", "adg_phase_sweep_part", "adg_set_limiter", "adg_troubled_flags",
+    "adg_step_host",
 )
 
 
@@ -115,6 +116,7 @@ def load_library(path=None):
                                            ctypes.POINTER(ctypes.c_int),
                                            ctypes.POINTER(ctypes.c_longlong), ctypes.c_double]),
         "adg_troubled_flags": (ctypes.c_int, [H, ctypes.POINTER(ctypes.c_ubyte), ctypes.c_size_t]),
+        "adg_step_host": (ctypes.c_int, [H, dp, dp, ctypes.POINTER(AdgStepRecord)]),
         "adg_phase_finish": (ctypes.c_int, [H]),
         "adg_trace_parity": (ctypes.c_int, [H]),
         "adg_flush_l2": (ctypes.c_int, [H]),

@@ -52,17 +52,38 @@ void launch_sweep_v2(const SweepParams& P, unsigned grid, cudaStream_t s) {
   sweep_kernel_v2<NQ, TS, DMMA, ROLLED, MB><<<grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
 }
 
+typedef int (*occupancy_fn)();
+
+// resident CTAs per SM of a kernel with the given block and dynamic shared memory
+template <class K>
+int occupancy_of(K kernel, int threads, size_t smem) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem) != cudaSuccess) n = 1;
+  return n > 0 ? n : 1;
+}
+
+template <class PDE, int DIM, int NQ>
+int occ_generic() {
+  using S = Shape<DIM, NQ, PDE::M>;
+  return occupancy_of(sweep_kernel<PDE, DIM, NQ>, S::THREADS, S::SMEM_BYTES);
+}
+
 struct Dispatch {
   launch_fn sweep;
   int rec;
+  occupancy_fn occ = nullptr;   // resident sweep CTAs per SM (adg_step_host chunking)
 };
 
 template <int DIM, int NQ>
-Dispatch make_dispatch() { return Dispatch{&launch_sweep<EulerPDE<DIM>, DIM, NQ>, Shape<DIM, NQ>::REC}; }
+Dispatch make_dispatch() {
+  return Dispatch{&launch_sweep<EulerPDE<DIM>, DIM, NQ>, Shape<DIM, NQ>::REC, &occ_generic<EulerPDE<DIM>, DIM, NQ>};
+}
 
 template <int DIM, int NQ>
 Dispatch make_dispatch_adv() {
-  return Dispatch{&launch_sweep<AdvectionPDE<DIM>, DIM, NQ>, Shape<DIM, NQ, 1>::REC};
+  return Dispatch{&launch_sweep<AdvectionPDE<DIM>, DIM, NQ>, Shape<DIM, NQ, 1>::REC,
+                  &occ_generic<AdvectionPDE<DIM>, DIM, NQ>};
 }
 
 // AdvectionSystem: the generic kernel with the advection plug-in, every d and p
@@ -117,23 +138,35 @@ Dispatch make_dispatch_st() {
 
 // ADG_KERNEL=15 / 18 / 19: DMMA-tile / constant-bank line / lane-group line
 // derivative engines of the high-order kernel (A/B)
+template <int NQ, int LN>
+int occ_ho() {
+  return occupancy_of(sweep_kernel_ho<NQ, true, LN>, ShapeHO<NQ>::THREADS, ShapeHO<NQ>::SMEM_BYTES);
+}
+
 template <int NQ>
 Dispatch make_dispatch_ho() {
   static_assert(ShapeHO<NQ>::REC == Shape<3, NQ>::REC, "record layout must match");
   const char* v = getenv("ADG_KERNEL");
   const int var = v ? atoi(v) : 0;
-  if (var == 15) return Dispatch{&launch_sweep_ho<NQ, 0>, ShapeHO<NQ>::REC};
-  if (var == 18) return Dispatch{&launch_sweep_ho<NQ, 1>, ShapeHO<NQ>::REC};
-  if (var == 19) return Dispatch{&launch_sweep_ho<NQ, 2>, ShapeHO<NQ>::REC};
+  if (var == 15) return Dispatch{&launch_sweep_ho<NQ, 0>, ShapeHO<NQ>::REC, &occ_ho<NQ, 0>};
+  if (var == 18) return Dispatch{&launch_sweep_ho<NQ, 1>, ShapeHO<NQ>::REC, &occ_ho<NQ, 1>};
+  if (var == 19) return Dispatch{&launch_sweep_ho<NQ, 2>, ShapeHO<NQ>::REC, &occ_ho<NQ, 2>};
   // measured (cfg3, one B200): DMMA tiles win at n <= 9 (p=7: 6.55 vs 4.74 / 6.18 TF/s),
   // the constant-bank lines at n = 10 (p=9: 6.89 vs 6.54 / 2.24 TF/s)
-  return Dispatch{&launch_sweep_ho<NQ, (NQ == 10 ? 1 : 0)>, ShapeHO<NQ>::REC};
+  return Dispatch{&launch_sweep_ho<NQ, (NQ == 10 ? 1 : 0)>, ShapeHO<NQ>::REC, &occ_ho<NQ, (NQ == 10 ? 1 : 0)>};
+}
+
+template <int NQ, int TS, bool DMMA, bool ROLLED, int MB>
+int occ_v2() {
+  using S = ShapeV2<NQ, TS, DMMA, ROLLED, MB>;
+  return occupancy_of(sweep_kernel_v2<NQ, TS, DMMA, ROLLED, MB>, S::THREADS, S::SMEM_BYTES);
 }
 
 template <int NQ, int TS, bool DMMA, bool ROLLED = (NQ == 4), int MB = 0>
 Dispatch make_dispatch_v2() {
   static_assert(ShapeV2<NQ, TS, DMMA, ROLLED, MB>::REC == Shape<3, NQ>::REC, "record layout must match");
-  return Dispatch{&launch_sweep_v2<NQ, TS, DMMA, ROLLED, MB>, ShapeV2<NQ, TS, DMMA, ROLLED, MB>::REC};
+  return Dispatch{&launch_sweep_v2<NQ, TS, DMMA, ROLLED, MB>, ShapeV2<NQ, TS, DMMA, ROLLED, MB>::REC,
+                  &occ_v2<NQ, TS, DMMA, ROLLED, MB>};
 }
 
 
@@ -272,6 +305,7 @@ struct adg_handle {
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
   int sweep_index = 0;       // index of the next regular sweep (0 = priming)
+  int disp_ctas_per_sm = 0;  // resident sweep CTAs per SM (adg_step_host chunking)
   bool seeded = false;
   bool loaded = false;
   int host_steps = 0;        // steps whose records were fetched
@@ -295,7 +329,15 @@ struct adg_handle {
   unsigned lim_grid = 0;
   size_t lim_detect_smem = 0;
   double lim_cfl = 0.9;
+  // adg_step_host: copy streams and per-chunk events
+  cudaStream_t copy_in = nullptr, copy_out = nullptr;
+  std::vector<cudaEvent_t> chunk_ev;
+  StepRecord* rec_host = nullptr;      // pinned landing slot of the step record
+  bool hst_fresh = false;              // hst mirrors the device (no phase call since the last pull)
 };
+
+constexpr int ADG_HOST_CHUNKS = 9;       // plane chunks of the pipelined host step (ADG_HOST_CHUNKS env)
+constexpr int ADG_HOST_CHUNKS_MAX = 81;
 
 static adg_status fail(adg_handle* h, adg_status code, const std::string& msg) {
   if (h) h->err = msg;
@@ -450,6 +492,7 @@ static adg_status launch_finish(adg_handle* h, int priming, int seed) {
 static adg_status pull_state(adg_handle* h) {
   CUDA_TRY(h, cudaMemcpyAsync(&h->hst, h->st, sizeof(DevState), cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  h->hst_fresh = true;
   return ADG_OK;
 }
 
@@ -564,6 +607,10 @@ void adg_destroy(adg_handle* h) {
                       h->lim_prev[1], h->lim_troubled, h->lim_list, h->lim_lam, h->lim_scratch};
   for (void* b : lim_bufs)
     if (b) cudaFree(b);
+  for (cudaEvent_t e : h->chunk_ev) cudaEventDestroy(e);
+  if (h->copy_in) cudaStreamDestroy(h->copy_in);
+  if (h->rec_host) cudaFreeHost(h->rec_host);
+  if (h->copy_out) cudaStreamDestroy(h->copy_out);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   delete h;
 }
@@ -646,6 +693,7 @@ adg_status adg_store_state(adg_handle* h, double* Q, size_t n) {
 
 adg_status adg_phase_seed(adg_handle* h) {
   if (!h) return ADG_ERR_CONFIG;
+  h->hst_fresh = false;
   if (!h->ops_set) return fail(h, ADG_ERR_CONFIG, "operators not set");
   if (!h->loaded) return fail(h, ADG_ERR_CONFIG, "state not loaded");
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
@@ -673,6 +721,7 @@ static bool straightforward(const adg_handle* h) { return h->cfg.driver_mode == 
 
 adg_status adg_phase_rerun(adg_handle* h) {
   if (!h) return ADG_ERR_CONFIG;
+  h->hst_fresh = false;
   if (straightforward(h)) {                     // the prediction sweep of the step
     if (!h->seeded) return fail(h, ADG_ERR_CONFIG, "time control not seeded");
     return launch(h, MODE_SF_PREDICT);
@@ -683,6 +732,7 @@ adg_status adg_phase_rerun(adg_handle* h) {
 
 adg_status adg_phase_sweep_part(adg_handle* h, int part) {
   if (!h) return ADG_ERR_CONFIG;
+  h->hst_fresh = false;
   if (!h->seeded) return fail(h, ADG_ERR_CONFIG, "time control not seeded");
   if (straightforward(h)) {
     adg_status s = launch(h, MODE_SF_CORRECT, part);
@@ -698,6 +748,7 @@ adg_status adg_phase_sweep(adg_handle* h) { return adg_phase_sweep_part(h, ADG_P
 
 adg_status adg_phase_finish(adg_handle* h) {
   if (!h) return ADG_ERR_CONFIG;
+  h->hst_fresh = false;
   adg_status s = launch_finish(h, (!straightforward(h) && h->sweep_index == 0) ? 1 : 0, 0);
   h->sweep_index += 1;
   return s;
@@ -987,6 +1038,125 @@ adg_status adg_run_timed(adg_handle* h, int steps, double* out) {
   s = pull_state(h);
   if (s != ADG_OK) return s;
   return status_from_state(h);
+}
+
+// ---------------------------------------------------------------------------
+// One realisation step from host buffers with the transfers pipelined against
+// the sweep (single slab, fused driver).  The cell planes are cut into chunks;
+// per chunk: H2D of its Q (copy-in stream) -> sweep of its cells (compute
+// stream) -> D2H of its Q (copy-out stream).  Without a rerun a cell's sweep
+// reads only its own Q plus device-resident D and face records, so chunk i
+// computes while chunk i+1 lands and chunk i-1 drains.  When the step needs
+// the priming sweep or a rerun (both read every cell's Q; the rerun decision
+// of the previous step is known on the host after its final sync), all of Q
+// is uploaded first and only the D2H is pipelined.
+static adg_status ensure_copy_streams(adg_handle* h) {
+  if (!h->copy_in) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->copy_in, cudaStreamNonBlocking));
+  if (!h->copy_out) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->copy_out, cudaStreamNonBlocking));
+  if (!h->rec_host) CUDA_TRY(h, cudaMallocHost(&h->rec_host, sizeof(StepRecord)));
+  if (h->chunk_ev.empty()) {
+    h->chunk_ev.resize(3 * ADG_HOST_CHUNKS_MAX + 1);
+    for (auto& e : h->chunk_ev) CUDA_TRY(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  return ADG_OK;
+}
+
+static adg_status launch_range(adg_handle* h, int mode, long long first, long long count) {
+  if (count <= 0) return ADG_OK;
+  SweepParams P = sweep_params(h, mode);
+  P.cell_a = (int)first;
+  h->disp.sweep(P, (unsigned)count, h->stream);
+  return cuda_check(h, cudaGetLastError(), "sweep launch");
+}
+
+adg_status adg_step_host(adg_handle* h, const double* Q_in, double* Q_out, adg_step_record* out) {
+  if (!h || !Q_in || !Q_out) return ADG_ERR_CONFIG;
+  if (h->hst.status) return status_from_state(h);
+  if (!h->seeded) return fail(h, ADG_ERR_CONFIG, "time control not seeded");
+  if (straightforward(h) || h->cfg.world != 1 || h->cfg.halo_mode != 0 || h->lim)
+    return fail(h, ADG_ERR_CONFIG, "adg_step_host pipelines the fused single-slab driver");
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  adg_status s = ensure_copy_streams(h);
+  if (s != ADG_OK) return s;
+  if (!h->hst_fresh && (s = pull_state(h)) != ADG_OK) return s;   // rerun decision after phase calls
+  if (h->hst.status) return status_from_state(h);
+  const size_t cell_doubles = (size_t)h->NS * h->m;
+  static const int want = [] {
+    const char* v = getenv("ADG_HOST_CHUNKS");
+    const int c = v ? atoi(v) : ADG_HOST_CHUNKS;
+    return c < 1 ? 1 : (c > ADG_HOST_CHUNKS_MAX ? ADG_HOST_CHUNKS_MAX : c);
+  }();
+  // chunk i = cells [cell_of(i), cell_of(i+1)): boundaries on whole waves of
+  // resident CTAs so the chunked sweep keeps the single launch's wave count
+  const long long C = h->cells_local;
+  long long wave = 0;
+  {
+    int dev_sms = 148, per_sm = 1;
+    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, h->cfg.device);
+    if (h->disp_ctas_per_sm == 0) h->disp_ctas_per_sm = h->disp.occ ? h->disp.occ() : 1;
+    per_sm = h->disp_ctas_per_sm;
+    wave = (long long)dev_sms * per_sm;
+  }
+  long long waves = (C + wave - 1) / wave;
+  const int nch = (int)(waves < want ? waves : want);
+  auto cell_of = [&](int i) {
+    const long long w = waves * i / nch;                 // whole waves per chunk
+    return w * wave < C ? w * wave : C;
+  };
+  cudaEvent_t* ev_in = h->chunk_ev.data();
+  cudaEvent_t* ev_sw = ev_in + ADG_HOST_CHUNKS_MAX;
+  cudaEvent_t ev_start = h->chunk_ev[3 * ADG_HOST_CHUNKS_MAX];
+  const int before = h->hst.step;
+  // the previous call left the compute stream idle; order the copies after it
+  CUDA_TRY(h, cudaEventRecord(ev_start, h->stream));
+  CUDA_TRY(h, cudaStreamWaitEvent(h->copy_in, ev_start, 0));
+  CUDA_TRY(h, cudaStreamWaitEvent(h->copy_out, ev_start, 0));
+  const bool whole = (h->sweep_index == 0) || h->hst.rerun_next;
+  if (whole) {
+    // priming and / or rerun read every cell's Q: upload all of it first
+    CUDA_TRY(h, cudaMemcpyAsync(h->Q, Q_in, sizeof(double) * cell_doubles * h->cells_local,
+                                cudaMemcpyHostToDevice, h->stream));
+    if (h->sweep_index == 0) {
+      if ((s = adg_phase_sweep(h)) != ADG_OK) return s;
+      if ((s = adg_phase_finish(h)) != ADG_OK) return s;
+    }
+    if ((s = adg_phase_rerun(h)) != ADG_OK) return s;
+  } else {
+    for (int i = 0; i < nch; ++i) {
+      const size_t off = (size_t)cell_of(i) * cell_doubles;
+      const size_t n = (size_t)(cell_of(i + 1) - cell_of(i)) * cell_doubles;
+      CUDA_TRY(h, cudaMemcpyAsync(h->Q + off, Q_in + off, sizeof(double) * n, cudaMemcpyHostToDevice,
+                                  h->copy_in));
+      CUDA_TRY(h, cudaEventRecord(ev_in[i], h->copy_in));
+    }
+  }
+  const int mode = MODE_NORMAL;
+  for (int i = 0; i < nch; ++i) {
+    const long long c0 = cell_of(i), c1 = cell_of(i + 1);
+    if (!whole) CUDA_TRY(h, cudaStreamWaitEvent(h->stream, ev_in[i], 0));
+    if ((s = launch_range(h, mode, c0, c1 - c0)) != ADG_OK) return s;
+    CUDA_TRY(h, cudaEventRecord(ev_sw[i], h->stream));
+    CUDA_TRY(h, cudaStreamWaitEvent(h->copy_out, ev_sw[i], 0));
+    CUDA_TRY(h, cudaMemcpyAsync(Q_out + c0 * cell_doubles, h->Q + c0 * cell_doubles,
+                                sizeof(double) * (size_t)(c1 - c0) * cell_doubles, cudaMemcpyDeviceToHost,
+                                h->copy_out));
+  }
+  if ((s = adg_phase_finish(h)) != ADG_OK) return s;
+  // one sync for the state, the step record and the last chunk
+  CUDA_TRY(h, cudaMemcpyAsync(&h->hst, h->st, sizeof(DevState), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(h, cudaMemcpyAsync(h->rec_host, h->recs + (before % h->rec_cap), sizeof(StepRecord),
+                              cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->copy_out));
+  h->hst_fresh = true;
+  if ((s = status_from_state(h)) != ADG_OK) return s;
+  if (out && h->hst.step == before + 1) {
+    const StepRecord& r = *h->rec_host;
+    out->step = r.step; out->reruns = r.reruns; out->T = r.T; out->dt_old = r.dt_old;
+    out->dt_new = r.dt_new; out->dt_adm = r.dt_adm; out->picard_iters = r.picard_iters;
+    out->predicts = r.predicts; out->troubled = r.troubled;
+  }
+  return ADG_OK;
 }
 
 adg_status adg_flush_l2(adg_handle* h) {

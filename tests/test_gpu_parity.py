@@ -269,3 +269,31 @@ def test_gpu_straightforward_final_time(cuda_ok):
     drv = Driver(grid, kern, TimeControl(), "straightforward", host_sync="run")
     drv.run(final_time=0.05)
     assert abs(drv.tc.T - 0.05) < 1e-14
+
+
+@pytest.mark.parametrize("d,L,p,steps,kw", [(3, 2, 3, 6, {}), (3, 2, 3, 4, {"inject_rerun": True}),
+                                           (3, 1, 5, 4, {}), (2, 3, 3, 8, {}),
+                                           (3, 2, 3, 8, {"spike_step": 3})])
+def test_step_host_pipeline_equals_device_run(cuda_ok, d, L, p, steps, kw):
+    """adg_step_host (H2D / sweep / D2H pipelined over plane chunks, rerun and
+    priming steps through the whole-upload path) gives the adg_run state, step
+    records and counters bitwise."""
+    import ctypes
+    from paper_1801_08682_b200 import _lib
+    Q0 = scenarios.build("bump", d, L, p, seed=4, noise=1e-2)
+    a = make_driver(Q0, d, L, p, kw, host_sync="manual")
+    Qh = np.ascontiguousarray(Q0.copy())
+    recs = []
+    for _ in range(steps):
+        r = _lib.AdgStepRecord()
+        a.handle.call("adg_step_host", _lib.dptr(Qh), _lib.dptr(Qh), ctypes.byref(r))
+        recs.append((r.step, r.reruns, r.T, r.dt_old, r.dt_new, r.dt_adm, r.picard_iters))
+    b = make_driver(Q0, d, L, p, kw, host_sync="run")
+    b.run(steps=steps)
+    assert np.array_equal(Qh, b.grid.Q)
+    ref = [(r["step"], r["reruns"], r["T"], r["dt_old"], r["dt_new"], r["dt_adm"], r["picard_iters"])
+           for r in b.step_records]
+    assert recs == ref
+    lib = a.handle.lib
+    assert lib.adg_sweep_count(a.handle.h) == b.sweep_count
+    assert lib.adg_rerun_count(a.handle.h) == b.rerun_count
