@@ -223,10 +223,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # ADG_BENCH_GLOO=1: every rank on cuda:0 with host-staged gloo transport -- a
+    # functional check of the multi-rank code path on a one-GPU box (no timing claim)
+    staged = os.environ.get("ADG_BENCH_GLOO") == "1" and world > 1
+    if staged:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if staged:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     d, L, p = cfgd["d"], cfgd["L"], cfgd["p"]
     cells = 3 ** (d * L)
     dofs = roofline.dof(d, p, cells)
@@ -239,7 +247,7 @@ def main():
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if staged else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -250,7 +258,7 @@ def main():
     # segments.  Default K + W = E: one episode, the first W steps (incl. the
     # priming sweep) untimed.
     E = cfgd["steps"]
-    drv = SlabDriver(Q0, d, L, p, rank, world, local, mode=args.mode)
+    drv = SlabDriver(Q0, d, L, p, rank, world, local, mode=args.mode, staged=staged)
     h = drv.handle
     K = args.steps
     clocks = ClockSampler(local)
@@ -289,13 +297,17 @@ def main():
                 time.sleep(0.05)
             start.record()
             for i in range(n):
+                # rerun -> { halo exchange (NCCL stream) || interior planes } -> boundary
+                # planes -> all-reduce -> time control (parallel.SlabDriver.enqueue_step)
                 e0, e1, e2, e3 = ev[i]
                 e0.record()
                 h.call("adg_phase_rerun")
                 e1.record()
-                drv.halo.exchange(drv.tr[h.lib.adg_trace_parity(h.h)])
+                pending = drv.halo.start(drv.tr[h.lib.adg_trace_parity(h.h)])
                 e2.record()
-                h.call("adg_phase_sweep")
+                h.call("adg_phase_sweep_part", _lib.ADG_PART_INTERIOR)
+                drv.halo.wait(pending)
+                h.call("adg_phase_sweep_part", _lib.ADG_PART_BOUNDARY)
                 e3.record()
                 drv.halo.reduce(drv.red)
                 h.call("adg_phase_finish")
