@@ -262,6 +262,7 @@ bool dispatch_for(int d, int p, int system, Dispatch* out) {
              : kernel_variant() == 8 ? make_dispatch_v2<4, 1, true, false, 8>()
              : kernel_variant() == 14 ? make_dispatch_v2<4, 1, true, false>()      // axis 1 through shared memory
              : kernel_variant() == 16 ? make_dispatch_v2<4, 1, true, false, 16>()  // A1S, 8 CTAs/SM
+             : kernel_variant() == 20 ? make_dispatch_v2<4, 1, true, false, 20>()  // A1S + axis-0 partial sums
              : kernel_variant() == 17 ? make_dispatch_v2<4, 1, true, false, 17>()  // A1S, 7 CTAs/SM
              : make_dispatch_v2<4, 1, true, false, 10>();   // default: axis 1 via lane transpose + DMMA
         return true;

@@ -44,8 +44,13 @@ struct ShapeV2 {
   // CTAs/SM the register allocation must allow (TS = 1 at NQ = 6 keeps 60 doubles of Picard state)
   // MINB_OVERRIDE 10: axis-1 derivative on the tensor cores through a lane transpose (A1S)
   // MINB_OVERRIDE 16 / 17: A1S with 8 / 7 CTAs per SM forced (<= 128 / 144 registers)
-  static constexpr bool A1S = (MINB_OVERRIDE == 10 || MINB_OVERRIDE == 16 || MINB_OVERRIDE == 17);
-  static constexpr int MINB = (MINB_OVERRIDE == 16) ? 8 : (MINB_OVERRIDE == 17) ? 7
+  // MINB_OVERRIDE 20: A1S + A0X (axis 0 from per-warp partial sums: the warp of
+  // planes {2w, 2w+1} contracts its own two planes for its nodes and for the other
+  // warp's nodes; one shuffle, one store and one load per component replace the
+  // four-plane shared-memory gather)
+  static constexpr bool A0X = (MINB_OVERRIDE == 20);
+  static constexpr bool A1S = (MINB_OVERRIDE == 10 || MINB_OVERRIDE == 16 || MINB_OVERRIDE == 17 || A0X);
+  static constexpr int MINB = (MINB_OVERRIDE == 16) ? 8 : (MINB_OVERRIDE == 17) ? 7 : A0X ? 6
                             : (MINB_OVERRIDE && MINB_OVERRIDE != 9 && !A1S) ? MINB_OVERRIDE : (MINB_OVERRIDE == 9) ? 1
                             : (TS == 1 && NQ >= 6) ? 1
                             : THREADS <= 64 ? 6 : THREADS <= 128 ? 4 : (THREADS <= 256 ? 2 : 1);
@@ -81,6 +86,7 @@ struct ShapeV2 {
   static_assert(NQ % TS == 0, "time split must divide NQ");
   static_assert(!DMMA || NQ == 4, "DMMA axis-2 path needs i2 in lane bits 0-1");
   static_assert(!A1S || (DMMA && TS == 1 && DBUF), "A1S runs in the double-buffered DMMA slice loop");
+  static_assert(!A0X || (NQ == 4 && THREADS == 64), "A0X pairs the two warps of a p = 3 cell");
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -245,6 +251,18 @@ sweep_kernel_v2(const SweepParams P) {
   // in lane sigma(owner), so one shuffle in and one out replace the axis-1
   // shared-memory gather.
   const int sig = (tid & 16) | ((tid & 3) << 2) | ((tid >> 2) & 3);
+  // A0X (NQ = 4, 64 threads): warp w holds planes i0 = 2w + (lane bit 4); the
+  // partner lane (lane ^ 16) holds the other plane of the same (i1, i2) line.
+  // cl/ch: my output row on the warp's low / high plane; ol/oh: the row of the
+  // node in the other warp with the same lane (i0 ^ 2)
+  double a0_cl = 0.0, a0_ch = 0.0, a0_ol = 0.0, a0_oh = 0.0;
+  if (S::A0X) {
+    const int w2 = 2 * (tid >> 5);
+    a0_cl = P.ops.diff[i0][w2];
+    a0_ch = P.ops.diff[i0][w2 + 1];
+    a0_ol = P.ops.diff[i0 ^ 2][w2];
+    a0_oh = P.ops.diff[i0 ^ 2][w2 + 1];
+  }
   // padded gather bases for the shared-memory axes
   int gbase[DIM], gstr[DIM];
   gbase[0] = px - i0 * P0; gstr[0] = P0;
@@ -494,7 +512,19 @@ sweep_kernel_v2(const SweepParams P) {
       double* sFs = (TS == 1 && S::DBUF) ? sF + (k & 1) * (DS * M * PS) : sFt;
       double F[DIM][M];
       flux<DIM>(q[s], F);
-      if (act) {
+      double own0[M];                            // A0X: this warp's two planes, my row
+      if (S::A0X) {
+        const bool hi = (tid & 16) != 0;         // my plane is the warp's high plane
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          const double pf = __shfl_xor_sync(0xffffffffu, F[0][c], 16);
+          const double flo = hi ? pf : F[0][c], fhi = hi ? F[0][c] : pf;
+          own0[c] = fma(a0_ch, fhi, a0_cl * flo);
+          // the other warp's node on this lane: its row (i0 ^ 2) over my two planes
+          sFs[c * NSP + (tid ^ 32)] = fma(a0_oh, fhi, a0_ol * flo);
+        }
+      }
+      if (act && !S::A0X) {
 #pragma unroll
         for (int a = 0; a < DS; ++a)
 #pragma unroll
@@ -526,7 +556,9 @@ sweep_kernel_v2(const SweepParams P) {
 #pragma unroll
         for (int a = 0; a < DS; ++a) {
           double v = 0.0;
-          if (S::F1T && a == 1) {
+          if (S::A0X && a == 0) {
+            v = own0[c] + sFs[c * NSP + tid];    // + the other warp's two planes
+          } else if (S::F1T && a == 1) {
             const double2* b2 = reinterpret_cast<const double2*>(sFs + (a * M + c) * PS + g1t);
 #pragma unroll
             for (int jj = 0; jj < NQ / 2; ++jj) {
