@@ -271,7 +271,9 @@ bool dispatch_for(int d, int p, int system, Dispatch* out) {
         *out = kernel_variant() == 1 ? make_dispatch<3, 6>()
              : kernel_variant() == 2 ? make_dispatch_v2<6, 2, false>()
              : kernel_variant() == 9 ? make_dispatch_v2<6, 1, false, false, 9>()
-             : kernel_variant() == 12 ? make_dispatch_ho<6>() : make_dispatch_v2<6, 1, false>();
+             : kernel_variant() == 12 ? make_dispatch_ho<6>()
+             : kernel_variant() == 30 ? make_dispatch_v2<6, 1, false, false, 30>()   // pencil Picard loop
+             : make_dispatch_v2<6, 1, false>();
         return true;
       // p >= 6: time line in local memory, spatial derivatives as DMMA GEMMs
       case 7: *out = kernel_variant() == 1 ? make_dispatch<3, 7>() : make_dispatch_ho<7>(); return true;

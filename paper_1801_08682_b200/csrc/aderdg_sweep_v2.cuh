@@ -48,9 +48,13 @@ struct ShapeV2 {
   // planes {2w, 2w+1} contracts its own two planes for its nodes and for the other
   // warp's nodes; one shuffle, one store and one load per component replace the
   // four-plane shared-memory gather)
+  // MINB_OVERRIDE 30 (PEN, NQ = 6): pencil Picard loop — a thread owns one time
+  // level of one i2-pencil (6 nodes); axis 2 is register-local, axes 0/1 and the
+  // time contraction are 16-byte broadcast gathers of whole pencils
+  static constexpr bool PEN = (MINB_OVERRIDE == 30);
   static constexpr bool A0X = (MINB_OVERRIDE == 20);
   static constexpr bool A1S = (MINB_OVERRIDE == 10 || MINB_OVERRIDE == 16 || MINB_OVERRIDE == 17 || A0X);
-  static constexpr int MINB = (MINB_OVERRIDE == 16) ? 8 : (MINB_OVERRIDE == 17) ? 7 : A0X ? 6
+  static constexpr int MINB = PEN ? 1 : (MINB_OVERRIDE == 16) ? 8 : (MINB_OVERRIDE == 17) ? 7 : A0X ? 6
                             : (MINB_OVERRIDE && MINB_OVERRIDE != 9 && !A1S) ? MINB_OVERRIDE : (MINB_OVERRIDE == 9) ? 1
                             : (TS == 1 && NQ >= 6) ? 1
                             : THREADS <= 64 ? 6 : THREADS <= 128 ? 4 : (THREADS <= 256 ? 2 : 1);
@@ -71,7 +75,12 @@ struct ShapeV2 {
   static constexpr int R_FB = DIM * M * PS;            // fbar (after the Picard loop)
   static constexpr int R_DIV = (NQ + 1) * M * NSP;     // divergence of all slices / q slices + qbar
   static constexpr int R_PRED0 = (R_F > R_FB ? R_F : R_FB) + R_DIV;
-  static constexpr int R_PRED = ((ROLL || DBUF) && 2 * R_F > R_PRED0) ? 2 * R_F : R_PRED0;
+  static constexpr int R_PRED1 = ((ROLL || DBUF) && 2 * R_F > R_PRED0) ? 2 * R_F : R_PRED0;
+  // PEN: F0 | F1 | div pencil buffers, row (t, j0, j1) at t*30 + j0*S0 + j1*S1 (strides from a
+  // bank-conflict search over the warp blocks below: every 8-byte gather of a warp hits <= 16
+  // distinct addresses in distinct bank pairs)
+  static constexpr int PB0 = 6 * 1083, PB1 = 6 * 1092, PB2 = 6 * 1083;
+  static constexpr int R_PRED = (PEN && PB0 + PB1 + PB2 > R_PRED1) ? PB0 + PB1 + PB2 : R_PRED1;
   static constexpr int R_U = R_REC > R_PRED ? R_REC : R_PRED;
   static constexpr int R_FACE = 2 * DIM * NF * M;
   static constexpr int OFF_BAR = 0;                    // 2 doubles for the mbarrier
@@ -87,6 +96,8 @@ struct ShapeV2 {
   static_assert(!DMMA || NQ == 4, "DMMA axis-2 path needs i2 in lane bits 0-1");
   static_assert(!A1S || (DMMA && TS == 1 && DBUF), "A1S runs in the double-buffered DMMA slice loop");
   static_assert(!A0X || (NQ == 4 && THREADS == 64), "A0X pairs the two warps of a p = 3 cell");
+  static_assert(!PEN || (NQ == 6 && TS == 1 && !DMMA && NSP == 224), "PEN is the p = 5 pencil layout");
+  static_assert(SMEM_BYTES <= 232448, "shared memory per CTA");
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -395,7 +406,133 @@ sweep_kernel_v2(const SweepParams P) {
   double* sFt = sF + ts * (DS * M * PS);
   int iters = 0;
   bool failed = false;
-  if constexpr (TS == 1 && S::ROLL) {
+  if constexpr (S::PEN) {
+    // Pencil Picard loop (p = 5).  Thread (t, j0, j1) owns time level t of the
+    // i2-pencil (j0, j1, 0..5): 30 contiguous doubles [i2][c], the reference's
+    // node-major layout.  Per iteration: flux of the 6 nodes; the axis-2
+    // derivative from registers; F_0 / F_1 pencils to shared memory; the axis-0
+    // (axis-1) derivative reads the 6 pencils (t, j, j1) ((t, j0, j)) that the
+    // warp's threads sharing (t, j1) ((t, j0)) read too — 8-byte broadcast
+    // gathers; the divergence pencils go back to shared memory and the time
+    // contraction reads the 6 pencils (k, j0, j1) the same way.  Warps are
+    // (t, j0, j1) blocks (2x4x4, 4x4x2, 4x2x4, ...) so each gather instruction
+    // touches <= 16 distinct doubles (one wavefront; 16-byte loads measured
+    // ~4 wavefronts each whatever the broadcast).
+    constexpr int ROW = NQ * M;                         // one pencil: 30 doubles
+    int pt, pj0, pj1;
+    bool pact = true;
+    {
+      const int w = tid >> 5, l = tid & 31;
+      if (w < 3) { pt = 2 * w + (l >> 4); pj0 = (l >> 2) & 3; pj1 = l & 3; }
+      else if (w == 3) { pt = l >> 3; pj0 = (l >> 1) & 3; pj1 = 4 + (l & 1); }
+      else if (w == 4) { pt = l >> 3; pj0 = 4 + (l & 1); pj1 = (l >> 1) & 3; }
+      else if (w == 5) {
+        const int u = l & 15;
+        pt = 4 + (u >> 3);
+        if (l < 16) { pj0 = (u >> 1) & 3; pj1 = 4 + (u & 1); }
+        else { pj0 = 4 + (u & 1); pj1 = (u >> 1) & 3; }
+      } else {
+        pact = l < 24;
+        const int u = pact ? l : 0;
+        pt = u >> 2; pj0 = 4 + ((u >> 1) & 1); pj1 = 4 + (u & 1);
+      }
+    }
+    double* sP0 = sU;                                   // F_0 pencils
+    double* sP1 = sU + S::PB0;                          // F_1 pencils
+    double* sPd = sU + S::PB0 + S::PB1;                 // divergence pencils
+    double* w0 = sP0 + pt * ROW + pj0 * 180 + pj1 * 1083;
+    double* w1 = sP1 + pt * ROW + pj0 * 181 + pj1 * 1092;
+    double* wd = sPd + pt * ROW + pj0 * 180 + pj1 * 1083;
+    const double* r0 = sP0 + pt * ROW + pj1 * 1083;    // + j * 180: rows (t, j, j1)
+    const double* r1 = sP1 + pt * ROW + pj0 * 181;     // + j * 1092: rows (t, j0, j)
+    const double* rd = sPd + pj0 * 180 + pj1 * 1083;   // + k * ROW: rows (k, j0, j1)
+    const double* rq = sQ + (pj0 * NQ + pj1) * ROW;
+    double d0[NQ], d1[NQ], ig[NQ];
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) {
+      d0[j] = P.ops.diff[pj0][j];
+      d1[j] = P.ops.diff[pj1][j];
+      ig[j] = P.ops.integ[pt][j];
+    }
+    double qp[NQ][M];
+#pragma unroll
+    for (int e = 0; e < ROW; ++e) qp[e / M][e % M] = rq[e];
+#pragma unroll 1
+    for (int it = 0; it < cap; ++it) {
+      double dv[NQ][M];
+#pragma unroll
+      for (int o = 0; o < NQ; ++o)
+#pragma unroll
+        for (int c = 0; c < M; ++c) dv[o][c] = 0.0;
+#pragma unroll
+      for (int i2 = 0; i2 < NQ; ++i2) {
+        double F[DIM][M];
+        flux<DIM>(qp[i2], F);
+        if (pact) {
+#pragma unroll
+          for (int c = 0; c < M; ++c) {
+            w0[i2 * M + c] = F[0][c];
+            w1[i2 * M + c] = F[1][c];
+          }
+        }
+#pragma unroll
+        for (int o = 0; o < NQ; ++o)
+#pragma unroll
+          for (int c = 0; c < M; ++c) dv[o][c] = fma(P.ops.diff[o][i2], F[2][c], dv[o][c]);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < NQ; ++j)
+#pragma unroll
+        for (int e = 0; e < ROW; ++e) dv[e / M][e % M] = fma(d0[j], r0[j * 180 + e], dv[e / M][e % M]);
+#pragma unroll
+      for (int j = 0; j < NQ; ++j)
+#pragma unroll
+        for (int e = 0; e < ROW; ++e) dv[e / M][e % M] = fma(d1[j], r1[j * 1092 + e], dv[e / M][e % M]);
+      if (pact) {
+#pragma unroll
+        for (int e = 0; e < ROW; ++e) wd[e] = dv[e / M][e % M];
+      }
+      __syncthreads();
+      // time contraction of the divergence pencils (k = 0..5) + Picard update
+      double acc[NQ][M];
+#pragma unroll
+      for (int k = 0; k < NQ; ++k)
+#pragma unroll
+        for (int e = 0; e < ROW; ++e)
+          acc[e / M][e % M] = (k == 0) ? ig[0] * rd[e] : fma(ig[k], rd[k * ROW + e], acc[e / M][e % M]);
+      bool conv = true;
+      double dsum = 0.0;
+#pragma unroll
+      for (int e = 0; e < ROW; ++e) {
+        const double qn = rq[e] - scale * acc[e / M][e % M];
+        const double dd = fabs(qn - qp[e / M][e % M]);
+        conv = conv && (dd <= tol);
+        dsum += dd;
+        qp[e / M][e % M] = qn;
+      }
+      iters = it + 1;
+      const int fl = block_flags<NW>(!pact || conv, pact && !finite(dsum), sFlags, it & 1);
+      if (fl & 2) { failed = true; break; }
+      if (fl & 1) break;
+    }
+    if (!failed) {
+      // publish the final iterate in the trace layout; continue in the node view
+      double* sQt = sDiv;
+      if (pact) {
+#pragma unroll
+        for (int i2 = 0; i2 < NQ; ++i2)
+#pragma unroll
+          for (int c = 0; c < M; ++c) sQt[(pt * M + c) * NSP + trace_addr<NQ>(pj0, pj1, i2)] = qp[i2][c];
+      }
+      __syncthreads();
+      const int qa = trace_addr<NQ>(i0, i1, i2);
+#pragma unroll
+      for (int s = 0; s < TH; ++s)
+#pragma unroll
+        for (int c = 0; c < M; ++c) q[s][c] = sQt[(s * M + c) * NSP + qa];
+    }
+  } else if constexpr (TS == 1 && S::ROLL) {
     // Rolled slice loop (keeps the Picard loop inside the instruction cache):
     // each trip processes RR slices from register slots 0..RR-1, then the
     // time line rotates by RR slots (back in order after NQ slices).
