@@ -478,7 +478,7 @@ if constexpr (FA) {
 
     }
     // time contraction + Picard update per node
-    double dmax = 0.0, dsum = 0.0;
+    BitMax bm;
 #ifndef ADG_HO_CR
 #define ADG_HO_CR 1
 #endif
@@ -495,7 +495,7 @@ if constexpr (FA) {
           const double qn = Qx[n][c] - scale * acc;
           const double qold = (it == 0) ? Qx[n][c] : qo[n][t][c];
           const double dd = fabs(qn - qold);
-          if (an[n]) { dmax = fmax(dmax, dd); dsum += dd; }
+          if (an[n]) bm.add(dd);
           qo[n][t][c] = qn;
         }
       }
@@ -517,15 +517,15 @@ if constexpr (FA) {
           const double qn = Qx[n][c] - scale * acc;
           const double qold = (it == 0) ? Qx[n][c] : qo[n][t][c];
           const double dd = fabs(qn - qold);
-          if (an[n]) { dmax = fmax(dmax, dd); dsum += dd; }
+          if (an[n]) bm.add(dd);
           qo[n][t][c] = qn;
         }
       }
     }
 #endif
     iters = it + 1;
-    if (__syncthreads_or(!finite(dsum))) { failed = true; break; }
-    const double delta = block_max<NW>(dmax, sRed);
+    if (__syncthreads_or(bm.bad())) { failed = true; break; }
+    const double delta = block_max<NW>(__longlong_as_double((long long)bm.m), sRed);
     if (delta <= tol) break;
   }
 

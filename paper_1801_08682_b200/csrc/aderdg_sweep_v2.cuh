@@ -501,18 +501,15 @@ sweep_kernel_v2(const SweepParams P) {
 #pragma unroll
         for (int e = 0; e < ROW; ++e)
           acc[e / M][e % M] = (k == 0) ? ig[0] * rd[e] : fma(ig[k], rd[k * ROW + e], acc[e / M][e % M]);
-      bool conv = true;
-      double dsum = 0.0;
+      BitMax bm;
 #pragma unroll
       for (int e = 0; e < ROW; ++e) {
         const double qn = rq[e] - scale * acc[e / M][e % M];
-        const double dd = fabs(qn - qp[e / M][e % M]);
-        conv = conv && (dd <= tol);
-        dsum += dd;
+        bm.add(fabs(qn - qp[e / M][e % M]));
         qp[e / M][e % M] = qn;
       }
       iters = it + 1;
-      const int fl = block_flags<NW>(!pact || conv, pact && !finite(dsum), sFlags, it & 1);
+      const int fl = block_flags<NW>(!pact || bm.conv(tol), pact && bm.bad(), sFlags, it & 1);
       if (fl & 2) { failed = true; break; }
       if (fl & 1) break;
     }
@@ -620,20 +617,17 @@ sweep_kernel_v2(const SweepParams P) {
       // Picard update; max |q_new - q| via the bit patterns of non-negative
       // doubles (NaN/inf patterns sort above every finite value)
       // converged iff every |q_new - q| <= tol; a running sum carries inf/NaN
-      bool conv = true;
-      double dsum = 0.0;
+      BitMax bm;
 #pragma unroll
       for (int t = 0; t < NQ; ++t)
 #pragma unroll
         for (int c = 0; c < M; ++c) {
           const double qn = Qx[c] - scale * acc[t][c];
-          const double dd = fabs(qn - q[t][c]);
-          conv = conv && (dd <= tol);
-          dsum += dd;
+          bm.add(fabs(qn - q[t][c]));
           q[t][c] = qn;
         }
       iters = it + 1;
-      const int fl = block_flags<NW>(!act || conv, act && !finite(dsum), sFlags, it & 1);
+      const int fl = block_flags<NW>(!act || bm.conv(tol), act && bm.bad(), sFlags, it & 1);
       if (fl & 2) { failed = true; break; }
       if (fl & 1) break;
     }
@@ -744,8 +738,7 @@ sweep_kernel_v2(const SweepParams P) {
 #pragma unroll
         for (int c = 0; c < M; ++c) accr[t][c] = fma(P.ops.integ[t][NQ - 1], dvp[c], accr[t][c]);
     }
-    bool conv = true;
-    double dsum = 0.0;
+    BitMax bm;
 #pragma unroll
     for (int c = 0; c < M; ++c) {
       double dvk[NQ];
@@ -764,14 +757,12 @@ sweep_kernel_v2(const SweepParams P) {
           for (int k = 0; k < NQ; ++k) acc = fma(P.ops.integ[t][k], dvk[k], acc);
         }
         const double qn = Qx[c] - scale * acc;
-        const double dd = fabs(qn - q[s][c]);
-        conv = conv && (dd <= tol);
-        dsum += dd;
+        bm.add(fabs(qn - q[s][c]));
         q[s][c] = qn;
       }
     }
     iters = it + 1;
-    const int fl = block_flags<NW>(!act || conv, act && !finite(dsum), sFlags, it & 1);
+    const int fl = block_flags<NW>(!act || bm.conv(tol), act && bm.bad(), sFlags, it & 1);
     if (fl & 2) { failed = true; break; }
     if (fl & 1) break;
   }
