@@ -104,16 +104,16 @@ bool dispatch_adv(int n, Dispatch* out) {
   return false;
 }
 
-template <int NQ, int LN = 2>
+template <int NQ, int LN = 2, bool TM = false>
 void launch_sweep_ho(const SweepParams& P, unsigned grid, cudaStream_t s) {
   using S = ShapeHO<NQ>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(sweep_kernel_ho<NQ, true, LN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(sweep_kernel_ho<NQ, true, LN, TM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)S::SMEM_BYTES);
     attr = true;
   }
-  sweep_kernel_ho<NQ, true, LN><<<grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
+  sweep_kernel_ho<NQ, true, LN, TM><<<grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
 }
 
 int kernel_variant() {
@@ -138,9 +138,9 @@ Dispatch make_dispatch_st() {
 
 // ADG_KERNEL=15 / 18 / 19: DMMA-tile / constant-bank line / lane-group line
 // derivative engines of the high-order kernel (A/B)
-template <int NQ, int LN>
+template <int NQ, int LN, bool TM = false>
 int occ_ho() {
-  return occupancy_of(sweep_kernel_ho<NQ, true, LN>, ShapeHO<NQ>::THREADS, ShapeHO<NQ>::SMEM_BYTES);
+  return occupancy_of(sweep_kernel_ho<NQ, true, LN, TM>, ShapeHO<NQ>::THREADS, ShapeHO<NQ>::SMEM_BYTES);
 }
 
 template <int NQ>
@@ -151,9 +151,16 @@ Dispatch make_dispatch_ho() {
   if (var == 15) return Dispatch{&launch_sweep_ho<NQ, 0>, ShapeHO<NQ>::REC, &occ_ho<NQ, 0>};
   if (var == 18) return Dispatch{&launch_sweep_ho<NQ, 1>, ShapeHO<NQ>::REC, &occ_ho<NQ, 1>};
   if (var == 19) return Dispatch{&launch_sweep_ho<NQ, 2>, ShapeHO<NQ>::REC, &occ_ho<NQ, 2>};
+  // ADG_KERNEL=40 / 41: the default engine with / without the first node's time line in TMEM
+  constexpr int LD = (NQ == 10 ? 1 : 0);
+  if (var == 40) return Dispatch{&launch_sweep_ho<NQ, LD, true>, ShapeHO<NQ>::REC, &occ_ho<NQ, LD, true>};
+  if (var == 41) return Dispatch{&launch_sweep_ho<NQ, LD, false>, ShapeHO<NQ>::REC, &occ_ho<NQ, LD, false>};
   // measured (cfg3, one B200): DMMA tiles win at n <= 9 (p=7: 6.55 vs 4.74 / 6.18 TF/s),
-  // the constant-bank lines at n = 10 (p=9: 6.89 vs 6.54 / 2.24 TF/s)
-  return Dispatch{&launch_sweep_ho<NQ, (NQ == 10 ? 1 : 0)>, ShapeHO<NQ>::REC, &occ_ho<NQ, (NQ == 10 ? 1 : 0)>};
+  // the constant-bank lines at n = 10 (p=9: 6.89 vs 6.54 / 2.24 TF/s); the TMEM time line
+  // wins at n <= 8 (p=7: 7.03 vs 6.44 TF/s) and loses at n = 10 (7.29 vs 7.92: the extra
+  // registers spill under the 128-register cap)
+  constexpr bool TD = (NQ <= 8);
+  return Dispatch{&launch_sweep_ho<NQ, LD, TD>, ShapeHO<NQ>::REC, &occ_ho<NQ, LD, TD>};
 }
 
 template <int NQ, int TS, bool DMMA, bool ROLLED, int MB>

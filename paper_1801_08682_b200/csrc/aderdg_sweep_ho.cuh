@@ -81,6 +81,49 @@ struct ShapeHO {
   static constexpr size_t SMEM_BYTES = sizeof(double) * TOTAL;
 };
 
+
+// ---------------------------------------------------------------------------
+// Tensor memory (TMEM, 256 KB per SM) as per-thread storage for the Picard
+// time line.  tcgen05.ld/st with the 32x32b shape move one 32-bit column per
+// thread; warp w owns lanes 32*(w%4).. and, with 16 warps sharing the four lane
+// quadrants, columns (w/4)*128 .. +127 of a 512-column allocation: 64 doubles
+// per thread.  One CTA per SM (512 threads x 128 registers), so the CTA takes
+// the whole TMEM and releases it before it exits.
+__device__ __forceinline__ void tmem_alloc_512(uint32_t* dst) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n"
+               "tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::"r"(smem_u32(dst))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_dealloc_512(uint32_t t) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(t) : "memory");
+}
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// one double = two columns; the wait carries the registers as operands so no use
+// of a loaded value can be scheduled before the load completes
+__device__ __forceinline__ void tmem_ld_d(uint32_t a, uint32_t& lo, uint32_t& hi) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(a));
+}
+__device__ __forceinline__ double tmem_wait_d(uint32_t& lo, uint32_t& hi) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(lo), "+r"(hi)::"memory");
+  return __hiloint2double((int)hi, (int)lo);
+}
+__device__ __forceinline__ void tmem_st_d(uint32_t a, double v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(a), "r"((uint32_t)__double2loint(v)),
+               "r"((uint32_t)__double2hiint(v))
+               : "memory");
+}
+// K doubles at columns base + stride*i (loads issued back to back, one wait)
+template <int K>
+__device__ __forceinline__ void tmem_ld_doubles(uint32_t base, uint32_t stride, double (&v)[K]) {
+  uint32_t lo[K], hi[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) tmem_ld_d(base + stride * i, lo[i], hi[i]);
+#pragma unroll
+  for (int i = 0; i < K; ++i) v[i] = tmem_wait_d(lo[i], hi[i]);
+}
+
 // One derivative line of axis A on the FP64 pipe: the NQ inputs of the line
 // into registers, out[i] = sum_j diff[i][j] in[j] with diff from the constant
 // bank (kernel parameters), NQ independent accumulators, written back in place.
@@ -105,7 +148,7 @@ __device__ __forceinline__ void deriv_line(double* ln, const SweepParams& P) {
 // 1 = one line per thread, diff from the constant bank; 2 = a line per group of
 // ceil(n/2) lanes, each lane two outputs with its two diff rows in registers,
 // the line's inputs broadcast to the group (DFMA-bound, no padding waste).
-template <int NQ, bool FA = true, int LN = 0>
+template <int NQ, bool FA = true, int LN = 0, bool TM = false>
 __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
   using S = ShapeHO<NQ, FA>;
   constexpr int DIM = 3, M = 5, NS = S::NS, NF = S::NF, NPT = S::NPT, REC = S::REC;
@@ -316,7 +359,10 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
     sTab[e] = c * SC + (y / NQ) * sb + (y % NQ) * sc2;
   }
   // per-node time line in thread-private (local) memory
-  double qo[NPT][NQ][M];
+  // (TM: node 0's line is in TMEM; qo holds the others, index n - 1)
+  constexpr int QN = TM ? (NPT > 1 ? NPT - 1 : 1) : NPT;
+  constexpr int Q0 = TM ? 1 : 0;
+  double qo[QN][NQ][M];
   double dh[S::DH_SMEM ? 1 : NPT][S::DH_SMEM ? 1 : NQ][M];
   auto dhp = [&](int n, int k, int c) -> double& {
     if constexpr (S::DH_SMEM) return sDH[(k * M + c) * (THREADS * NPT) + n * THREADS + tid];
@@ -324,7 +370,27 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
   };
   int iters = 0;
   bool failed = false;
+  // TM: the time line of the thread's first node lives in TMEM, column
+  // (c*NQ + t)*2 of the thread's 128-column slice
+  __shared__ uint32_t s_tmem;
+  uint32_t tq = 0;
+  if constexpr (TM) {
+    if (warp == 0) tmem_alloc_512(&s_tmem);
+    tmem_fence_before();
+  }
   __syncthreads();
+  if constexpr (TM) {
+    tmem_fence_after();
+    tq = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 128);
+  }
+  auto qo_slice = [&](int n, int k, double (&qq)[M]) {
+    if (TM && n == 0) {
+      tmem_ld_doubles<M>(tq + 2 * k, 2 * NQ, qq);
+    } else {
+#pragma unroll
+      for (int c = 0; c < M; ++c) qq[c] = qo[n - Q0][k][c];
+    }
+  };
 #pragma unroll 1
   for (int it = 0; it < cap; ++it) {
 #pragma unroll 1
@@ -333,8 +399,12 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
 #pragma unroll
       for (int n = 0; n < NPT; ++n) {
         double qq[M];
+        if (it == 0) {
 #pragma unroll
-        for (int c = 0; c < M; ++c) qq[c] = (it == 0) ? Qx[n][c] : qo[n][k][c];
+          for (int c = 0; c < M; ++c) qq[c] = Qx[n][c];
+        } else {
+          qo_slice(n, k, qq);
+        }
         flux<DIM>(qq, F[n]);
       }
 if constexpr (FA) {
@@ -483,6 +553,7 @@ if constexpr (FA) {
 #define ADG_HO_CR 1
 #endif
 #if ADG_HO_CR == 0
+    static_assert(!TM, "the TMEM time line needs the register time contraction (ADG_HO_CR 1)");
 #pragma unroll
     for (int n = 0; n < NPT; ++n) {
 #pragma unroll 1
@@ -509,19 +580,29 @@ if constexpr (FA) {
         double dk[NQ];
 #pragma unroll
         for (int k = 0; k < NQ; ++k) dk[k] = dhp(n, k, c);
+        double ql[NQ];                                   // TM: the old time line of (0, c)
+        if (TM && n == 0) {
+          if (it > 0) tmem_ld_doubles<NQ>(tq + 2 * NQ * c, 2, ql);
+          else {
+#pragma unroll
+            for (int t = 0; t < NQ; ++t) ql[t] = Qx[n][c];
+          }
+        }
 #pragma unroll
         for (int t = 0; t < NQ; ++t) {
           double acc = 0.0;
 #pragma unroll
           for (int k = 0; k < NQ; ++k) acc = fma(P.ops.integ[t][k], dk[k], acc);
           const double qn = Qx[n][c] - scale * acc;
-          const double qold = (it == 0) ? Qx[n][c] : qo[n][t][c];
+          const double qold = (TM && n == 0) ? ql[t] : (it == 0) ? Qx[n][c] : qo[n - Q0][t][c];
           const double dd = fabs(qn - qold);
           if (an[n]) bm.add(dd);
-          qo[n][t][c] = qn;
+          if (TM && n == 0) tmem_st_d(tq + 2 * (NQ * c + t), qn);
+          else qo[n - Q0][t][c] = qn;
         }
       }
     }
+    if constexpr (TM) tmem_wait_st();
 #endif
     iters = it + 1;
     if (__syncthreads_or(bm.bad())) { failed = true; break; }
@@ -548,7 +629,9 @@ if constexpr (FA) {
 #pragma unroll 1
       for (int t = 0; t < NQ; ++t) {
         double F[DIM][M];
-        flux<DIM>(qo[n][t], F);
+        double qt[M];
+        qo_slice(n, t, qt);
+        flux<DIM>(qt, F);
         const double w = P.ops.w[t];
 #pragma unroll
         for (int a = 0; a < DIM; ++a)
@@ -558,13 +641,22 @@ if constexpr (FA) {
             fb[n][a][c] = fma(w, F[a][c], fb[n][a][c]);
           }
 #pragma unroll
-        for (int c = 0; c < M; ++c) qb[n][c] = fma(w, qo[n][t][c], qb[n][c]);
+        for (int c = 0; c < M; ++c) qb[n][c] = fma(w, qt[c], qb[n][c]);
       }
     }
     failed = __syncthreads_or(bad);
   }
+  auto tmem_release = [&]() {
+    if constexpr (TM) {
+      tmem_fence_before();
+      __syncthreads();
+      tmem_fence_after();
+      if (warp == 0) tmem_dealloc_512(s_tmem);
+    }
+  };
   if (failed) {
     if (tid == 0) report_error(st, 2 * gcell + 1);
+    tmem_release();
     return;
   }
   if (tid == 0) {
@@ -650,10 +742,13 @@ if constexpr (FA) {
   for (int t = 0; t < NQ; ++t) {
     __syncthreads();
 #pragma unroll
-    for (int n = 0; n < NPT; ++n)
+    for (int n = 0; n < NPT; ++n) {
+      double qt[M];
+      qo_slice(n, t, qt);
       if (an[n])
 #pragma unroll
-        for (int c = 0; c < M; ++c) sN[c * NS + xn[n]] = qo[n][t][c];
+        for (int c = 0; c < M; ++c) sN[c * NS + xn[n]] = qt[c];
+    }
     __syncthreads();
     for (int e = tid; e < 2 * DIM * NF; e += THREADS) {
       const int y = e % NF, f = e / NF, a = f >> 1;
@@ -674,6 +769,7 @@ if constexpr (FA) {
       atomicMax(&sSmax[f], (unsigned long long)__double_as_longlong(sp));
     }
   }
+  tmem_release();   // (its barrier also orders the s_max atomics)
   __syncthreads();
   if (tid < 2 * DIM) {
     double* rec = P.tr_out + ((long long)tid * P.slots + own_slot) * REC;
