@@ -104,7 +104,7 @@ bool dispatch_adv(int n, Dispatch* out) {
   return false;
 }
 
-template <int NQ, int LN = 2, bool TM = false>
+template <int NQ, int LN = 2, int TM = 0>
 void launch_sweep_ho(const SweepParams& P, unsigned grid, cudaStream_t s) {
   using S = ShapeHO<NQ>;
   static bool attr = false;
@@ -138,7 +138,7 @@ Dispatch make_dispatch_st() {
 
 // ADG_KERNEL=15 / 18 / 19: DMMA-tile / constant-bank line / lane-group line
 // derivative engines of the high-order kernel (A/B)
-template <int NQ, int LN, bool TM = false>
+template <int NQ, int LN, int TM = 0>
 int occ_ho() {
   return occupancy_of(sweep_kernel_ho<NQ, true, LN, TM>, ShapeHO<NQ>::THREADS, ShapeHO<NQ>::SMEM_BYTES);
 }
@@ -151,15 +151,17 @@ Dispatch make_dispatch_ho() {
   if (var == 15) return Dispatch{&launch_sweep_ho<NQ, 0>, ShapeHO<NQ>::REC, &occ_ho<NQ, 0>};
   if (var == 18) return Dispatch{&launch_sweep_ho<NQ, 1>, ShapeHO<NQ>::REC, &occ_ho<NQ, 1>};
   if (var == 19) return Dispatch{&launch_sweep_ho<NQ, 2>, ShapeHO<NQ>::REC, &occ_ho<NQ, 2>};
-  // ADG_KERNEL=40 / 41: the default engine with / without the first node's time line in TMEM
+  // ADG_KERNEL=40 / 42 / 41: the default engine with the first node's time line / divergence
+  // history in TMEM, or neither
   constexpr int LD = (NQ == 10 ? 1 : 0);
-  if (var == 40) return Dispatch{&launch_sweep_ho<NQ, LD, true>, ShapeHO<NQ>::REC, &occ_ho<NQ, LD, true>};
-  if (var == 41) return Dispatch{&launch_sweep_ho<NQ, LD, false>, ShapeHO<NQ>::REC, &occ_ho<NQ, LD, false>};
+  if (var == 40) return Dispatch{&launch_sweep_ho<NQ, LD, 1>, ShapeHO<NQ>::REC, &occ_ho<NQ, LD, 1>};
+  if (var == 42) return Dispatch{&launch_sweep_ho<NQ, LD, 2>, ShapeHO<NQ>::REC, &occ_ho<NQ, LD, 2>};
+  if (var == 41) return Dispatch{&launch_sweep_ho<NQ, LD, 0>, ShapeHO<NQ>::REC, &occ_ho<NQ, LD, 0>};
   // measured (cfg3, one B200): DMMA tiles win at n <= 9 (p=7: 6.55 vs 4.74 / 6.18 TF/s),
   // the constant-bank lines at n = 10 (p=9: 6.89 vs 6.54 / 2.24 TF/s); the TMEM time line
   // wins at n <= 8 (p=7: 7.03 vs 6.44 TF/s) and loses at n = 10 (7.29 vs 7.92: the extra
   // registers spill under the 128-register cap)
-  constexpr bool TD = (NQ <= 8);
+  constexpr int TD = (NQ <= 8) ? 1 : 0;
   return Dispatch{&launch_sweep_ho<NQ, LD, TD>, ShapeHO<NQ>::REC, &occ_ho<NQ, LD, TD>};
 }
 
@@ -280,7 +282,8 @@ bool dispatch_for(int d, int p, int system, Dispatch* out) {
              : kernel_variant() == 9 ? make_dispatch_v2<6, 1, false, false, 9>()
              : kernel_variant() == 12 ? make_dispatch_ho<6>()
              : kernel_variant() == 30 ? make_dispatch_v2<6, 1, false, false, 30>()   // pencil Picard loop
-             : make_dispatch_v2<6, 1, false>();
+             : kernel_variant() == 32 ? make_dispatch_v2<6, 1, false>()              // C-order nodes (A/B)
+             : make_dispatch_v2<6, 1, false, false, 31>();   // default: warp node blocks (2.45e9 vs 2.36e9)
         return true;
       // p >= 6: time line in local memory, spatial derivatives as DMMA GEMMs
       case 7: *out = kernel_variant() == 1 ? make_dispatch<3, 7>() : make_dispatch_ho<7>(); return true;

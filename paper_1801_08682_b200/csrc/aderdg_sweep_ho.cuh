@@ -148,7 +148,7 @@ __device__ __forceinline__ void deriv_line(double* ln, const SweepParams& P) {
 // 1 = one line per thread, diff from the constant bank; 2 = a line per group of
 // ceil(n/2) lanes, each lane two outputs with its two diff rows in registers,
 // the line's inputs broadcast to the group (DFMA-bound, no padding waste).
-template <int NQ, bool FA = true, int LN = 0, bool TM = false>
+template <int NQ, bool FA = true, int LN = 0, int TM = 0>
 __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
   using S = ShapeHO<NQ, FA>;
   constexpr int DIM = 3, M = 5, NS = S::NS, NF = S::NF, NPT = S::NPT, REC = S::REC;
@@ -360,13 +360,16 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
   }
   // per-node time line in thread-private (local) memory
   // (TM: node 0's line is in TMEM; qo holds the others, index n - 1)
-  constexpr int QN = TM ? (NPT > 1 ? NPT - 1 : 1) : NPT;
-  constexpr int Q0 = TM ? 1 : 0;
+  constexpr int QN = (TM == 1) ? (NPT > 1 ? NPT - 1 : 1) : NPT;
+  constexpr int Q0 = (TM == 1) ? 1 : 0;
   double qo[QN][NQ][M];
-  double dh[S::DH_SMEM ? 1 : NPT][S::DH_SMEM ? 1 : NQ][M];
+  // (TM 2: node 0's divergence history is in TMEM instead; dh holds the others, index n - 1)
+  constexpr int D0 = (TM == 2) ? 1 : 0;
+  constexpr int DN = S::DH_SMEM ? 1 : (NPT - D0 > 0 ? NPT - D0 : 1);
+  double dh[DN][S::DH_SMEM ? 1 : NQ][M];
   auto dhp = [&](int n, int k, int c) -> double& {
     if constexpr (S::DH_SMEM) return sDH[(k * M + c) * (THREADS * NPT) + n * THREADS + tid];
-    else return dh[n][k][c];
+    else return dh[n - D0][k][c];
   };
   int iters = 0;
   bool failed = false;
@@ -384,7 +387,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
     tq = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 128);
   }
   auto qo_slice = [&](int n, int k, double (&qq)[M]) {
-    if (TM && n == 0) {
+    if (TM == 1 && n == 0) {
       tmem_ld_doubles<M>(tq + 2 * k, 2 * NQ, qq);
     } else {
 #pragma unroll
@@ -484,9 +487,12 @@ if constexpr (FA) {
 #pragma unroll
         for (int n = 0; n < NPT; ++n)
 #pragma unroll
-          for (int c = 0; c < M; ++c)
-            dhp(n, k, c) = (sFA[c * SC + pn[n]] + sFA[S::R_FA + c * SC + pn[n]]) +
-                           sFA[2 * S::R_FA + c * SC + pn[n]];
+          for (int c = 0; c < M; ++c) {
+            const double v = (sFA[c * SC + pn[n]] + sFA[S::R_FA + c * SC + pn[n]]) +
+                             sFA[2 * S::R_FA + c * SC + pn[n]];
+            if (TM == 2 && n == 0) tmem_st_d(tq + 2 * (NQ * c + k), v);
+            else dhp(n, k, c) = v;
+          }
       } else {
 #pragma unroll 1
         for (int a = 0; a < DIM; ++a) {
@@ -544,9 +550,11 @@ if constexpr (FA) {
       for (int n = 0; n < NPT; ++n)
 #pragma unroll
         for (int c = 0; c < M; ++c) dhp(n, k, c) = sDv[c * SC + pn[n]];
+        static_assert(TM != 2, "the TMEM divergence history is wired into the fused-axes path");
       }
 
     }
+    if constexpr (TM == 2) tmem_wait_st();
     // time contraction + Picard update per node
     BitMax bm;
 #ifndef ADG_HO_CR
@@ -578,10 +586,14 @@ if constexpr (FA) {
       for (int c = 0; c < M; ++c) {
         // the divergence history of (n, c) is read once; every time level from registers
         double dk[NQ];
+        if (TM == 2 && n == 0) {
+          tmem_ld_doubles<NQ>(tq + 2 * NQ * c, 2, dk);
+        } else {
 #pragma unroll
-        for (int k = 0; k < NQ; ++k) dk[k] = dhp(n, k, c);
+          for (int k = 0; k < NQ; ++k) dk[k] = dhp(n, k, c);
+        }
         double ql[NQ];                                   // TM: the old time line of (0, c)
-        if (TM && n == 0) {
+        if (TM == 1 && n == 0) {
           if (it > 0) tmem_ld_doubles<NQ>(tq + 2 * NQ * c, 2, ql);
           else {
 #pragma unroll
@@ -594,15 +606,15 @@ if constexpr (FA) {
 #pragma unroll
           for (int k = 0; k < NQ; ++k) acc = fma(P.ops.integ[t][k], dk[k], acc);
           const double qn = Qx[n][c] - scale * acc;
-          const double qold = (TM && n == 0) ? ql[t] : (it == 0) ? Qx[n][c] : qo[n - Q0][t][c];
+          const double qold = (TM == 1 && n == 0) ? ql[t] : (it == 0) ? Qx[n][c] : qo[n - Q0][t][c];
           const double dd = fabs(qn - qold);
           if (an[n]) bm.add(dd);
-          if (TM && n == 0) tmem_st_d(tq + 2 * (NQ * c + t), qn);
+          if (TM == 1 && n == 0) tmem_st_d(tq + 2 * (NQ * c + t), qn);
           else qo[n - Q0][t][c] = qn;
         }
       }
     }
-    if constexpr (TM) tmem_wait_st();
+    if constexpr (TM == 1) tmem_wait_st();
 #endif
     iters = it + 1;
     if (__syncthreads_or(bm.bad())) { failed = true; break; }

@@ -52,13 +52,18 @@ struct ShapeV2 {
   // level of one i2-pencil (6 nodes); axis 2 is register-local, axes 0/1 and the
   // time contraction are 16-byte broadcast gathers of whole pencils
   static constexpr bool PEN = (MINB_OVERRIDE == 30);
+  // MINB_OVERRIDE 31 (BLK, NQ = 6): node-per-thread kernel with warps mapped to node
+  // blocks (2x4x4, 4x4x2, ...: every axis sees <= 16 lines per warp) and a flux
+  // slice layout i0*73 + i1*12 + i2 that keeps those gathers bank-conflict free
+  static constexpr bool BLK = (MINB_OVERRIDE == 31);
   static constexpr bool A0X = (MINB_OVERRIDE == 20);
   static constexpr bool A1S = (MINB_OVERRIDE == 10 || MINB_OVERRIDE == 16 || MINB_OVERRIDE == 17 || A0X);
-  static constexpr int MINB = PEN ? 1 : (MINB_OVERRIDE == 16) ? 8 : (MINB_OVERRIDE == 17) ? 7 : A0X ? 6
+  static constexpr int MINB = (PEN || BLK) ? 1 : (MINB_OVERRIDE == 16) ? 8 : (MINB_OVERRIDE == 17) ? 7 : A0X ? 6
                             : (MINB_OVERRIDE && MINB_OVERRIDE != 9 && !A1S) ? MINB_OVERRIDE : (MINB_OVERRIDE == 9) ? 1
                             : (TS == 1 && NQ >= 6) ? 1
                             : THREADS <= 64 ? 6 : THREADS <= 128 ? 4 : (THREADS <= 256 ? 2 : 1);
-  static constexpr int P0 = NQ * NQ + plane_pad(NQ);   // padded axis-0 plane stride
+  static constexpr int P1 = BLK ? 12 : NQ;             // axis-1 row stride of a flux slice
+  static constexpr int P0 = BLK ? 73 : NQ * NQ + plane_pad(NQ);   // padded axis-0 plane stride
   static constexpr int PS = NQ * P0;                   // padded slice size
   static constexpr int DS = DMMA ? (A1S ? 1 : DIM - 1) : DIM;   // axes through shared memory
   static constexpr bool F1T = !A1S && ((NQ == 4) || (NQ == 6 && MINB_OVERRIDE == 9));  // axis-1 flux stored transposed, 16-byte gathers
@@ -96,7 +101,7 @@ struct ShapeV2 {
   static_assert(!DMMA || NQ == 4, "DMMA axis-2 path needs i2 in lane bits 0-1");
   static_assert(!A1S || (DMMA && TS == 1 && DBUF), "A1S runs in the double-buffered DMMA slice loop");
   static_assert(!A0X || (NQ == 4 && THREADS == 64), "A0X pairs the two warps of a p = 3 cell");
-  static_assert(!PEN || (NQ == 6 && TS == 1 && !DMMA && NSP == 224), "PEN is the p = 5 pencil layout");
+  static_assert(!(PEN || BLK) || (NQ == 6 && TS == 1 && !DMMA && NSP == 224), "PEN / BLK are p = 5 layouts");
   static_assert(SMEM_BYTES <= 232448, "shared memory per CTA");
 };
 
@@ -164,6 +169,29 @@ __device__ __forceinline__ int trace_addr(int i0, int i1, int i2) {
   return (i0 * NQ + i1) * NQ + i2;
 }
 
+// p = 5 warp blocks over a 6x6x6 index cube (a, b, c): warps 0-2 take a-pairs x
+// b 0-3 x c 0-3; warp 3 a 0-3 x b 0-3 x c 4-5; warp 4 a 0-3 x b 4-5 x c 0-3;
+// warp 5 a 4-5 x (b 0-3 x c 4-5 | b 4-5 x c 0-3); warp 6 (24 lanes) a 0-5 x
+// b 4-5 x c 4-5.  Every warp's projections onto (a, b), (a, c), (b, c) have at
+// most 16 elements, so a gather that varies one index hits <= 16 distinct rows.
+__device__ __forceinline__ void block_map_p5(int tid, int& a, int& b, int& c, bool& act) {
+  const int w = tid >> 5, l = tid & 31;
+  act = true;
+  if (w < 3) { a = 2 * w + (l >> 4); b = (l >> 2) & 3; c = l & 3; }
+  else if (w == 3) { a = l >> 3; b = (l >> 1) & 3; c = 4 + (l & 1); }
+  else if (w == 4) { a = l >> 3; b = 4 + (l & 1); c = (l >> 1) & 3; }
+  else if (w == 5) {
+    const int u = l & 15;
+    a = 4 + (u >> 3);
+    if (l < 16) { b = (u >> 1) & 3; c = 4 + (u & 1); }
+    else { b = 4 + (u & 1); c = (u >> 1) & 3; }
+  } else {
+    act = l < 24;
+    const int u = act ? l : 0;
+    a = u >> 2; b = 4 + ((u >> 1) & 1); c = 4 + (u & 1);
+  }
+}
+
 template <int NQ, int TS, bool DMMA, bool ROLLED = (NQ == 4), int MB = 0>
 __global__ void __launch_bounds__(ShapeV2<NQ, TS, DMMA, ROLLED, MB>::THREADS, ShapeV2<NQ, TS, DMMA, ROLLED, MB>::MINB)
 sweep_kernel_v2(const SweepParams P) {
@@ -194,12 +222,18 @@ sweep_kernel_v2(const SweepParams P) {
   const int tid = threadIdx.x;
   const int ts = tid / NSP;
   const int x0 = tid % NSP;
-  const bool act = x0 < NS;
-  const int x = act ? x0 : 0;
+  bool act = x0 < NS;
+  int x = act ? x0 : 0;
+  if constexpr (S::BLK) {
+    int b0, b1, b2;
+    block_map_p5(tid, b0, b1, b2, act);
+    x = (b0 * NQ + b1) * NQ + b2;
+  }
   const long long cell = sweep_cell(P);
   const long long gcell = cell + P.cell_offset;
   const int i0 = x / (NQ * NQ), i1 = (x / NQ) % NQ, i2 = x % NQ;
-  const int px = i0 * P0 + i1 * NQ + i2;              // padded slice index
+  constexpr int P1 = S::P1;
+  const int px = i0 * P0 + i1 * P1 + i2;              // padded slice index
 
   const int plane = (int)(cell / P.plane_cells);
   const int rest = (int)(cell % P.plane_cells);
@@ -277,7 +311,7 @@ sweep_kernel_v2(const SweepParams P) {
   // padded gather bases for the shared-memory axes
   int gbase[DIM], gstr[DIM];
   gbase[0] = px - i0 * P0; gstr[0] = P0;
-  gbase[1] = px - i1 * NQ; gstr[1] = NQ;
+  gbase[1] = px - i1 * P1; gstr[1] = P1;
   gbase[2] = px - i2;      gstr[2] = 1;
   // F1T: axis-1 flux stored with i1 fastest (plane stride P1T), gathered as
   // 16-byte pairs; 8 distinct 16-byte chunks per warp -> one wavefront.
@@ -420,23 +454,8 @@ sweep_kernel_v2(const SweepParams P) {
     // ~4 wavefronts each whatever the broadcast).
     constexpr int ROW = NQ * M;                         // one pencil: 30 doubles
     int pt, pj0, pj1;
-    bool pact = true;
-    {
-      const int w = tid >> 5, l = tid & 31;
-      if (w < 3) { pt = 2 * w + (l >> 4); pj0 = (l >> 2) & 3; pj1 = l & 3; }
-      else if (w == 3) { pt = l >> 3; pj0 = (l >> 1) & 3; pj1 = 4 + (l & 1); }
-      else if (w == 4) { pt = l >> 3; pj0 = 4 + (l & 1); pj1 = (l >> 1) & 3; }
-      else if (w == 5) {
-        const int u = l & 15;
-        pt = 4 + (u >> 3);
-        if (l < 16) { pj0 = (u >> 1) & 3; pj1 = 4 + (u & 1); }
-        else { pj0 = 4 + (u & 1); pj1 = (u >> 1) & 3; }
-      } else {
-        pact = l < 24;
-        const int u = pact ? l : 0;
-        pt = u >> 2; pj0 = 4 + ((u >> 1) & 1); pj1 = 4 + (u & 1);
-      }
-    }
+    bool pact;
+    block_map_p5(tid, pt, pj0, pj1, pact);
     double* sP0 = sU;                                   // F_0 pencils
     double* sP1 = sU + S::PB0;                          // F_1 pencils
     double* sPd = sU + S::PB0 + S::PB1;                 // divergence pencils
@@ -931,12 +950,12 @@ sweep_kernel_v2(const SweepParams P) {
   // ---------------- face records: qbar and fbar traces ----------------
 #pragma unroll
   for (int a = 0; a < DIM; ++a) {
-    const int pst = (a == 0) ? P0 : (a == 1) ? NQ : 1;
+    const int pst = (a == 0) ? P0 : (a == 1) ? P1 : 1;
     for (int e = tid; e < 2 * M * NF; e += THREADS) {
       const int y = e % NF, sc = e / NF, c = sc % M, side = sc / M;
       const double* vec = side ? P.ops.right : P.ops.left;
       const int ya = y / NQ, yb = y % NQ;
-      const int pxb = (a == 0) ? ya * NQ + yb : (a == 1) ? ya * P0 + yb : ya * P0 + yb * NQ;
+      const int pxb = (a == 0) ? ya * P1 + yb : (a == 1) ? ya * P0 + yb : ya * P0 + yb * P1;
       double vq = 0.0, vf = 0.0;
 #pragma unroll
       for (int i = 0; i < NQ; ++i) {
