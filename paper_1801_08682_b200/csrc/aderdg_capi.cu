@@ -273,7 +273,8 @@ bool dispatch_for(int d, int p, int system, Dispatch* out) {
              : kernel_variant() == 16 ? make_dispatch_v2<4, 1, true, false, 16>()  // A1S, 8 CTAs/SM
              : kernel_variant() == 20 ? make_dispatch_v2<4, 1, true, false, 20>()  // A1S + axis-0 partial sums
              : kernel_variant() == 17 ? make_dispatch_v2<4, 1, true, false, 17>()  // A1S, 7 CTAs/SM
-             : make_dispatch_v2<4, 1, true, false, 10>();   // default: axis 1 via lane transpose + DMMA
+             : kernel_variant() == 21 ? make_dispatch_v2<4, 1, true, false, 10>()  // A1S, slice at a time
+             : make_dispatch_v2<4, 1, true, false, 11>();   // default: A1S + pipelined slices (1.092e10 vs 1.074e10)
         return true;
       case 5: *out = make_dispatch<3, 5>(); return true;
       case 6:

@@ -57,7 +57,9 @@ struct ShapeV2 {
   // slice layout i0*73 + i1*12 + i2 that keeps those gathers bank-conflict free
   static constexpr bool BLK = (MINB_OVERRIDE == 31);
   static constexpr bool A0X = (MINB_OVERRIDE == 20);
-  static constexpr bool A1S = (MINB_OVERRIDE == 10 || MINB_OVERRIDE == 16 || MINB_OVERRIDE == 17 || A0X);
+  // MINB_OVERRIDE 11: A1S with a software-pipelined slice loop (p = 3 default)
+  static constexpr bool PIPE = (MINB_OVERRIDE == 11);
+  static constexpr bool A1S = (MINB_OVERRIDE == 10 || MINB_OVERRIDE == 16 || MINB_OVERRIDE == 17 || A0X || PIPE);
   static constexpr int MINB = (PEN || BLK) ? 1 : (MINB_OVERRIDE == 16) ? 8 : (MINB_OVERRIDE == 17) ? 7 : A0X ? 6
                             : (MINB_OVERRIDE && MINB_OVERRIDE != 9 && !A1S) ? MINB_OVERRIDE : (MINB_OVERRIDE == 9) ? 1
                             : (TS == 1 && NQ >= 6) ? 1
@@ -642,6 +644,99 @@ sweep_kernel_v2(const SweepParams P) {
 #pragma unroll
         for (int c = 0; c < M; ++c) {
           const double qn = Qx[c] - scale * acc[t][c];
+          bm.add(fabs(qn - q[t][c]));
+          q[t][c] = qn;
+        }
+      iters = it + 1;
+      const int fl = block_flags<NW>(!act || bm.conv(tol), act && bm.bad(), sFlags, it & 1);
+      if (fl & 2) { failed = true; break; }
+      if (fl & 1) break;
+    }
+  } else if constexpr (S::PIPE) {
+    // Software-pipelined slice loop (p = 3, A1S): the interval after the barrier
+    // that publishes slice s also computes the flux of slice s+1 — its axis-0 flux
+    // goes to the other buffer, whose readers (slice s-1) all passed this barrier —
+    // and issues its axis-1 DMMA, so two independent dependency chains share every
+    // barrier interval.
+#pragma unroll 1
+    for (int it = 0; it < cap; ++it) {
+      double accr[NQ][M];
+      double dvp[M];
+      double F2c[M], d1c[M];           // current slice: axis-2 flux (A operand), axis-1 DMMA (transposed lane)
+      {
+        double F[DIM][M];
+        flux<DIM>(q[0], F);
+        if (act) {
+#pragma unroll
+          for (int c = 0; c < M; ++c) sF[c * PS + px] = F[0][c];
+        }
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          const double a1 = __shfl_sync(0xffffffffu, F[1][c], sig);
+          double z1;
+          dmma_8x8x4(d1c[c], z1, a1, bfrag, 0.0, 0.0);
+          F2c[c] = F[2][c];
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < NQ; ++s) {
+        __syncthreads();
+        const double* sFs = sF + (s & 1) * (DS * M * PS);
+        double dv[M];
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          const double* b = sFs + c * PS + gbase[0];
+          double v = 0.0;
+#pragma unroll
+          for (int j = 0; j < NQ; ++j) v = fma(drow[0][j], b[j * gstr[0]], v);
+          dv[c] = v + __shfl_sync(0xffffffffu, d1c[c], sig);
+        }
+        double F2n[M], d1n[M];
+        if (s + 1 < NQ) {
+          double F[DIM][M];
+          flux<DIM>(q[s + 1 < NQ ? s + 1 : 0], F);
+          double* sFn = sF + ((s + 1) & 1) * (DS * M * PS);
+          if (act) {
+#pragma unroll
+            for (int c = 0; c < M; ++c) sFn[c * PS + px] = F[0][c];
+          }
+#pragma unroll
+          for (int c = 0; c < M; ++c) {
+            const double a1 = __shfl_sync(0xffffffffu, F[1][c], sig);
+            double z1;
+            dmma_8x8x4(d1n[c], z1, a1, bfrag, 0.0, 0.0);
+            F2n[c] = F[2][c];
+          }
+        }
+        if (s > 0) {
+          // time contraction of slice s-1, deferred past its DMMA latency
+#pragma unroll
+          for (int t = 0; t < NQ; ++t)
+#pragma unroll
+            for (int c = 0; c < M; ++c)
+              accr[t][c] = (s == 1) ? P.ops.integ[t][0] * dvp[c] : fma(P.ops.integ[t][s - 1], dvp[c], accr[t][c]);
+        }
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          double d1;
+          dmma_8x8x4(dv[c], d1, F2c[c], bfrag, dv[c], 0.0);
+          dvp[c] = dv[c];
+        }
+        if (s + 1 < NQ) {
+#pragma unroll
+          for (int c = 0; c < M; ++c) { F2c[c] = F2n[c]; d1c[c] = d1n[c]; }
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < NQ; ++t)
+#pragma unroll
+        for (int c = 0; c < M; ++c) accr[t][c] = fma(P.ops.integ[t][NQ - 1], dvp[c], accr[t][c]);
+      BitMax bm;
+#pragma unroll
+      for (int t = 0; t < NQ; ++t)
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          const double qn = Qx[c] - scale * accr[t][c];
           bm.add(fabs(qn - q[t][c]));
           q[t][c] = qn;
         }
