@@ -274,7 +274,9 @@ bool dispatch_for(int d, int p, int system, Dispatch* out) {
              : kernel_variant() == 20 ? make_dispatch_v2<4, 1, true, false, 20>()  // A1S + axis-0 partial sums
              : kernel_variant() == 17 ? make_dispatch_v2<4, 1, true, false, 17>()  // A1S, 7 CTAs/SM
              : kernel_variant() == 21 ? make_dispatch_v2<4, 1, true, false, 10>()  // A1S, slice at a time
-             : make_dispatch_v2<4, 1, true, false, 11>();   // default: A1S + pipelined slices (1.092e10 vs 1.074e10)
+             : kernel_variant() == 22 ? make_dispatch_v2<4, 1, true, false, 11>()  // pipelined, DMMAs after the barrier
+             : make_dispatch_v2<4, 1, true, false, 14>();   // default: A1S + pipelined slices, DMMAs in the
+                                                            // producing interval (1.095e10 vs 1.091e10 vs 1.074e10)
         return true;
       case 5: *out = make_dispatch<3, 5>(); return true;
       case 6:

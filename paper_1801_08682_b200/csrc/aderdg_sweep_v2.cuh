@@ -57,8 +57,11 @@ struct ShapeV2 {
   // slice layout i0*73 + i1*12 + i2 that keeps those gathers bank-conflict free
   static constexpr bool BLK = (MINB_OVERRIDE == 31);
   static constexpr bool A0X = (MINB_OVERRIDE == 20);
-  // MINB_OVERRIDE 11: A1S with a software-pipelined slice loop (p = 3 default)
-  static constexpr bool PIPE = (MINB_OVERRIDE == 11);
+  // MINB_OVERRIDE 11: A1S with a software-pipelined slice loop (p = 3 default);
+  // 14: the same with the axis-1 and axis-2 DMMAs of a slice completed (and the
+  // axis-1 result transposed back) in the interval that produces the slice
+  static constexpr bool PIPE = (MINB_OVERRIDE == 11 || MINB_OVERRIDE == 14);
+  static constexpr bool PIPE2 = (MINB_OVERRIDE == 14);
   static constexpr bool A1S = (MINB_OVERRIDE == 10 || MINB_OVERRIDE == 16 || MINB_OVERRIDE == 17 || A0X || PIPE);
   static constexpr int MINB = (PEN || BLK) ? 1 : (MINB_OVERRIDE == 16) ? 8 : (MINB_OVERRIDE == 17) ? 7 : A0X ? 6
                             : (MINB_OVERRIDE && MINB_OVERRIDE != 9 && !A1S) ? MINB_OVERRIDE : (MINB_OVERRIDE == 9) ? 1
@@ -657,27 +660,39 @@ sweep_kernel_v2(const SweepParams P) {
     // that publishes slice s also computes the flux of slice s+1 — its axis-0 flux
     // goes to the other buffer, whose readers (slice s-1) all passed this barrier —
     // and issues its axis-1 DMMA, so two independent dependency chains share every
-    // barrier interval.
+    // barrier interval.  PIPE2 also issues the slice's axis-2 DMMA (C = 0) there and
+    // transposes the axis-1 result back, leaving only the axis-0 gather after the barrier.
 #pragma unroll 1
     for (int it = 0; it < cap; ++it) {
       double accr[NQ][M];
       double dvp[M];
-      double F2c[M], d1c[M];           // current slice: axis-2 flux (A operand), axis-1 DMMA (transposed lane)
-      {
+      double F2c[M], d1c[M];           // current slice: axis-2 flux (A operand) / PIPE2: axis-2 result,
+                                       // axis-1 DMMA result (PIPE2: transposed back)
+      auto produce = [&](int sl, double (&f2)[M], double (&d1)[M]) {
         double F[DIM][M];
-        flux<DIM>(q[0], F);
+        flux<DIM>(q[sl], F);
+        double* sFn = sF + (sl & 1) * (DS * M * PS);
         if (act) {
 #pragma unroll
-          for (int c = 0; c < M; ++c) sF[c * PS + px] = F[0][c];
+          for (int c = 0; c < M; ++c) sFn[c * PS + px] = F[0][c];
         }
 #pragma unroll
         for (int c = 0; c < M; ++c) {
           const double a1 = __shfl_sync(0xffffffffu, F[1][c], sig);
           double z1;
-          dmma_8x8x4(d1c[c], z1, a1, bfrag, 0.0, 0.0);
-          F2c[c] = F[2][c];
+          dmma_8x8x4(d1[c], z1, a1, bfrag, 0.0, 0.0);
+          if (S::PIPE2) dmma_8x8x4(f2[c], z1, F[2][c], bfrag, 0.0, 0.0);
+          else f2[c] = F[2][c];
         }
-      }
+      };
+      auto finish_produce = [&](double (&d1)[M]) {
+        if (S::PIPE2) {
+#pragma unroll
+          for (int c = 0; c < M; ++c) d1[c] = __shfl_sync(0xffffffffu, d1[c], sig);
+        }
+      };
+      produce(0, F2c, d1c);
+      finish_produce(d1c);
 #pragma unroll
       for (int s = 0; s < NQ; ++s) {
         __syncthreads();
@@ -689,25 +704,10 @@ sweep_kernel_v2(const SweepParams P) {
           double v = 0.0;
 #pragma unroll
           for (int j = 0; j < NQ; ++j) v = fma(drow[0][j], b[j * gstr[0]], v);
-          dv[c] = v + __shfl_sync(0xffffffffu, d1c[c], sig);
+          dv[c] = S::PIPE2 ? (v + d1c[c]) + F2c[c] : v + __shfl_sync(0xffffffffu, d1c[c], sig);
         }
         double F2n[M], d1n[M];
-        if (s + 1 < NQ) {
-          double F[DIM][M];
-          flux<DIM>(q[s + 1 < NQ ? s + 1 : 0], F);
-          double* sFn = sF + ((s + 1) & 1) * (DS * M * PS);
-          if (act) {
-#pragma unroll
-            for (int c = 0; c < M; ++c) sFn[c * PS + px] = F[0][c];
-          }
-#pragma unroll
-          for (int c = 0; c < M; ++c) {
-            const double a1 = __shfl_sync(0xffffffffu, F[1][c], sig);
-            double z1;
-            dmma_8x8x4(d1n[c], z1, a1, bfrag, 0.0, 0.0);
-            F2n[c] = F[2][c];
-          }
-        }
+        if (s + 1 < NQ) produce(s + 1 < NQ ? s + 1 : 0, F2n, d1n);
         if (s > 0) {
           // time contraction of slice s-1, deferred past its DMMA latency
 #pragma unroll
@@ -718,11 +718,14 @@ sweep_kernel_v2(const SweepParams P) {
         }
 #pragma unroll
         for (int c = 0; c < M; ++c) {
-          double d1;
-          dmma_8x8x4(dv[c], d1, F2c[c], bfrag, dv[c], 0.0);
+          if (!S::PIPE2) {
+            double d1;
+            dmma_8x8x4(dv[c], d1, F2c[c], bfrag, dv[c], 0.0);
+          }
           dvp[c] = dv[c];
         }
         if (s + 1 < NQ) {
+          finish_produce(d1n);
 #pragma unroll
           for (int c = 0; c < M; ++c) { F2c[c] = F2n[c]; d1c[c] = d1n[c]; }
         }
