@@ -46,11 +46,14 @@ struct ShapeHO {
   static constexpr int RR = NF * M;                          // GEMM columns per axis
   static constexpr int NT = (RR + 7) / 8;                    // n-tiles
   static constexpr int RP = NT * 8;
-  // padded natural node layout [c][SC] (brute-forced: stores, DMMA B loads and
-  // C scatters of every axis are at most 3-way bank conflicted)
-  static constexpr int P1 = (NQ == 10) ? 13 : (NQ == 6) ? 6 : 11;
-  static constexpr int P0 = (NQ == 6) ? 36 : (NQ == 7) ? 77 : (NQ == 8) ? 91 : (NQ == 9) ? 107 : 131;
-  static constexpr int SC = (NQ == 6) ? 217 : (NQ == 7) ? 541 : (NQ == 8) ? 729 : (NQ == 9) ? 965 : 1311;
+  // padded natural node layout [c][SC]: strides searched against a wavefront model of
+  // this kernel's accesses (8-byte loads: one wavefront per 16 distinct doubles in
+  // distinct bank pairs).  n = 8: P0 100, P1 12, SC 800 make the node stores and the
+  // DMMA B loads conflict-free (C scatters 1.67x); n = 10: P0 111, P1 10, SC 1124 for
+  // the line engine (model: 4620 vs 5750 wavefronts per slice, 21 KB less shared memory)
+  static constexpr int P1 = (NQ == 10) ? 10 : (NQ == 6) ? 6 : (NQ == 8) ? 12 : 11;
+  static constexpr int P0 = (NQ == 6) ? 36 : (NQ == 7) ? 77 : (NQ == 8) ? 100 : (NQ == 9) ? 107 : 111;
+  static constexpr int SC = (NQ == 6) ? 217 : (NQ == 7) ? 541 : (NQ == 8) ? 800 : (NQ == 9) ? 965 : 1124;
   static constexpr int REC = 2 * NF * M + 2;
   // shared memory (doubles)
   static constexpr int R_RED = 2 * NW + 2 * DIM + 4;
