@@ -19,6 +19,7 @@
 #include "aderdg_kernels.cuh"
 #include "aderdg_sweep_v2.cuh"
 #include "aderdg_sweep_ho.cuh"
+#include "aderdg_sweep_hoc.cuh"
 #include "aderdg_sweep_st.cuh"
 #include "aderdg_limiter.cuh"
 
@@ -116,6 +117,20 @@ void launch_sweep_ho(const SweepParams& P, unsigned grid, cudaStream_t s) {
   sweep_kernel_ho<NQ, true, LN, TM><<<grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
 }
 
+// the 2-CTA cluster variant of the high-order kernel: two CTAs per cell
+template <int NQ>
+void launch_sweep_hoc(const SweepParams& P, unsigned grid, cudaStream_t s) {
+  using S = ShapeHO<NQ>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sweep_kernel_hoc<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM_BYTES);
+    attr = true;
+  }
+  sweep_kernel_hoc<NQ><<<2 * grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
+}
+
+int occ_hoc() { return 1; }
+
 int kernel_variant() {
   // ADG_KERNEL=1: first-generation kernel; 2: time-split v2; 3 (default): v2 without time split
   const char* v = getenv("ADG_KERNEL");
@@ -156,6 +171,10 @@ Dispatch make_dispatch_ho() {
   constexpr int LD = (NQ == 10 ? 1 : 0);
   if (var == 40) return Dispatch{&launch_sweep_ho<NQ, LD, 1>, ShapeHO<NQ>::REC, &occ_ho<NQ, LD, 1>};
   if (var == 42) return Dispatch{&launch_sweep_ho<NQ, LD, 2>, ShapeHO<NQ>::REC, &occ_ho<NQ, LD, 2>};
+  if constexpr (NQ % 2 == 0 && NQ >= 8) {
+    // ADG_KERNEL=45: half a cell per SM on a 2-CTA cluster (aderdg_sweep_hoc.cuh)
+    if (var == 45) return Dispatch{&launch_sweep_hoc<NQ>, ShapeHO<NQ>::REC, &occ_hoc};
+  }
   if (var == 41) return Dispatch{&launch_sweep_ho<NQ, LD, 0>, ShapeHO<NQ>::REC, &occ_ho<NQ, LD, 0>};
   // measured (cfg3, one B200): DMMA tiles win at n <= 9 (p=7: 6.55 vs 4.74 / 6.18 TF/s),
   // the constant-bank lines at n = 10 (p=9: 6.89 vs 6.54 / 2.24 TF/s); the TMEM time line

@@ -32,6 +32,8 @@ CASES = [
     (40, 3, 1, 9, 2, 8),   # p=9: TMEM old iterate
     (42, 3, 1, 9, 2, 8),   # p=9: TMEM divergence history
     (15, 3, 1, 9, 2, 8),   # p=9: DMMA tile engine
+    (45, 3, 1, 9, 2, 8),   # p=9: half a cell per SM on a 2-CTA cluster (distributed shared memory)
+    (45, 3, 1, 7, 3, 4),   # p=7: the same
     (1, 3, 1, 5, 3, 1),    # first-generation kernel
 ]
 
