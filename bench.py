@@ -260,6 +260,11 @@ def main():
     E = cfgd["steps"]
     drv = SlabDriver(Q0, d, L, p, rank, world, local, mode=args.mode, staged=staged)
     h = drv.handle
+    # N > 1: the timed steps are enqueued from C over the library's own NCCL
+    # communicator (adg_run_timed_mgpu); ADG_MGPU_PY=1 keeps the per-step Python loop
+    native = world > 1 and not staged and os.environ.get("ADG_MGPU_PY") != "1"
+    if native:
+        drv.init_native_comm()
     K = args.steps
     clocks = ClockSampler(local)
     seg_ms, kern_ms, recs = [], 0.0, []
@@ -286,6 +291,17 @@ def main():
             h.call("adg_run_timed", n, tout)
             seg_ms.append(tout[0])
             kern_ms += tout[1]
+        elif native:
+            barrier()
+            torch.cuda.synchronize()
+            if not clocks_started:
+                clocks.start()
+                clocks_started = True
+                time.sleep(0.05)
+            seg, kern = drv.run_timed(n)
+            barrier()
+            seg_ms.append(seg)
+            kern_ms += kern
         else:
             ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n)]
             start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -402,6 +418,9 @@ def main():
                        "driver": args.mode,
                        "nodes": cells * (p + 1) ** d, "dof": dofs,
                        "parallelism": f"x-slab x{world}" if world > 1 else "single GPU",
+                       "exchange": (None if world == 1 else "gloo staged (functional only)" if staged
+                                    else "library NCCL comm, steps enqueued from C" if native
+                                    else "torch.distributed NCCL, per-step Python loop"),
                        "l2": "no flush: per-step working set (Q,D r/w + 2 trace parities) "
                              f"{roofline.bytes_step(d, p, cells) / 1e6:.0f} MB > 126 MB L2",
                        "episode_steps": E, "episodes": len(seg_ms),

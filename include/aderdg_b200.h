@@ -202,6 +202,20 @@ adg_status adg_flush_l2(adg_handle* h);
  * launches (rerun pass + sweep), both measured on the handle's stream. */
 adg_status adg_run_timed(adg_handle* h, int steps, double* out);
 
+/* Multi-GPU steps enqueued from C (no per-step Python): the library opens its own
+ * NCCL communicator (libnccl.so.2, resolved at run time) over the slab ranks.
+ * adg_nccl_unique_id fills 128 bytes on rank 0 (ncclGetUniqueId); the host
+ * broadcasts them; every rank calls adg_nccl_init.  adg_run_timed_mgpu then
+ * enqueues `steps` overlapped slab steps (rerun -> { grouped ncclSend/ncclRecv of
+ * the boundary face records on the comm stream || interior planes } -> boundary
+ * planes -> ncclAllReduce MAX of ADG_BUF_REDUCE -> finish) with the same events
+ * and outputs as adg_run_timed.  world = 1 with halo_mode = 1 exchanges with
+ * itself (the single-GPU test of this path).  Replaces the Python per-step loop
+ * of parallel.SlabDriver.enqueue_step. */
+adg_status adg_nccl_unique_id(unsigned char* out128);
+adg_status adg_nccl_init(adg_handle* h, const unsigned char* id128, int rank, int world);
+adg_status adg_run_timed_mgpu(adg_handle* h, int steps, double* out);
+
 #ifdef __cplusplus
 }
 #endif

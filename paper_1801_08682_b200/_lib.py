@@ -31,7 +31,7 @@ EXPORTS = (
     "adg_phase_seed_finish", "adg_phase_rerun", "adg_phase_sweep",
     "adg_phase_finish", "adg_trace_parity", "adg_flush_l2", "adg_reset", "adg_set_dt_new",
     "adg_run_timed", "adg_phase_sweep_part", "adg_set_limiter", "adg_troubled_flags",
-    "adg_step_host",
+    "adg_step_host", "adg_nccl_unique_id", "adg_nccl_init", "adg_run_timed_mgpu",
 )
 
 
@@ -123,6 +123,9 @@ def load_library(path=None):
         "adg_reset": (ctypes.c_int, [H]),
         "adg_set_dt_new": (ctypes.c_int, [H, ctypes.c_double]),
         "adg_run_timed": (ctypes.c_int, [H, ctypes.c_int, dp]),
+        "adg_nccl_unique_id": (ctypes.c_int, [ctypes.POINTER(ctypes.c_ubyte)]),
+        "adg_nccl_init": (ctypes.c_int, [H, ctypes.POINTER(ctypes.c_ubyte), ctypes.c_int, ctypes.c_int]),
+        "adg_run_timed_mgpu": (ctypes.c_int, [H, ctypes.c_int, dp]),
     }
     for name, (res, args) in proto.items():
         fn = getattr(lib, name)

@@ -7,6 +7,8 @@
 // host synchronisation; adg_step syncs once at the end, adg_run only after
 // the last step.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 #include <stdio.h>
 #include <string.h>
 #include <math.h>
@@ -319,6 +321,45 @@ bool dispatch_for(int d, int p, int system, Dispatch* out) {
 
 }  // namespace
 
+// NCCL entry points resolved at run time (torch has already loaded libnccl.so.2
+// in the bench / test processes; no link-time dependency of the library)
+struct NcclApi {
+  bool ok = false;
+  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclGroupStart) groupStart = nullptr;
+  decltype(&ncclGroupEnd) groupEnd = nullptr;
+  decltype(&ncclAllReduce) allReduce = nullptr;
+  decltype(&ncclGetErrorString) errorString = nullptr;
+};
+
+static NcclApi& nccl_api() {
+  static NcclApi a;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (lib) {
+      a.getUniqueId = (decltype(a.getUniqueId))dlsym(lib, "ncclGetUniqueId");
+      a.commInitRank = (decltype(a.commInitRank))dlsym(lib, "ncclCommInitRank");
+      a.commDestroy = (decltype(a.commDestroy))dlsym(lib, "ncclCommDestroy");
+      a.send = (decltype(a.send))dlsym(lib, "ncclSend");
+      a.recv = (decltype(a.recv))dlsym(lib, "ncclRecv");
+      a.groupStart = (decltype(a.groupStart))dlsym(lib, "ncclGroupStart");
+      a.groupEnd = (decltype(a.groupEnd))dlsym(lib, "ncclGroupEnd");
+      a.allReduce = (decltype(a.allReduce))dlsym(lib, "ncclAllReduce");
+      a.errorString = (decltype(a.errorString))dlsym(lib, "ncclGetErrorString");
+      a.ok = a.getUniqueId && a.commInitRank && a.commDestroy && a.send && a.recv && a.groupStart &&
+             a.groupEnd && a.allReduce && a.errorString;
+    }
+  }
+  return a;
+}
+
 struct adg_handle {
   adg_config cfg;
   int n = 0, m = 0, NS = 0, NF = 0, REC = 0, K = 0;
@@ -366,6 +407,11 @@ struct adg_handle {
   double lim_cfl = 0.9;
   // adg_step_host: copy streams and per-chunk events
   cudaStream_t copy_in = nullptr, copy_out = nullptr;
+  // library-owned NCCL communicator of the slab ranks (adg_nccl_init)
+  ncclComm_t comm = nullptr;
+  int comm_rank = 0, comm_world = 1;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t comm_ev[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> chunk_ev;
   StepRecord* rec_host = nullptr;      // pinned landing slot of the step record
   bool hst_fresh = false;              // hst mirrors the device (no phase call since the last pull)
@@ -644,6 +690,10 @@ void adg_destroy(adg_handle* h) {
     if (b) cudaFree(b);
   for (cudaEvent_t e : h->chunk_ev) cudaEventDestroy(e);
   if (h->copy_in) cudaStreamDestroy(h->copy_in);
+  if (h->comm) nccl_api().commDestroy(h->comm);
+  if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
+  for (cudaEvent_t e : h->comm_ev)
+    if (e) cudaEventDestroy(e);
   if (h->rec_host) cudaFreeHost(h->rec_host);
   if (h->copy_out) cudaStreamDestroy(h->copy_out);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
@@ -1053,6 +1103,123 @@ adg_status adg_run_timed(adg_handle* h, int steps, double* out) {
     s = adg_phase_sweep(h);
     CUDA_TRY(h, cudaEventRecord(ev[5 + 4 * i], h->stream));
     if (s != ADG_OK) break;
+    s = adg_phase_finish(h);
+  }
+  CUDA_TRY(h, cudaEventRecord(ev[1], h->stream));
+  CUDA_TRY(h, cudaEventSynchronize(ev[1]));
+  float ms = 0.f;
+  CUDA_TRY(h, cudaEventElapsedTime(&ms, ev[0], ev[1]));
+  out[0] = ms;
+  double kern = 0.0;
+  for (int i = 0; i < steps; ++i) {
+    float a = 0.f, b = 0.f;
+    CUDA_TRY(h, cudaEventElapsedTime(&a, ev[2 + 4 * i], ev[3 + 4 * i]));
+    CUDA_TRY(h, cudaEventElapsedTime(&b, ev[4 + 4 * i], ev[5 + 4 * i]));
+    kern += a + b;
+  }
+  out[1] = kern;
+  for (auto& e : ev) cudaEventDestroy(e);
+  if (s != ADG_OK) return s;
+  s = pull_state(h);
+  if (s != ADG_OK) return s;
+  return status_from_state(h);
+}
+
+// ---------------------------------------------------------------------------
+// Multi-GPU slab steps enqueued from C with the library's own NCCL communicator.
+#define NCCL_TRY(h, call)                                                           \
+  do {                                                                              \
+    ncclResult_t r_ = (call);                                                       \
+    if (r_ != ncclSuccess) return fail(h, ADG_ERR_RUNTIME, nccl_api().errorString(r_)); \
+  } while (0)
+
+adg_status adg_nccl_unique_id(unsigned char* out128) {
+  if (!out128) return ADG_ERR_CONFIG;
+  NcclApi& n = nccl_api();
+  if (!n.ok) return ADG_ERR_RUNTIME;
+  ncclUniqueId id;
+  if (n.getUniqueId(&id) != ncclSuccess) return ADG_ERR_RUNTIME;
+  static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+  memcpy(out128, &id, sizeof id);
+  return ADG_OK;
+}
+
+adg_status adg_nccl_init(adg_handle* h, const unsigned char* id128, int rank, int world) {
+  if (!h || !id128) return ADG_ERR_CONFIG;
+  if (world != h->cfg.world || rank != h->cfg.rank)
+    return fail(h, ADG_ERR_CONFIG, "adg_nccl_init: rank/world differ from the slab configuration");
+  NcclApi& n = nccl_api();
+  if (!n.ok) return fail(h, ADG_ERR_RUNTIME, "libnccl.so.2 not found");
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  if (h->comm) { n.commDestroy(h->comm); h->comm = nullptr; }
+  ncclUniqueId id;
+  memcpy(&id, id128, sizeof id);
+  NCCL_TRY(h, n.commInitRank(&h->comm, world, id, rank));
+  h->comm_rank = rank;
+  h->comm_world = world;
+  if (!h->comm_stream) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
+  for (auto& e : h->comm_ev)
+    if (!e) CUDA_TRY(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return ADG_OK;
+}
+
+// the ring exchange of the boundary face records of parity `par` on the comm stream
+// (the same four slices as parallel.HaloExchange.views; every rank sends to next first,
+// so with world 2 / 1 the messages of one peer pair match in issue order)
+static adg_status enqueue_halo(adg_handle* h, int par) {
+  NcclApi& n = nccl_api();
+  double* tr = h->tr[par];
+  const size_t nrec = (size_t)h->plane_cells * h->REC;
+  const long long P = h->planes_local, pc = h->plane_cells;
+  double* send_prev = tr + (0 * h->slots + pc) * h->REC;             // low-x records, first plane
+  double* recv_next = tr + (0 * h->slots + (P + 1) * pc) * h->REC;   // halo-hi
+  double* send_next = tr + (1 * h->slots + P * pc) * h->REC;         // high-x records, last plane
+  double* recv_prev = tr + (1 * h->slots + 0) * h->REC;              // halo-lo
+  const int next = (h->comm_rank + 1) % h->comm_world, prev = (h->comm_rank + h->comm_world - 1) % h->comm_world;
+  CUDA_TRY(h, cudaEventRecord(h->comm_ev[0], h->stream));            // after the rerun pass
+  CUDA_TRY(h, cudaStreamWaitEvent(h->comm_stream, h->comm_ev[0], 0));
+  NCCL_TRY(h, n.groupStart());
+  NCCL_TRY(h, n.send(send_next, nrec, ncclFloat64, next, h->comm, h->comm_stream));
+  NCCL_TRY(h, n.recv(recv_prev, nrec, ncclFloat64, prev, h->comm, h->comm_stream));
+  NCCL_TRY(h, n.send(send_prev, nrec, ncclFloat64, prev, h->comm, h->comm_stream));
+  NCCL_TRY(h, n.recv(recv_next, nrec, ncclFloat64, next, h->comm, h->comm_stream));
+  NCCL_TRY(h, n.groupEnd());
+  CUDA_TRY(h, cudaEventRecord(h->comm_ev[1], h->comm_stream));
+  return ADG_OK;
+}
+
+adg_status adg_run_timed_mgpu(adg_handle* h, int steps, double* out) {
+  if (!h || !out || steps < 1) return ADG_ERR_CONFIG;
+  if (!h->comm) return fail(h, ADG_ERR_CONFIG, "adg_run_timed_mgpu needs adg_nccl_init");
+  if (h->hst.status) return status_from_state(h);
+  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+  if (!straightforward(h) && h->sweep_index == 0)
+    return fail(h, ADG_ERR_CONFIG, "adg_run_timed_mgpu needs a primed driver (run one step first)");
+  const bool exchange = h->comm_world > 1 || h->cfg.halo_mode == 1;
+  std::vector<cudaEvent_t> ev(4 * (size_t)steps + 2);
+  for (auto& e : ev) CUDA_TRY(h, cudaEventCreate(&e));
+  adg_status s = ADG_OK;
+  CUDA_TRY(h, cudaEventRecord(ev[0], h->stream));
+  for (int i = 0; i < steps && s == ADG_OK; ++i) {
+    CUDA_TRY(h, cudaEventRecord(ev[2 + 4 * i], h->stream));
+    s = adg_phase_rerun(h);
+    CUDA_TRY(h, cudaEventRecord(ev[3 + 4 * i], h->stream));
+    if (s != ADG_OK) break;
+    CUDA_TRY(h, cudaEventRecord(ev[4 + 4 * i], h->stream));
+    if (exchange) {
+      s = enqueue_halo(h, adg_trace_parity(h));
+      if (s == ADG_OK) s = adg_phase_sweep_part(h, ADG_PART_INTERIOR);
+      if (s == ADG_OK) {
+        CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->comm_ev[1], 0));
+        s = adg_phase_sweep_part(h, ADG_PART_BOUNDARY);
+      }
+    } else {
+      s = adg_phase_sweep(h);
+    }
+    CUDA_TRY(h, cudaEventRecord(ev[5 + 4 * i], h->stream));
+    if (s != ADG_OK) break;
+    if (h->comm_world > 1)
+      NCCL_TRY(h, nccl_api().allReduce(h->st, h->st, 2, ncclInt64, ncclMax, h->comm, h->stream));
     s = adg_phase_finish(h);
   }
   CUDA_TRY(h, cudaEventRecord(ev[1], h->stream));

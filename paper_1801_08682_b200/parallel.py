@@ -214,6 +214,32 @@ class SlabDriver:
         self.handle.call("adg_sync")
         return self.handle.lib.adg_step_count(self.handle.h)
 
+    def init_native_comm(self, group=None):
+        """Open the library's own NCCL communicator over the slab ranks
+        (adg_nccl_init): rank 0 draws the unique id, torch.distributed broadcasts it.
+        Afterwards run_timed() enqueues whole steps from C."""
+        import ctypes
+        uid = (ctypes.c_ubyte * 128)()
+        if self.rank == 0:
+            st = self.handle.lib.adg_nccl_unique_id(uid)
+            if st != 0:
+                raise RuntimeError("adg_nccl_unique_id failed (libnccl.so.2 not loadable?)")
+        if self.world > 1:
+            import torch.distributed as dist
+            box = [bytes(uid)]
+            dist.broadcast_object_list(box, src=0, group=group)
+            uid = (ctypes.c_ubyte * 128).from_buffer_copy(box[0])
+        self.handle.call("adg_nccl_init", uid, self.rank, self.world)
+        self.native_comm = True
+
+    def run_timed(self, steps):
+        """`steps` overlapped slab steps enqueued from C (adg_run_timed_mgpu);
+        returns (segment ms, sweep-kernel ms) measured on the launch stream."""
+        import ctypes
+        out = (ctypes.c_double * 2)()
+        self.handle.call("adg_run_timed_mgpu", int(steps), out)
+        return out[0], out[1]
+
     def local_state(self):
         lay = self.lay
         Q = np.empty(lay.state_doubles)
