@@ -179,21 +179,24 @@ __device__ __forceinline__ int trace_addr(int i0, int i1, int i2) {
 // warp 5 a 4-5 x (b 0-3 x c 4-5 | b 4-5 x c 0-3); warp 6 (24 lanes) a 0-5 x
 // b 4-5 x c 4-5.  Every warp's projections onto (a, b), (a, c), (b, c) have at
 // most 16 elements, so a gather that varies one index hits <= 16 distinct rows.
+// Within a warp each lane quad is a 2x2 block in (b, c) at fixed a: an 8-byte
+// shared load costs one wavefront when every quad reads <= 2 distinct doubles
+// (measured, tools/smem_wavefronts.cu: 16 bytes per quad per wavefront), so the
+// gathers that vary a or b (rows fixed in c or b) are single-wavefront.
 __device__ __forceinline__ void block_map_p5(int tid, int& a, int& b, int& c, bool& act) {
-  const int w = tid >> 5, l = tid & 31;
+  const int w = tid >> 5, l = tid & 31, q = l >> 2, db = (l >> 1) & 1, dc = l & 1;
   act = true;
-  if (w < 3) { a = 2 * w + (l >> 4); b = (l >> 2) & 3; c = l & 3; }
-  else if (w == 3) { a = l >> 3; b = (l >> 1) & 3; c = 4 + (l & 1); }
-  else if (w == 4) { a = l >> 3; b = 4 + (l & 1); c = (l >> 1) & 3; }
+  if (w < 3) { a = 2 * w + (q >> 2); b = 2 * ((q >> 1) & 1) + db; c = 2 * (q & 1) + dc; }
+  else if (w == 3) { a = q >> 1; b = 2 * (q & 1) + db; c = 4 + dc; }
+  else if (w == 4) { a = q >> 1; b = 4 + db; c = 2 * (q & 1) + dc; }
   else if (w == 5) {
-    const int u = l & 15;
-    a = 4 + (u >> 3);
-    if (l < 16) { b = (u >> 1) & 3; c = 4 + (u & 1); }
-    else { b = 4 + (u & 1); c = (u >> 1) & 3; }
+    const int u = q & 3;
+    a = 4 + (u >> 1);
+    if (q < 4) { b = 2 * (u & 1) + db; c = 4 + dc; }
+    else { b = 4 + db; c = 2 * (u & 1) + dc; }
   } else {
     act = l < 24;
-    const int u = act ? l : 0;
-    a = u >> 2; b = 4 + ((u >> 1) & 1); c = 4 + (u & 1);
+    a = act ? q : 0; b = 4 + db; c = 4 + dc;
   }
 }
 
