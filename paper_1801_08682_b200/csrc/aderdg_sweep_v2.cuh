@@ -1008,16 +1008,21 @@ sweep_kernel_v2(const SweepParams P) {
   }
 
   // ---------------- s_max over the space-time face traces ----------------
-  // tasks per face axis a (compile-time): (side, t, face node y), y fastest, so a
-  // warp gathers whole face planes with one address formula; per-thread maxima
-  // are reduced over the warp and merged with one shared atomic per warp and side
+  // tasks per face axis a (compile-time): (t, face node y, side), side fastest at
+  // NQ != 4: the two lanes of a pair read the same trace nodes, so every lane quad
+  // touches two distinct doubles per load (one wavefront, tools/smem_wavefronts.cu);
+  // per-thread maxima are reduced over the warp and merged with one shared atomic per
+  // warp and side
   double smx[2 * DIM];
 #pragma unroll
   for (int f = 0; f < 2 * DIM; ++f) smx[f] = 0.0;
 #pragma unroll
   for (int a = 0; a < DIM; ++a) {
     for (int e = tid; e < 2 * NQ * NF; e += THREADS) {
-      const int y = e % NF, st_ = e / NF, t = st_ % NQ, side = st_ / NQ;
+      // (NQ = 4 keeps y fastest: its Latin-cube trace layout is conflict-free per face plane)
+      const int side = (NQ == 4) ? e / (NQ * NF) : e & 1;
+      const int y = (NQ == 4) ? e % NF : (e >> 1) % NF;
+      const int t = (NQ == 4) ? (e / NF) % NQ : (e >> 1) / NF;
       const double* vec = side ? P.ops.right : P.ops.left;
       const int ya = y / NQ, yb = y % NQ;
       double qs[M];
@@ -1053,7 +1058,10 @@ sweep_kernel_v2(const SweepParams P) {
   for (int a = 0; a < DIM; ++a) {
     const int pst = (a == 0) ? P0 : (a == 1) ? P1 : 1;
     for (int e = tid; e < 2 * M * NF; e += THREADS) {
-      const int y = e % NF, sc = e / NF, c = sc % M, side = sc / M;
+      // side fastest at NQ != 4 (lane pairs share loads); NQ = 4 keeps y fastest
+      const int side = (NQ == 4) ? e / (M * NF) : e & 1;
+      const int y = (NQ == 4) ? e % NF : (e >> 1) % NF;
+      const int c = (NQ == 4) ? (e / NF) % M : (e >> 1) / NF;
       const double* vec = side ? P.ops.right : P.ops.left;
       const int ya = y / NQ, yb = y % NQ;
       const int pxb = (a == 0) ? ya * P1 + yb : (a == 1) ? ya * P0 + yb : ya * P0 + yb * P1;
