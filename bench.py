@@ -264,7 +264,11 @@ def main():
     # communicator (adg_run_timed_mgpu); ADG_MGPU_PY=1 keeps the per-step Python loop
     native = world > 1 and not staged and os.environ.get("ADG_MGPU_PY") != "1"
     if native:
-        drv.init_native_comm()
+        try:
+            drv.init_native_comm()
+        except RuntimeError as e:        # same verdict on every rank (parallel.SlabDriver)
+            print(f"[bench] native NCCL step loop unavailable ({e}); per-step Python loop", file=sys.stderr)
+            native = False
     K = args.steps
     clocks = ClockSampler(local)
     seg_ms, kern_ms, recs = [], 0.0, []

@@ -220,15 +220,19 @@ class SlabDriver:
         Afterwards run_timed() enqueues whole steps from C."""
         import ctypes
         uid = (ctypes.c_ubyte * 128)()
+        ok = True
         if self.rank == 0:
-            st = self.handle.lib.adg_nccl_unique_id(uid)
-            if st != 0:
-                raise RuntimeError("adg_nccl_unique_id failed (libnccl.so.2 not loadable?)")
+            ok = self.handle.lib.adg_nccl_unique_id(uid) == 0
         if self.world > 1:
+            # rank 0's verdict travels with the id, so every rank takes the same branch
             import torch.distributed as dist
-            box = [bytes(uid)]
+            box = [bytes(uid) if ok else b""]
             dist.broadcast_object_list(box, src=0, group=group)
-            uid = (ctypes.c_ubyte * 128).from_buffer_copy(box[0])
+            ok = len(box[0]) == 128
+            if ok:
+                uid = (ctypes.c_ubyte * 128).from_buffer_copy(box[0])
+        if not ok:
+            raise RuntimeError("adg_nccl_unique_id failed (libnccl.so.2 not loadable)")
         self.handle.call("adg_nccl_init", uid, self.rank, self.world)
         self.native_comm = True
 
