@@ -400,7 +400,7 @@ def main():
                "h2d_bytes_per_step": 8 * n_state * world, "d2h_bytes_per_step": 8 * n_state * world,
                "ms_per_step": 1e3 * e2e_s / K,
                "path": ("adg_step_host: pinned H2D + fused step + D2H per step, pipelined over "
-                        "9 plane chunks" if world == 1 else
+                        "up to 16 wave-aligned cell chunks" if world == 1 else
                         "adg_load_state (pinned H2D) + phase step + adg_store_state (D2H), per step")}
 
     cpu = None
