@@ -80,3 +80,68 @@ def test_halo_exchange_and_reduction(world):
             assert np.array_equal(hi[c], 1e6 * g_hi + 1e4 * 0 + 10 * c + np.arange(rec))
         assert red[0] == (world - 1) * 10
         assert 0x7FFFFFFFFFFFFFFF - red[1] == 100     # min error key wins
+
+
+class _FakeLib:
+    """Stands in for the C library: rank 0's unique-id call succeeds or fails."""
+
+    def __init__(self, ok):
+        self.ok = ok
+
+    def adg_nccl_unique_id(self, buf):
+        if not self.ok:
+            return 4
+        for i in range(128):
+            buf[i] = (7 * i + 3) % 256
+        return 0
+
+
+class _FakeHandle:
+    def __init__(self, ok):
+        self.lib = _FakeLib(ok)
+        self.calls = []
+
+    def call(self, name, *args):
+        self.calls.append((name, bytes(args[0]), args[1], args[2]))
+
+
+def _native_worker(rank, world, port, ok, result_q):
+    from paper_1801_08682_b200.parallel import SlabDriver
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    drv = object.__new__(SlabDriver)          # host logic only: no device handle
+    drv.rank, drv.world = rank, world
+    drv.handle = _FakeHandle(ok if rank == 0 else True)
+    try:
+        drv.init_native_comm()
+        result_q.put((rank, "ok", drv.handle.calls))
+    except RuntimeError:
+        result_q.put((rank, "raised", drv.handle.calls))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("ok", [True, False])
+def test_native_comm_init_is_collective(ok):
+    """SlabDriver.init_native_comm: rank 0's unique id (or its failure) reaches every
+    rank, so all ranks open the library communicator with the same id or all fall
+    back together (no rank left waiting in ncclCommInitRank)."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_native_worker, args=(r, world, port, ok, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    if ok:
+        assert all(r[1] == "ok" for r in res)
+        ids = {r[2][0][1] for r in res}
+        assert len(ids) == 1 and len(next(iter(ids))) == 128
+        assert [r[2][0][2] for r in res] == [0, 1] and all(r[2][0][3] == world for r in res)
+    else:
+        assert all(r[1] == "raised" and r[2] == [] for r in res)
