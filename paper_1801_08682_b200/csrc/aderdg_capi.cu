@@ -407,6 +407,8 @@ struct adg_handle {
   double lim_cfl = 0.9;
   // adg_step_host: copy streams and per-chunk events
   cudaStream_t copy_in = nullptr, copy_out = nullptr;
+  cudaStream_t sweep_st[4] = {nullptr, nullptr, nullptr, nullptr};   // concurrent chunk sweeps
+  std::vector<cudaEvent_t> trace_ev;   // ADG_HOST_TRACE timeline (timing events)
   // library-owned NCCL communicator of the slab ranks (adg_nccl_init)
   ncclComm_t comm = nullptr;
   int comm_rank = 0, comm_world = 1;
@@ -697,6 +699,9 @@ void adg_destroy(adg_handle* h) {
     if (e) cudaEventDestroy(e);
   if (h->rec_host) cudaFreeHost(h->rec_host);
   if (h->copy_out) cudaStreamDestroy(h->copy_out);
+  for (cudaStream_t x : h->sweep_st)
+    if (x) cudaStreamDestroy(x);
+  for (cudaEvent_t e : h->trace_ev) cudaEventDestroy(e);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   delete h;
 }
@@ -1294,6 +1299,8 @@ adg_status adg_run_timed_mgpu(adg_handle* h, int steps, double* out) {
 static adg_status ensure_copy_streams(adg_handle* h) {
   if (!h->copy_in) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->copy_in, cudaStreamNonBlocking));
   if (!h->copy_out) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->copy_out, cudaStreamNonBlocking));
+  for (cudaStream_t& x : h->sweep_st)
+    if (!x) CUDA_TRY(h, cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
   if (!h->rec_host) CUDA_TRY(h, cudaMallocHost(&h->rec_host, sizeof(StepRecord)));
   if (h->chunk_ev.empty()) {
     h->chunk_ev.resize(3 * ADG_HOST_CHUNKS_MAX + 1);
@@ -1302,11 +1309,12 @@ static adg_status ensure_copy_streams(adg_handle* h) {
   return ADG_OK;
 }
 
-static adg_status launch_range(adg_handle* h, int mode, long long first, long long count) {
+static adg_status launch_range(adg_handle* h, int mode, long long first, long long count,
+                               cudaStream_t st) {
   if (count <= 0) return ADG_OK;
   SweepParams P = sweep_params(h, mode);
   P.cell_a = (int)first;
-  h->disp.sweep(P, (unsigned)count, h->stream);
+  h->disp.sweep(P, (unsigned)count, st);
   return cuda_check(h, cudaGetLastError(), "sweep launch");
 }
 
@@ -1339,9 +1347,33 @@ adg_status adg_step_host(adg_handle* h, const double* Q_in, double* Q_out, adg_s
     wave = (long long)dev_sms * per_sm;
   }
   long long waves = (C + wave - 1) / wave;
-  const int nch = (int)(waves < want ? waves : want);
+  // ADG_HOST_WAVES="1,2,4,...": explicit waves per chunk (the remainder goes to the last)
+  static const std::vector<int> sched = [] {
+    std::vector<int> v;
+    if (const char* e = getenv("ADG_HOST_WAVES"))
+      for (const char* q = e; *q;) {
+        const int w = atoi(q);
+        if (w > 0 && (int)v.size() < ADG_HOST_CHUNKS_MAX) v.push_back(w);
+        while (*q && *q != ',') ++q;
+        if (*q == ',') ++q;
+      }
+    return v;
+  }();
+  int nch = (int)(waves < want ? waves : want);
+  std::vector<long long> wcut;
+  if (!sched.empty()) {
+    long long acc = 0;
+    wcut.push_back(0);
+    for (int w : sched) {
+      if (acc >= waves) break;
+      acc += w;
+      wcut.push_back(acc < waves ? acc : waves);
+    }
+    wcut.back() = waves;
+    nch = (int)wcut.size() - 1;
+  }
   auto cell_of = [&](int i) {
-    const long long w = waves * i / nch;                 // whole waves per chunk
+    const long long w = wcut.empty() ? waves * i / nch : wcut[i];   // whole waves per chunk
     return w * wave < C ? w * wave : C;
   };
   cudaEvent_t* ev_in = h->chunk_ev.data();
@@ -1371,17 +1403,44 @@ adg_status adg_step_host(adg_handle* h, const double* Q_in, double* Q_out, adg_s
       CUDA_TRY(h, cudaEventRecord(ev_in[i], h->copy_in));
     }
   }
+  // ADG_HOST_SWEEP_STREAMS=2..4: chunk sweeps on rotating streams (they are
+  // independent: order-free atomics into the step state).  Measured cfg 2: no gain
+  // over one stream (1.434 vs 1.423 ms/step at 16 chunks) -- the step is bound by the
+  // PCIe copies, whose concurrent rate varies 1.06-1.35 ms per 2 x 50 MB between runs
+  static const int nst = [] {
+    const char* v = getenv("ADG_HOST_SWEEP_STREAMS");
+    const int c = v ? atoi(v) : 1;
+    return c < 1 ? 1 : (c > 4 ? 4 : c);
+  }();
+  static const bool trace = getenv("ADG_HOST_TRACE") != nullptr;
+  cudaEvent_t* te = nullptr;
+  if (trace) {
+    if ((int)h->trace_ev.size() < 3 * nch + 2) {
+      for (cudaEvent_t e : h->trace_ev) cudaEventDestroy(e);
+      h->trace_ev.assign(3 * nch + 2, nullptr);
+      for (auto& e : h->trace_ev) CUDA_TRY(h, cudaEventCreate(&e));
+    }
+    te = h->trace_ev.data();
+    CUDA_TRY(h, cudaEventRecord(te[0], h->stream));
+  }
+  if (whole) CUDA_TRY(h, cudaEventRecord(ev_start, h->stream));   // Q resident (+ priming / rerun)
   const int mode = MODE_NORMAL;
   for (int i = 0; i < nch; ++i) {
     const long long c0 = cell_of(i), c1 = cell_of(i + 1);
-    if (!whole) CUDA_TRY(h, cudaStreamWaitEvent(h->stream, ev_in[i], 0));
-    if ((s = launch_range(h, mode, c0, c1 - c0)) != ADG_OK) return s;
-    CUDA_TRY(h, cudaEventRecord(ev_sw[i], h->stream));
+    cudaStream_t st = nst == 1 ? h->stream : h->sweep_st[i % nst];
+    CUDA_TRY(h, cudaStreamWaitEvent(st, whole ? ev_start : ev_in[i], 0));
+    if (te && !whole) CUDA_TRY(h, cudaEventRecord(te[1 + i], st));
+    if ((s = launch_range(h, mode, c0, c1 - c0, st)) != ADG_OK) return s;
+    CUDA_TRY(h, cudaEventRecord(ev_sw[i], st));
+    if (te) CUDA_TRY(h, cudaEventRecord(te[1 + nch + i], st));
     CUDA_TRY(h, cudaStreamWaitEvent(h->copy_out, ev_sw[i], 0));
     CUDA_TRY(h, cudaMemcpyAsync(Q_out + c0 * cell_doubles, h->Q + c0 * cell_doubles,
                                 sizeof(double) * (size_t)(c1 - c0) * cell_doubles, cudaMemcpyDeviceToHost,
                                 h->copy_out));
+    if (te) CUDA_TRY(h, cudaEventRecord(te[1 + 2 * nch + i], h->copy_out));
   }
+  if (nst > 1)
+    for (int i = 0; i < nch; ++i) CUDA_TRY(h, cudaStreamWaitEvent(h->stream, ev_sw[i], 0));
   if ((s = adg_phase_finish(h)) != ADG_OK) return s;
   // one sync for the state, the step record and the last chunk
   CUDA_TRY(h, cudaMemcpyAsync(&h->hst, h->st, sizeof(DevState), cudaMemcpyDeviceToHost, h->stream));
@@ -1389,6 +1448,22 @@ adg_status adg_step_host(adg_handle* h, const double* Q_in, double* Q_out, adg_s
                               cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   CUDA_TRY(h, cudaStreamSynchronize(h->copy_out));
+  if (te) {
+    CUDA_TRY(h, cudaEventRecord(te[3 * nch + 1], h->copy_out));
+    CUDA_TRY(h, cudaEventSynchronize(te[3 * nch + 1]));
+    float t = 0.f;
+    fprintf(stderr, "[adg_step_host] chunks %d streams %d whole %d\n", nch, nst, (int)whole);
+    for (int i = 0; i < nch; ++i) {
+      float a = 0.f, b = 0.f, c = 0.f;
+      if (!whole) cudaEventElapsedTime(&a, te[0], te[1 + i]);
+      cudaEventElapsedTime(&b, te[0], te[1 + nch + i]);
+      cudaEventElapsedTime(&c, te[0], te[1 + 2 * nch + i]);
+      fprintf(stderr, "  chunk %2d cells %6lld  in %.3f  swept %.3f  out %.3f ms\n", i,
+              cell_of(i + 1) - cell_of(i), a, b, c);
+    }
+    cudaEventElapsedTime(&t, te[0], te[3 * nch + 1]);
+    fprintf(stderr, "  end %.3f ms\n", t);
+  }
   h->hst_fresh = true;
   if ((s = status_from_state(h)) != ADG_OK) return s;
   if (out && h->hst.step == before + 1) {
