@@ -202,6 +202,13 @@ adg_status adg_flush_l2(adg_handle* h);
  * launches (rerun pass + sweep), both measured on the handle's stream. */
 adg_status adg_run_timed(adg_handle* h, int steps, double* out);
 
+/* adg_run_timed with options: flags & ADG_TIMED_KERNEL_EVENTS records CUDA events
+ * around every rerun / sweep launch (out[1] = their summed ms; without it out[1] = 0
+ * and the segment carries only its two bracketing events, which is what the
+ * throughput number is measured on).  adg_run_timed = flags ADG_TIMED_KERNEL_EVENTS. */
+#define ADG_TIMED_KERNEL_EVENTS 1
+adg_status adg_run_timed_ex(adg_handle* h, int steps, int flags, double* out);
+
 /* Multi-GPU steps enqueued from C (no per-step Python): the library opens its own
  * NCCL communicator (libnccl.so.2, resolved at run time) over the slab ranks.
  * adg_nccl_unique_id fills 128 bytes on rank 0 (ncclGetUniqueId); the host

@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 ADG_OK, ADG_ERR_CONFIG, ADG_ERR_NUMERICAL, ADG_ERR_RUNTIME, ADG_ERR_PREDICTOR = 0, 2, 3, 4, 5
 ADG_BUF_Q, ADG_BUF_D, ADG_BUF_TRACE0, ADG_BUF_TRACE1, ADG_BUF_REDUCE = range(5)
 ADG_PART_ALL, ADG_PART_INTERIOR, ADG_PART_BOUNDARY = range(3)
+ADG_TIMED_KERNEL_EVENTS = 1   # adg_run_timed_ex flags
 
 #: every symbol the header declares (checked by tests/test_abi.py)
 EXPORTS = (
@@ -30,7 +31,7 @@ EXPORTS = (
     "adg_last_error", "adg_layout_info", "adg_buffer", "adg_phase_seed",
     "adg_phase_seed_finish", "adg_phase_rerun", "adg_phase_sweep",
     "adg_phase_finish", "adg_trace_parity", "adg_flush_l2", "adg_reset", "adg_set_dt_new",
-    "adg_run_timed", "adg_phase_sweep_part", "adg_set_limiter", "adg_troubled_flags",
+    "adg_run_timed", "adg_run_timed_ex", "adg_phase_sweep_part", "adg_set_limiter", "adg_troubled_flags",
     "adg_step_host", "adg_nccl_unique_id", "adg_nccl_init", "adg_run_timed_mgpu",
 )
 
@@ -123,6 +124,7 @@ def load_library(path=None):
         "adg_reset": (ctypes.c_int, [H]),
         "adg_set_dt_new": (ctypes.c_int, [H, ctypes.c_double]),
         "adg_run_timed": (ctypes.c_int, [H, ctypes.c_int, dp]),
+        "adg_run_timed_ex": (ctypes.c_int, [H, ctypes.c_int, ctypes.c_int, dp]),
         "adg_nccl_unique_id": (ctypes.c_int, [ctypes.POINTER(ctypes.c_ubyte)]),
         "adg_nccl_init": (ctypes.c_int, [H, ctypes.POINTER(ctypes.c_ubyte), ctypes.c_int, ctypes.c_int]),
         "adg_run_timed_mgpu": (ctypes.c_int, [H, ctypes.c_int, dp]),

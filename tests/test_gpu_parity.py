@@ -297,3 +297,24 @@ def test_step_host_pipeline_equals_device_run(cuda_ok, d, L, p, steps, kw):
     lib = a.handle.lib
     assert lib.adg_sweep_count(a.handle.h) == b.sweep_count
     assert lib.adg_rerun_count(a.handle.h) == b.rerun_count
+
+
+@pytest.mark.parametrize("flags", [0, 1])
+@pytest.mark.parametrize("d,L,p,steps,kw", [(3, 2, 3, 5, {}), (2, 3, 3, 6, {"inject_rerun": True})])
+def test_run_timed_graph_equals_device_run(cuda_ok, flags, d, L, p, steps, kw):
+    """adg_run_timed_ex (the bench's captured step graph, with or without the per-launch
+    kernel events) after one primed step gives the adg_run state bitwise; the kernel
+    time is reported only when the events are on."""
+    import ctypes
+    from paper_1801_08682_b200 import _lib
+    Q0 = scenarios.build("bump", d, L, p, seed=5, noise=1e-2)
+    a = make_driver(Q0, d, L, p, kw, host_sync="manual")
+    a.run(steps=1)
+    out = (ctypes.c_double * 2)()
+    a.handle.call("adg_run_timed_ex", steps - 1, flags, out)
+    assert out[0] > 0.0
+    assert (out[1] > 0.0) == bool(flags & _lib.ADG_TIMED_KERNEL_EVENTS)
+    a.sync_state()
+    b = make_driver(Q0, d, L, p, kw, host_sync="run")
+    b.run(steps=steps)
+    assert np.array_equal(a.grid.Q, b.grid.Q)
