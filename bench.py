@@ -302,10 +302,9 @@ def main():
                 clocks.start()
                 clocks_started = True
                 time.sleep(0.05)
-            seg, kern = drv.run_timed(n)
+            seg, _ = drv.run_timed(n, flags=0)
             barrier()
             seg_ms.append(seg)
-            kern_ms += kern
         else:
             ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n)]
             start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -342,7 +341,7 @@ def main():
         first = False
     clk = clocks.stop()
     kern_seg_ms, replay_recs = sum(seg_ms), []
-    if world == 1:
+    if world == 1 or native:
         # instrumented replay of the timed segments (same initial states, same launch
         # sequence): CUDA events around every rerun / sweep launch give the kernel time
         kern_ms, kern_seg_ms, remaining, firstr = 0.0, 0.0, K, True
@@ -355,7 +354,12 @@ def main():
             n = min(remaining, max(1, E - warm))
             tout = (ctypes.c_double * 2)()
             s0 = h.lib.adg_step_count(h.h)
-            h.call("adg_run_timed_ex", n, _lib.ADG_TIMED_KERNEL_EVENTS, tout)
+            if world == 1:
+                h.call("adg_run_timed_ex", n, _lib.ADG_TIMED_KERNEL_EVENTS, tout)
+            else:
+                barrier()
+                tout[0], tout[1] = drv.run_timed(n, flags=_lib.ADG_TIMED_KERNEL_EVENTS)
+                barrier()
             kern_ms += tout[1]
             kern_seg_ms += tout[0]
             rr = h.step_records(s0 + 1, n)
@@ -473,7 +477,7 @@ def main():
                          "kernel_timing": ("CUDA events around every rerun / sweep launch in an "
                                            "instrumented replay of the timed steps (same states and "
                                            "launches); the timed graph carries only its two bracketing "
-                                           "events" if world == 1 else
+                                           "events" if (world == 1 or native) else
                                            "CUDA events around every sweep launch in the timed steps"),
                          "flops_per_step_per_gpu": flops / K if K else 0,
                          "peak_source": "profiles/fp64_peaks_r01.jsonl (measured DMMA m8n8k4; "

@@ -222,6 +222,8 @@ adg_status adg_run_timed_ex(adg_handle* h, int steps, int flags, double* out);
 adg_status adg_nccl_unique_id(unsigned char* out128);
 adg_status adg_nccl_init(adg_handle* h, const unsigned char* id128, int rank, int world);
 adg_status adg_run_timed_mgpu(adg_handle* h, int steps, double* out);
+/* adg_run_timed_mgpu with adg_run_timed_ex's flags. */
+adg_status adg_run_timed_mgpu_ex(adg_handle* h, int steps, int flags, double* out);
 
 #ifdef __cplusplus
 }

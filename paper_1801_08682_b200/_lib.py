@@ -32,7 +32,7 @@ EXPORTS = (
     "adg_phase_seed_finish", "adg_phase_rerun", "adg_phase_sweep",
     "adg_phase_finish", "adg_trace_parity", "adg_flush_l2", "adg_reset", "adg_set_dt_new",
     "adg_run_timed", "adg_run_timed_ex", "adg_phase_sweep_part", "adg_set_limiter", "adg_troubled_flags",
-    "adg_step_host", "adg_nccl_unique_id", "adg_nccl_init", "adg_run_timed_mgpu",
+    "adg_step_host", "adg_nccl_unique_id", "adg_nccl_init", "adg_run_timed_mgpu", "adg_run_timed_mgpu_ex",
 )
 
 
@@ -128,6 +128,7 @@ def load_library(path=None):
         "adg_nccl_unique_id": (ctypes.c_int, [ctypes.POINTER(ctypes.c_ubyte)]),
         "adg_nccl_init": (ctypes.c_int, [H, ctypes.POINTER(ctypes.c_ubyte), ctypes.c_int, ctypes.c_int]),
         "adg_run_timed_mgpu": (ctypes.c_int, [H, ctypes.c_int, dp]),
+        "adg_run_timed_mgpu_ex": (ctypes.c_int, [H, ctypes.c_int, ctypes.c_int, dp]),
     }
     for name, (res, args) in proto.items():
         fn = getattr(lib, name)

@@ -1242,6 +1242,10 @@ static adg_status enqueue_halo(adg_handle* h, int par) {
 }
 
 adg_status adg_run_timed_mgpu(adg_handle* h, int steps, double* out) {
+  return adg_run_timed_mgpu_ex(h, steps, ADG_TIMED_KERNEL_EVENTS, out);
+}
+
+adg_status adg_run_timed_mgpu_ex(adg_handle* h, int steps, int flags, double* out) {
   if (!h || !out || steps < 1) return ADG_ERR_CONFIG;
   if (!h->comm) return fail(h, ADG_ERR_CONFIG, "adg_run_timed_mgpu needs adg_nccl_init");
   if (h->hst.status) return status_from_state(h);
@@ -1253,12 +1257,15 @@ adg_status adg_run_timed_mgpu(adg_handle* h, int steps, double* out) {
   for (auto& e : ev) CUDA_TRY(h, cudaEventCreate(&e));
   adg_status s = ADG_OK;
   CUDA_TRY(h, cudaEventRecord(ev[0], h->stream));
+  // per-launch kernel events only on request (adg_run_timed_ex)
+  const bool step_ev = (flags & ADG_TIMED_KERNEL_EVENTS) != 0;
+  auto record = [&](cudaEvent_t e) { return step_ev ? cudaEventRecord(e, h->stream) : cudaSuccess; };
   for (int i = 0; i < steps && s == ADG_OK; ++i) {
-    CUDA_TRY(h, cudaEventRecord(ev[2 + 4 * i], h->stream));
+    CUDA_TRY(h, record(ev[2 + 4 * i]));
     s = adg_phase_rerun(h);
-    CUDA_TRY(h, cudaEventRecord(ev[3 + 4 * i], h->stream));
+    CUDA_TRY(h, record(ev[3 + 4 * i]));
     if (s != ADG_OK) break;
-    CUDA_TRY(h, cudaEventRecord(ev[4 + 4 * i], h->stream));
+    CUDA_TRY(h, record(ev[4 + 4 * i]));
     if (exchange) {
       s = enqueue_halo(h, adg_trace_parity(h));
       if (s == ADG_OK) s = adg_phase_sweep_part(h, ADG_PART_INTERIOR);
@@ -1269,7 +1276,7 @@ adg_status adg_run_timed_mgpu(adg_handle* h, int steps, double* out) {
     } else {
       s = adg_phase_sweep(h);
     }
-    CUDA_TRY(h, cudaEventRecord(ev[5 + 4 * i], h->stream));
+    CUDA_TRY(h, record(ev[5 + 4 * i]));
     if (s != ADG_OK) break;
     if (h->comm_world > 1)
       NCCL_TRY(h, nccl_api().allReduce(h->st, h->st, 2, ncclInt64, ncclMax, h->comm, h->stream));
@@ -1281,7 +1288,7 @@ adg_status adg_run_timed_mgpu(adg_handle* h, int steps, double* out) {
   CUDA_TRY(h, cudaEventElapsedTime(&ms, ev[0], ev[1]));
   out[0] = ms;
   double kern = 0.0;
-  for (int i = 0; i < steps; ++i) {
+  for (int i = 0; i < steps && step_ev; ++i) {
     float a = 0.f, b = 0.f;
     CUDA_TRY(h, cudaEventElapsedTime(&a, ev[2 + 4 * i], ev[3 + 4 * i]));
     CUDA_TRY(h, cudaEventElapsedTime(&b, ev[4 + 4 * i], ev[5 + 4 * i]));

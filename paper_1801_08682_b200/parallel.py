@@ -236,12 +236,13 @@ class SlabDriver:
         self.handle.call("adg_nccl_init", uid, self.rank, self.world)
         self.native_comm = True
 
-    def run_timed(self, steps):
-        """`steps` overlapped slab steps enqueued from C (adg_run_timed_mgpu);
-        returns (segment ms, sweep-kernel ms) measured on the launch stream."""
+    def run_timed(self, steps, flags=_lib.ADG_TIMED_KERNEL_EVENTS):
+        """`steps` overlapped slab steps enqueued from C (adg_run_timed_mgpu_ex);
+        returns (segment ms, sweep-kernel ms) measured on the launch stream (the
+        kernel ms only with flags & ADG_TIMED_KERNEL_EVENTS, else 0)."""
         import ctypes
         out = (ctypes.c_double * 2)()
-        self.handle.call("adg_run_timed_mgpu", int(steps), out)
+        self.handle.call("adg_run_timed_mgpu_ex", int(steps), int(flags), out)
         return out[0], out[1]
 
     def local_state(self):

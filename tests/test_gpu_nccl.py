@@ -71,7 +71,8 @@ def _run_native(port, out):
     a = SlabDriver(Q0, 3, 2, 3, 0, 1, 0, inject_rerun=True, halo_mode=1)
     a.init_native_comm()
     a.run(1)                      # priming step through the Python phase loop
-    a.run_timed(4)                # then whole steps enqueued from C over the library's comm
+    a.run_timed(2, flags=0)       # then whole steps enqueued from C over the library's comm
+    a.run_timed(2)                # (without / with the per-launch kernel events)
     qa = a.local_state()
     b = SlabDriver(Q0, 3, 2, 3, 0, 1, 0, inject_rerun=True)
     b.run(5)
