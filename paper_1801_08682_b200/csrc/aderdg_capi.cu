@@ -417,6 +417,8 @@ struct adg_handle {
   std::vector<cudaEvent_t> chunk_ev;
   StepRecord* rec_host = nullptr;      // pinned landing slot of the step record
   bool hst_fresh = false;              // hst mirrors the device (no phase call since the last pull)
+  bool has_next_cond = false;          // adg_run_timed_ex: the finish sets the next rerun node's condition
+  unsigned long long next_cond = 0;
 };
 
 constexpr int ADG_HOST_CHUNKS = 16;      // wave-aligned chunks of the pipelined host step (ADG_HOST_CHUNKS env;
@@ -502,6 +504,8 @@ static FinishParams finish_params(adg_handle* h, int priming, int seed) {
   F.creeping = h->cfg.creeping;
   F.inject_rerun = h->cfg.inject_rerun;
   F.straightforward = (h->cfg.driver_mode == 1 && !seed) ? 1 : 0;
+  F.has_cond = h->has_next_cond ? 1 : 0;
+  F.cond = h->next_cond;
   return F;
 }
 
@@ -1122,24 +1126,70 @@ adg_status adg_run_timed_ex(adg_handle* h, int steps, int flags, double* out) {
   // so the throughput run leaves them out and an instrumented replay measures the kernels
   const bool step_ev = (flags & ADG_TIMED_KERNEL_EVENTS) != 0;
   auto record = [&](cudaEvent_t e) { return step_ev ? record0(e) : cudaSuccess; };
+  // each step's rerun pass is an IF node whose condition the previous step's finish
+  // kernel sets: no rerun launch at all on the common no-rerun step (cfg 2: the pass's
+  // 19683 early-exit CTAs cost ~9 us/step, 0.564 -> 0.555 ms).  ADG_NO_COND_RERUN=1:
+  // plain rerun launches.
+  const bool cond = graph && !straightforward(h) && getenv("ADG_NO_COND_RERUN") == nullptr;
+  std::vector<cudaGraphConditionalHandle> hc;
+  cudaStream_t side = nullptr;
+  if (cond) {
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t cg = nullptr;
+    CUDA_TRY(h, cudaStreamGetCaptureInfo(cap, &cs, nullptr, &cg, nullptr, nullptr));
+    hc.resize(steps);
+    for (int i = 0; i < steps; ++i)   // default 1: the first step's pass checks rerun_next itself
+      CUDA_TRY(h, cudaGraphConditionalHandleCreate(&hc[i], cg, 1, cudaGraphCondAssignDefault));
+    CUDA_TRY(h, cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+  }
+  auto rerun_node = [&](int i) -> adg_status {
+    if (!cond) return adg_phase_rerun(h);
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t cg = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    CUDA_TRY(h, cudaStreamGetCaptureInfo(h->stream, &cs, nullptr, &cg, &deps, &nd));
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = hc[i];
+    np.conditional.type = cudaGraphCondTypeIf;
+    np.conditional.size = 1;
+    cudaGraphNode_t cn;
+    CUDA_TRY(h, cudaGraphAddNode(&cn, cg, deps, nd, &np));
+    CUDA_TRY(h, cudaStreamUpdateCaptureDependencies(h->stream, &cn, 1, cudaStreamSetCaptureDependencies));
+    CUDA_TRY(h, cudaStreamBeginCaptureToGraph(side, np.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                              cudaStreamCaptureModeRelaxed));
+    cudaStream_t keep = h->stream;
+    h->stream = side;
+    adg_status r = adg_phase_rerun(h);
+    h->stream = keep;
+    cudaGraph_t body = nullptr;
+    CUDA_TRY(h, cudaStreamEndCapture(side, &body));
+    return r;
+  };
   auto enqueue = [&]() -> adg_status {
     CUDA_TRY(h, record0(ev[0]));
     adg_status r = ADG_OK;
     for (int i = 0; i < steps && r == ADG_OK; ++i) {
       CUDA_TRY(h, record(ev[2 + 4 * i]));
-      r = adg_phase_rerun(h);
+      r = rerun_node(i);
       CUDA_TRY(h, record(ev[3 + 4 * i]));
       if (r != ADG_OK) break;
       CUDA_TRY(h, record(ev[4 + 4 * i]));
       r = adg_phase_sweep(h);
       CUDA_TRY(h, record(ev[5 + 4 * i]));
       if (r != ADG_OK) break;
+      h->has_next_cond = cond && i + 1 < steps;
+      if (h->has_next_cond) h->next_cond = hc[i + 1];
       r = adg_phase_finish(h);
+      h->has_next_cond = false;
     }
     CUDA_TRY(h, record0(ev[1]));
     return r;
   };
   s = enqueue();
+  h->has_next_cond = false;
+  if (side) cudaStreamDestroy(side);
   if (graph) {
     h->stream = run;
     cudaGraph_t g = nullptr;
