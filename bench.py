@@ -271,7 +271,7 @@ def main():
             native = False
     K = args.steps
     clocks = ClockSampler(local)
-    seg_ms, kern_ms, recs = [], 0.0, []
+    seg_ms, kern_ms, recs, launches = [], 0.0, [], 0
     remaining, first = K, True
     clocks_started = False
     while remaining > 0:
@@ -336,7 +336,15 @@ def main():
             h.call("adg_sync")
             seg_ms.append(start.elapsed_time(stop))
             kern_ms += sum(e[0].elapsed_time(e[1]) + e[2].elapsed_time(e[3]) for e in ev)
-        recs += h.step_records(step0 + 1, n)
+        seg_recs = h.step_records(step0 + 1, n)
+        recs += seg_recs
+        if world == 1 and os.environ.get("ADG_NO_COND_RERUN") is None:
+            # graph steps: sweep + finish, and the rerun pass only where its conditional
+            # node fires (the segment's first step, whose condition defaults to 1, and steps
+            # after a finish that asked for a rerun)
+            launches += 2 * n + 1 + sum(1 for r in seg_recs[1:] if r.reruns)
+        else:
+            launches += 3 * n     # rerun-pass sweep_kernel + sweep_kernel + finish_kernel
         remaining -= n
         first = False
     clk = clocks.stop()
@@ -483,7 +491,7 @@ def main():
                          "peak_source": "profiles/fp64_peaks_r01.jsonl (measured DMMA m8n8k4; "
                                         f"DFMA {dfma} TF/s) — MEASURED_PEAKS.json has no fp64 entry",
                          "hbm_alg_bytes_per_step": bytes_alg, "hbm_frac_of_measured": hbm_frac},
-            "gpu_launches": 3 * K,   # per step: rerun-pass sweep_kernel + sweep_kernel + finish_kernel
+            "gpu_launches": launches,
             "clocks": clk,
             "e2e": e2e,
             "cpu_baseline": cpu,
