@@ -338,7 +338,8 @@ def main():
             kern_ms += sum(e[0].elapsed_time(e[1]) + e[2].elapsed_time(e[3]) for e in ev)
         seg_recs = h.step_records(step0 + 1, n)
         recs += seg_recs
-        if world == 1 and os.environ.get("ADG_NO_COND_RERUN") is None:
+        graph_steps = world == 1 or (native and os.environ.get("ADG_MGPU_NO_GRAPH") is None)
+        if graph_steps and os.environ.get("ADG_NO_COND_RERUN") is None:
             # graph steps: sweep + finish, and the rerun pass only where its conditional
             # node fires (the segment's first step, whose condition defaults to 1, and steps
             # after a finish that asked for a rerun)

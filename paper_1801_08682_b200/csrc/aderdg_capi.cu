@@ -1094,6 +1094,34 @@ adg_status adg_buffer(adg_handle* h, int which, void** ptr, size_t* bytes) {
   return ADG_ERR_CONFIG;
 }
 
+// The rerun pass of one step as an IF node of the capture on h->stream (condition
+// handle hc, set by the previous step's finish kernel); the pass itself is captured
+// into the node's body through `side`.
+static adg_status capture_rerun_if(adg_handle* h, cudaGraphConditionalHandle hc, cudaStream_t side) {
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t cg = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  CUDA_TRY(h, cudaStreamGetCaptureInfo(h->stream, &cs, nullptr, &cg, &deps, &nd));
+  cudaGraphNodeParams np = {};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = hc;
+  np.conditional.type = cudaGraphCondTypeIf;
+  np.conditional.size = 1;
+  cudaGraphNode_t cn;
+  CUDA_TRY(h, cudaGraphAddNode(&cn, cg, deps, nd, &np));
+  CUDA_TRY(h, cudaStreamUpdateCaptureDependencies(h->stream, &cn, 1, cudaStreamSetCaptureDependencies));
+  CUDA_TRY(h, cudaStreamBeginCaptureToGraph(side, np.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                            cudaStreamCaptureModeRelaxed));
+  cudaStream_t keep = h->stream;
+  h->stream = side;
+  adg_status r = adg_phase_rerun(h);
+  h->stream = keep;
+  cudaGraph_t body = nullptr;
+  CUDA_TRY(h, cudaStreamEndCapture(side, &body));
+  return r;
+}
+
 adg_status adg_run_timed(adg_handle* h, int steps, double* out) {
   return adg_run_timed_ex(h, steps, ADG_TIMED_KERNEL_EVENTS, out);
 }
@@ -1143,29 +1171,7 @@ adg_status adg_run_timed_ex(adg_handle* h, int steps, int flags, double* out) {
     CUDA_TRY(h, cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
   }
   auto rerun_node = [&](int i) -> adg_status {
-    if (!cond) return adg_phase_rerun(h);
-    cudaStreamCaptureStatus cs;
-    cudaGraph_t cg = nullptr;
-    const cudaGraphNode_t* deps = nullptr;
-    size_t nd = 0;
-    CUDA_TRY(h, cudaStreamGetCaptureInfo(h->stream, &cs, nullptr, &cg, &deps, &nd));
-    cudaGraphNodeParams np = {};
-    np.type = cudaGraphNodeTypeConditional;
-    np.conditional.handle = hc[i];
-    np.conditional.type = cudaGraphCondTypeIf;
-    np.conditional.size = 1;
-    cudaGraphNode_t cn;
-    CUDA_TRY(h, cudaGraphAddNode(&cn, cg, deps, nd, &np));
-    CUDA_TRY(h, cudaStreamUpdateCaptureDependencies(h->stream, &cn, 1, cudaStreamSetCaptureDependencies));
-    CUDA_TRY(h, cudaStreamBeginCaptureToGraph(side, np.conditional.phGraph_out[0], nullptr, nullptr, 0,
-                                              cudaStreamCaptureModeRelaxed));
-    cudaStream_t keep = h->stream;
-    h->stream = side;
-    adg_status r = adg_phase_rerun(h);
-    h->stream = keep;
-    cudaGraph_t body = nullptr;
-    CUDA_TRY(h, cudaStreamEndCapture(side, &body));
-    return r;
+    return cond ? capture_rerun_if(h, hc[i], side) : adg_phase_rerun(h);
   };
   auto enqueue = [&]() -> adg_status {
     CUDA_TRY(h, record0(ev[0]));
@@ -1306,33 +1312,85 @@ adg_status adg_run_timed_mgpu_ex(adg_handle* h, int steps, int flags, double* ou
   std::vector<cudaEvent_t> ev(4 * (size_t)steps + 2);
   for (auto& e : ev) CUDA_TRY(h, cudaEventCreate(&e));
   adg_status s = ADG_OK;
-  CUDA_TRY(h, cudaEventRecord(ev[0], h->stream));
+  // As adg_run_timed_ex: the steps (NCCL calls included: the comm stream forks from and
+  // joins the capture through comm_ev) are captured into one CUDA graph with the rerun
+  // pass as a conditional node (ADG_MGPU_NO_GRAPH=1: plain stream launches).
+  const cudaStream_t run = h->stream;
+  cudaStream_t cap = nullptr;
+  const bool graph = getenv("ADG_MGPU_NO_GRAPH") == nullptr &&
+                     cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) == cudaSuccess &&
+                     cudaStreamBeginCapture(cap, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+  if (graph) h->stream = cap;
+  const unsigned rec_flags = graph ? cudaEventRecordExternal : cudaEventRecordDefault;
+  auto record0 = [&](cudaEvent_t e) { return cudaEventRecordWithFlags(e, h->stream, rec_flags); };
   // per-launch kernel events only on request (adg_run_timed_ex)
   const bool step_ev = (flags & ADG_TIMED_KERNEL_EVENTS) != 0;
-  auto record = [&](cudaEvent_t e) { return step_ev ? cudaEventRecord(e, h->stream) : cudaSuccess; };
-  for (int i = 0; i < steps && s == ADG_OK; ++i) {
-    CUDA_TRY(h, record(ev[2 + 4 * i]));
-    s = adg_phase_rerun(h);
-    CUDA_TRY(h, record(ev[3 + 4 * i]));
-    if (s != ADG_OK) break;
-    CUDA_TRY(h, record(ev[4 + 4 * i]));
-    if (exchange) {
-      s = enqueue_halo(h, adg_trace_parity(h));
-      if (s == ADG_OK) s = adg_phase_sweep_part(h, ADG_PART_INTERIOR);
-      if (s == ADG_OK) {
-        CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->comm_ev[1], 0));
-        s = adg_phase_sweep_part(h, ADG_PART_BOUNDARY);
-      }
-    } else {
-      s = adg_phase_sweep(h);
+  auto record = [&](cudaEvent_t e) { return step_ev ? record0(e) : cudaSuccess; };
+  const bool cond = graph && !straightforward(h) && getenv("ADG_NO_COND_RERUN") == nullptr;
+  std::vector<cudaGraphConditionalHandle> hc;
+  cudaStream_t side = nullptr;
+  auto enqueue = [&]() -> adg_status {
+    if (cond) {
+      cudaStreamCaptureStatus cs;
+      cudaGraph_t cg = nullptr;
+      CUDA_TRY(h, cudaStreamGetCaptureInfo(cap, &cs, nullptr, &cg, nullptr, nullptr));
+      hc.resize(steps);
+      for (int i = 0; i < steps; ++i)
+        CUDA_TRY(h, cudaGraphConditionalHandleCreate(&hc[i], cg, 1, cudaGraphCondAssignDefault));
+      CUDA_TRY(h, cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
     }
-    CUDA_TRY(h, record(ev[5 + 4 * i]));
-    if (s != ADG_OK) break;
-    if (h->comm_world > 1)
-      NCCL_TRY(h, nccl_api().allReduce(h->st, h->st, 2, ncclInt64, ncclMax, h->comm, h->stream));
-    s = adg_phase_finish(h);
+    CUDA_TRY(h, record0(ev[0]));
+    adg_status r = ADG_OK;
+    for (int i = 0; i < steps && r == ADG_OK; ++i) {
+      CUDA_TRY(h, record(ev[2 + 4 * i]));
+      r = cond ? capture_rerun_if(h, hc[i], side) : adg_phase_rerun(h);
+      CUDA_TRY(h, record(ev[3 + 4 * i]));
+      if (r != ADG_OK) break;
+      CUDA_TRY(h, record(ev[4 + 4 * i]));
+      if (exchange) {
+        r = enqueue_halo(h, adg_trace_parity(h));
+        if (r == ADG_OK) r = adg_phase_sweep_part(h, ADG_PART_INTERIOR);
+        if (r == ADG_OK) {
+          CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->comm_ev[1], 0));
+          r = adg_phase_sweep_part(h, ADG_PART_BOUNDARY);
+        }
+      } else {
+        r = adg_phase_sweep(h);
+      }
+      CUDA_TRY(h, record(ev[5 + 4 * i]));
+      if (r != ADG_OK) break;
+      if (h->comm_world > 1)
+        NCCL_TRY(h, nccl_api().allReduce(h->st, h->st, 2, ncclInt64, ncclMax, h->comm, h->stream));
+      h->has_next_cond = cond && i + 1 < steps;
+      if (h->has_next_cond) h->next_cond = hc[i + 1];
+      r = adg_phase_finish(h);
+      h->has_next_cond = false;
+    }
+    CUDA_TRY(h, record0(ev[1]));
+    return r;
+  };
+  s = enqueue();
+  h->has_next_cond = false;
+  if (side) cudaStreamDestroy(side);
+  if (graph) {
+    h->stream = run;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    const cudaError_t e1 = cudaStreamEndCapture(cap, &g);
+    cudaError_t e2 = cudaErrorUnknown;
+    if (e1 == cudaSuccess && s == ADG_OK) {
+      e2 = cudaGraphInstantiate(&ge, g, 0);
+      if (e2 == cudaSuccess) e2 = cudaGraphLaunch(ge, run);
+    }
+    if (ge) cudaGraphExecDestroy(ge);
+    if (g) cudaGraphDestroy(g);
+    cudaStreamDestroy(cap);
+    if (s == ADG_OK && (e1 != cudaSuccess || e2 != cudaSuccess))
+      return fail(h, ADG_ERR_RUNTIME, std::string("adg_run_timed_mgpu graph: ") +
+                                          cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
+  } else if (cap) {
+    cudaStreamDestroy(cap);
   }
-  CUDA_TRY(h, cudaEventRecord(ev[1], h->stream));
   CUDA_TRY(h, cudaEventSynchronize(ev[1]));
   float ms = 0.f;
   CUDA_TRY(h, cudaEventElapsedTime(&ms, ev[0], ev[1]));
