@@ -424,6 +424,7 @@ struct adg_handle {
 constexpr int ADG_HOST_CHUNKS = 16;      // wave-aligned chunks of the pipelined host step (ADG_HOST_CHUNKS env;
                                           // cfg 2: 16 -> 1.526 ms, 9 -> 1.557, 23 -> 1.784)
 constexpr int ADG_HOST_CHUNKS_MAX = 81;
+constexpr int ADG_TIMED_NO_PULL = 1 << 16;   // internal adg_run_timed_ex flag: adg_run's graph chunks
 
 static adg_status fail(adg_handle* h, adg_status code, const std::string& msg) {
   if (h) h->err = msg;
@@ -901,9 +902,27 @@ adg_status adg_run(adg_handle* h, int steps, adg_step_record* out) {
   while (done < steps) {
     const int chunk = (steps - done) < h->rec_cap ? (steps - done) : h->rec_cap;
     const int before = h->hst.step;
-    for (int i = 0; i < chunk; ++i) {
+    int i = 0;
+    if (!straightforward(h) && h->sweep_index == 0) {   // priming sweep + first step on the stream
       adg_status s = enqueue_step(h);
       if (s != ADG_OK) return s;
+      i = 1;
+    }
+    // single GPU, fused driver, no limiter: the remaining steps as one CUDA graph with the
+    // rerun pass as a conditional node (adg_run_timed_ex; bitwise the stream launches,
+    // tests/test_gpu_parity.py::test_run_timed_graph_equals_device_run).  ADG_RUN_NO_GRAPH=1:
+    // stream launches.
+    const bool graph = !straightforward(h) && h->cfg.world == 1 && h->cfg.halo_mode == 0 && !h->lim &&
+                       chunk - i >= 2 && getenv("ADG_RUN_NO_GRAPH") == nullptr;
+    if (graph) {
+      double tout[2];
+      adg_status s = adg_run_timed_ex(h, chunk - i, ADG_TIMED_NO_PULL, tout);
+      if (s != ADG_OK) return s;
+    } else {
+      for (; i < chunk; ++i) {
+        adg_status s = enqueue_step(h);
+        if (s != ADG_OK) return s;
+      }
     }
     adg_status s = pull_state(h);
     if (s != ADG_OK) return s;
@@ -1229,6 +1248,7 @@ adg_status adg_run_timed_ex(adg_handle* h, int steps, int flags, double* out) {
   out[1] = kern;
   for (auto& e : ev) cudaEventDestroy(e);
   if (s != ADG_OK) return s;
+  if (flags & ADG_TIMED_NO_PULL) return ADG_OK;     // adg_run pulls state and records itself
   s = pull_state(h);
   if (s != ADG_OK) return s;
   return status_from_state(h);

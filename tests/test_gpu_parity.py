@@ -5,6 +5,7 @@ Bar (BASELINE.json north_star): relative L-inf <= 1e-10 in fp64 after the
 stated number of steps, identical rerun steps, identical abort step/cell.
 """
 
+import os
 import numpy as np
 import pytest
 
@@ -316,5 +317,13 @@ def test_run_timed_graph_equals_device_run(cuda_ok, flags, d, L, p, steps, kw):
     assert (out[1] > 0.0) == bool(flags & _lib.ADG_TIMED_KERNEL_EVENTS)
     a.sync_state()
     b = make_driver(Q0, d, L, p, kw, host_sync="run")
-    b.run(steps=steps)
+    os.environ["ADG_RUN_NO_GRAPH"] = "1"     # the reference: adg_run's plain stream launches
+    try:
+        b.run(steps=steps)
+    finally:
+        os.environ.pop("ADG_RUN_NO_GRAPH", None)
     assert np.array_equal(a.grid.Q, b.grid.Q)
+    c = make_driver(Q0, d, L, p, kw, host_sync="run")
+    c.run(steps=steps)                       # adg_run's default: graph chunks
+    assert np.array_equal(c.grid.Q, b.grid.Q)
+    assert [r["reruns"] for r in c.step_records] == [r["reruns"] for r in b.step_records]
