@@ -225,6 +225,30 @@ adg_status adg_run_timed_mgpu(adg_handle* h, int steps, double* out);
 /* adg_run_timed_mgpu with adg_run_timed_ex's flags. */
 adg_status adg_run_timed_mgpu_ex(adg_handle* h, int steps, int flags, double* out);
 
+/* In-process multi-GPU group: the reference's parallel driver seam
+ * Driver(grid, kernels, tc, mode, parallel=True, n_workers=N) (src/scheduler.py:92-95,
+ * 126-130, thread pool over cells) as N x-slab handles of one grid on N GPUs of one
+ * process.  The caller creates handle i with cfg.rank = i, cfg.world = N and its own
+ * cfg.device; adg_group_init opens one NCCL clique over them (ncclCommInitAll);
+ * adg_group_seed / adg_group_run drive every handle from its own host thread with the
+ * step sequence of adg_run_timed_mgpu (halo exchange hidden behind the interior
+ * planes, MAX all-reduce of the step reduction).  out[k] = rank 0's records with the
+ * Picard counts summed over ranks. */
+adg_status adg_group_init(adg_handle** hs, int n);
+adg_status adg_group_seed(adg_handle** hs, int n);
+adg_status adg_group_run(adg_handle** hs, int n, int steps, adg_step_record* out);
+/* Visible CUDA devices (0 without a driver / GPU). */
+int adg_device_count(void);
+
+/* Per-handle launch options (defaults in brackets):
+ * ADG_OPT_GRAPH [1]       adg_run / adg_run_timed* capture their steps into one CUDA graph
+ * ADG_OPT_COND_RERUN [1]  the rerun pass is a conditional graph node
+ * ADG_OPT_HOST_CHUNKS [16] wave-aligned cell chunks of adg_step_host (1..81) */
+#define ADG_OPT_GRAPH 1
+#define ADG_OPT_COND_RERUN 2
+#define ADG_OPT_HOST_CHUNKS 3
+adg_status adg_set_option(adg_handle* h, int option, int value);
+
 #ifdef __cplusplus
 }
 #endif

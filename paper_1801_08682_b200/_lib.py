@@ -33,7 +33,10 @@ EXPORTS = (
     "adg_phase_finish", "adg_trace_parity", "adg_flush_l2", "adg_reset", "adg_set_dt_new",
     "adg_run_timed", "adg_run_timed_ex", "adg_phase_sweep_part", "adg_set_limiter", "adg_troubled_flags",
     "adg_step_host", "adg_nccl_unique_id", "adg_nccl_init", "adg_run_timed_mgpu", "adg_run_timed_mgpu_ex",
+    "adg_group_init", "adg_group_seed", "adg_group_run", "adg_set_option", "adg_device_count",
 )
+
+ADG_OPT_GRAPH, ADG_OPT_COND_RERUN, ADG_OPT_HOST_CHUNKS = 1, 2, 3
 
 
 class AdgConfig(ctypes.Structure):
@@ -71,6 +74,18 @@ class AdgLayout(ctypes.Structure):
 _lib = None
 
 
+def _preload_nccl():
+    """The library resolves NCCL with dlopen("libnccl.so.2") when a multi-GPU path
+    first needs it; make that the torch-bundled NCCL (the one torch.distributed
+    uses) even in processes that never import torch.  Absent: the system library."""
+    try:
+        import nvidia.nccl
+        base = list(nvidia.nccl.__path__)[0]
+        ctypes.CDLL(os.path.join(base, "lib", "libnccl.so.2"), mode=ctypes.RTLD_GLOBAL)
+    except (ImportError, OSError, IndexError):
+        pass
+
+
 def load_library(path=None):
     """Load (once) and prototype the CUDA library; raise if it is missing."""
     global _lib
@@ -80,6 +95,7 @@ def load_library(path=None):
     if not os.path.exists(p):
         raise DeviceError(f"native library {p} is missing: run `python -c 'import "
                           f"__graft_entry__ as g; g.build()'` (there is no CPU fallback)")
+    _preload_nccl()
     lib = ctypes.CDLL(p)
     H = ctypes.c_void_p
     dp = ctypes.POINTER(ctypes.c_double)
@@ -129,6 +145,12 @@ def load_library(path=None):
         "adg_nccl_init": (ctypes.c_int, [H, ctypes.POINTER(ctypes.c_ubyte), ctypes.c_int, ctypes.c_int]),
         "adg_run_timed_mgpu": (ctypes.c_int, [H, ctypes.c_int, dp]),
         "adg_run_timed_mgpu_ex": (ctypes.c_int, [H, ctypes.c_int, ctypes.c_int, dp]),
+        "adg_group_init": (ctypes.c_int, [ctypes.POINTER(H), ctypes.c_int]),
+        "adg_group_seed": (ctypes.c_int, [ctypes.POINTER(H), ctypes.c_int]),
+        "adg_group_run": (ctypes.c_int, [ctypes.POINTER(H), ctypes.c_int, ctypes.c_int,
+                                         ctypes.POINTER(AdgStepRecord)]),
+        "adg_set_option": (ctypes.c_int, [H, ctypes.c_int, ctypes.c_int]),
+        "adg_device_count": (ctypes.c_int, []),
     }
     for name, (res, args) in proto.items():
         fn = getattr(lib, name)

@@ -12,8 +12,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libaderdg_b200.so")
 SOURCES = [os.path.join(CSRC, "aderdg_capi.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, "aderdg_kernels.cuh"), os.path.join(CSRC, "aderdg_sweep_v2.cuh"),
-                  os.path.join(CSRC, "aderdg_sweep_ho.cuh"), os.path.join(CSRC, "aderdg_sweep_hoc.cuh"),
-                  os.path.join(CSRC, "aderdg_sweep_st.cuh"),
+                  os.path.join(CSRC, "aderdg_sweep_ho.cuh"),
                   os.path.join(CSRC, "aderdg_limiter.cuh"),
                   os.path.join(os.path.dirname(HERE), "include", "aderdg_b200.h")]
 

@@ -14,15 +14,15 @@
 #include <math.h>
 #include <limits.h>
 #include <stdlib.h>
+#include <atomic>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/aderdg_b200.h"
 #include "aderdg_kernels.cuh"
 #include "aderdg_sweep_v2.cuh"
 #include "aderdg_sweep_ho.cuh"
-#include "aderdg_sweep_hoc.cuh"
-#include "aderdg_sweep_st.cuh"
 #include "aderdg_limiter.cuh"
 
 using namespace adg;
@@ -31,27 +31,35 @@ namespace {
 
 typedef void (*launch_fn)(const SweepParams&, unsigned grid, cudaStream_t s);
 
+// The dynamic shared-memory opt-in (cudaFuncAttributeMaxDynamicSharedMemorySize)
+// is a property of the function *per device context*: a second handle on another
+// GPU of the same process (Driver(device=1), the in-process multi-GPU group) must
+// set it again.  One bit per device ordinal; setting it twice is harmless, so a
+// relaxed atomic is enough when several host threads launch concurrently.
+template <class K>
+void ensure_smem_optin(K kernel, size_t bytes, std::atomic<unsigned long long>& done) {
+  if (bytes <= 48 * 1024) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_relaxed) & bit) return;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  done.fetch_or(bit, std::memory_order_relaxed);
+}
+
 template <class PDE, int DIM, int NQ>
 void launch_sweep(const SweepParams& P, unsigned grid, cudaStream_t s) {
   using S = Shape<DIM, NQ, PDE::M>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(sweep_kernel<PDE, DIM, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)S::SMEM_BYTES);
-    attr = true;
-  }
+  static std::atomic<unsigned long long> optin{0};
+  ensure_smem_optin(sweep_kernel<PDE, DIM, NQ>, S::SMEM_BYTES, optin);
   sweep_kernel<PDE, DIM, NQ><<<grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
 }
 
 template <int NQ, int TS, bool DMMA, bool ROLLED = (NQ == 4), int MB = 0>
 void launch_sweep_v2(const SweepParams& P, unsigned grid, cudaStream_t s) {
   using S = ShapeV2<NQ, TS, DMMA, ROLLED, MB>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(sweep_kernel_v2<NQ, TS, DMMA, ROLLED, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)S::SMEM_BYTES);
-    attr = true;
-  }
+  static std::atomic<unsigned long long> optin{0};
+  ensure_smem_optin(sweep_kernel_v2<NQ, TS, DMMA, ROLLED, MB>, S::SMEM_BYTES, optin);
   sweep_kernel_v2<NQ, TS, DMMA, ROLLED, MB><<<grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
 }
 
@@ -107,83 +115,28 @@ bool dispatch_adv(int n, Dispatch* out) {
   return false;
 }
 
-template <int NQ, int LN = 2, int TM = 0>
+// High-order engine (3D, p = 6..9).  Derivative engine and time-line placement per
+// order, measured on cfg 3: DMMA tiles at n <= 9, the constant-bank
+// line engine at n = 10; the first node's old iterate in TMEM at n <= 8.
+template <int NQ>
 void launch_sweep_ho(const SweepParams& P, unsigned grid, cudaStream_t s) {
   using S = ShapeHO<NQ>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(sweep_kernel_ho<NQ, true, LN, TM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)S::SMEM_BYTES);
-    attr = true;
-  }
+  constexpr int LN = (NQ == 10 ? 1 : 0), TM = (NQ <= 8 ? 1 : 0);
+  static std::atomic<unsigned long long> optin{0};
+  ensure_smem_optin(sweep_kernel_ho<NQ, true, LN, TM>, S::SMEM_BYTES, optin);
   sweep_kernel_ho<NQ, true, LN, TM><<<grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
 }
 
-// the 2-CTA cluster variant of the high-order kernel: two CTAs per cell
 template <int NQ>
-void launch_sweep_hoc(const SweepParams& P, unsigned grid, cudaStream_t s) {
-  using S = ShapeHO<NQ>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(sweep_kernel_hoc<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM_BYTES);
-    attr = true;
-  }
-  sweep_kernel_hoc<NQ><<<2 * grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
-}
-
-int occ_hoc() { return 1; }
-
-int kernel_variant() {
-  // ADG_KERNEL=1: first-generation kernel; 2: time-split v2; 3 (default): v2 without time split
-  const char* v = getenv("ADG_KERNEL");
-  return v ? atoi(v) : 3;
-}
-
-void launch_sweep_st(const SweepParams& P, unsigned grid, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(sweep_kernel_st, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ShapeST::SMEM_BYTES);
-    attr = true;
-  }
-  sweep_kernel_st<<<grid, ShapeST::THREADS, ShapeST::SMEM_BYTES, s>>>(P);
-}
-
-Dispatch make_dispatch_st() {
-  static_assert(ShapeST::REC == Shape<3, 4>::REC, "record layout must match");
-  return Dispatch{&launch_sweep_st, ShapeST::REC};
-}
-
-// ADG_KERNEL=15 / 18 / 19: DMMA-tile / constant-bank line / lane-group line
-// derivative engines of the high-order kernel (A/B)
-template <int NQ, int LN, int TM = 0>
 int occ_ho() {
+  constexpr int LN = (NQ == 10 ? 1 : 0), TM = (NQ <= 8 ? 1 : 0);
   return occupancy_of(sweep_kernel_ho<NQ, true, LN, TM>, ShapeHO<NQ>::THREADS, ShapeHO<NQ>::SMEM_BYTES);
 }
 
 template <int NQ>
 Dispatch make_dispatch_ho() {
   static_assert(ShapeHO<NQ>::REC == Shape<3, NQ>::REC, "record layout must match");
-  const char* v = getenv("ADG_KERNEL");
-  const int var = v ? atoi(v) : 0;
-  if (var == 15) return Dispatch{&launch_sweep_ho<NQ, 0>, ShapeHO<NQ>::REC, &occ_ho<NQ, 0>};
-  if (var == 18) return Dispatch{&launch_sweep_ho<NQ, 1>, ShapeHO<NQ>::REC, &occ_ho<NQ, 1>};
-  if (var == 19) return Dispatch{&launch_sweep_ho<NQ, 2>, ShapeHO<NQ>::REC, &occ_ho<NQ, 2>};
-  // ADG_KERNEL=40 / 42 / 41: the default engine with the first node's time line / divergence
-  // history in TMEM, or neither
-  constexpr int LD = (NQ == 10 ? 1 : 0);
-  if (var == 40) return Dispatch{&launch_sweep_ho<NQ, LD, 1>, ShapeHO<NQ>::REC, &occ_ho<NQ, LD, 1>};
-  if (var == 42) return Dispatch{&launch_sweep_ho<NQ, LD, 2>, ShapeHO<NQ>::REC, &occ_ho<NQ, LD, 2>};
-  if constexpr (NQ % 2 == 0 && NQ >= 8) {
-    // ADG_KERNEL=45: half a cell per SM on a 2-CTA cluster (aderdg_sweep_hoc.cuh)
-    if (var == 45) return Dispatch{&launch_sweep_hoc<NQ>, ShapeHO<NQ>::REC, &occ_hoc};
-  }
-  if (var == 41) return Dispatch{&launch_sweep_ho<NQ, LD, 0>, ShapeHO<NQ>::REC, &occ_ho<NQ, LD, 0>};
-  // measured (cfg3, one B200): DMMA tiles win at n <= 9 (p=7: 6.55 vs 4.74 / 6.18 TF/s),
-  // the constant-bank lines at n = 10 (p=9: 6.89 vs 6.54 / 2.24 TF/s); the TMEM time line
-  // wins at n <= 8 (p=7: 7.03 vs 6.44 TF/s) and loses at n = 10 (7.29 vs 7.92: the extra
-  // registers spill under the 128-register cap)
-  constexpr int TD = (NQ <= 8) ? 1 : 0;
-  return Dispatch{&launch_sweep_ho<NQ, LD, TD>, ShapeHO<NQ>::REC, &occ_ho<NQ, LD, TD>};
+  return Dispatch{&launch_sweep_ho<NQ>, ShapeHO<NQ>::REC, &occ_ho<NQ>};
 }
 
 template <int NQ, int TS, bool DMMA, bool ROLLED, int MB>
@@ -208,10 +161,13 @@ struct LimDispatch {
 
 template <class PDE, int DIM>
 void launch_lim_detect(const LimParams& L, unsigned grid, size_t smem, cudaStream_t s) {
-  static size_t attr = 0;
-  if (smem > attr) {
+  // per device: the largest opt-in set so far (detection smem depends on p only)
+  static std::atomic<size_t> optin[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (smem > optin[dev & 63].load(std::memory_order_relaxed)) {
     cudaFuncSetAttribute(lim_detect_kernel<PDE, DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = smem;
+    optin[dev & 63].store(smem, std::memory_order_relaxed);
   }
   lim_detect_kernel<PDE, DIM><<<grid, 256, smem, s>>>(L);
 }
@@ -229,7 +185,7 @@ LimDispatch lim_dispatch_for(int d, int system) {
   return d == 2 ? make_lim_dispatch<EulerPDE<2>, 2>() : make_lim_dispatch<EulerPDE<3>, 3>();
 }
 
-// the generic kernel (the one with the limiter hooks) for every Euler (d, p)
+// the generic kernel (the one with the limiter / outflow hooks) for every Euler (d, p)
 bool dispatch_generic(int d, int p, Dispatch* out) {
   const int n = p + 1;
   if (d == 2) {
@@ -262,61 +218,24 @@ bool dispatch_generic(int d, int p, Dispatch* out) {
   return false;
 }
 
+// The product kernel of every (system, d, p): one instantiation each, no run-time
+// variant selection.  3D Euler: p = 3 sweep_kernel_v2 (DMMA axes 1-2, pipelined
+// slices), p = 5 sweep_kernel_v2 node blocks, p = 6..9 sweep_kernel_ho; the rest
+// (2D, 3D p <= 2, p = 4) run the generic kernel.
 bool dispatch_for(int d, int p, int system, Dispatch* out) {
   const int n = p + 1;
   if (system == 1) return d == 2 ? dispatch_adv<2>(n, out) : d == 3 ? dispatch_adv<3>(n, out) : false;
-  if (d == 2) {
+  if (d == 3) {
     switch (n) {
-      case 1: *out = make_dispatch<2, 1>(); return true;
-      case 2: *out = make_dispatch<2, 2>(); return true;
-      case 3: *out = make_dispatch<2, 3>(); return true;
-      case 4: *out = make_dispatch<2, 4>(); return true;
-      case 5: *out = make_dispatch<2, 5>(); return true;
-      case 6: *out = make_dispatch<2, 6>(); return true;
-      case 7: *out = make_dispatch<2, 7>(); return true;
-      case 8: *out = make_dispatch<2, 8>(); return true;
-      case 9: *out = make_dispatch<2, 9>(); return true;
-      case 10: *out = make_dispatch<2, 10>(); return true;
-    }
-  } else if (d == 3) {
-    switch (n) {
-      case 1: *out = make_dispatch<3, 1>(); return true;
-      case 2: *out = make_dispatch<3, 2>(); return true;
-      case 3: *out = make_dispatch<3, 3>(); return true;
-      case 4:
-        *out = kernel_variant() == 1 ? make_dispatch<3, 4>()
-             : kernel_variant() == 2 ? make_dispatch_v2<4, 2, true>()
-             : kernel_variant() == 5 ? make_dispatch_v2<4, 1, true, true>()
-             : kernel_variant() == 6 ? make_dispatch_st()
-             : kernel_variant() == 7 ? make_dispatch_v2<4, 1, true, false, 7>()
-             : kernel_variant() == 8 ? make_dispatch_v2<4, 1, true, false, 8>()
-             : kernel_variant() == 14 ? make_dispatch_v2<4, 1, true, false>()      // axis 1 through shared memory
-             : kernel_variant() == 16 ? make_dispatch_v2<4, 1, true, false, 16>()  // A1S, 8 CTAs/SM
-             : kernel_variant() == 20 ? make_dispatch_v2<4, 1, true, false, 20>()  // A1S + axis-0 partial sums
-             : kernel_variant() == 17 ? make_dispatch_v2<4, 1, true, false, 17>()  // A1S, 7 CTAs/SM
-             : kernel_variant() == 21 ? make_dispatch_v2<4, 1, true, false, 10>()  // A1S, slice at a time
-             : kernel_variant() == 22 ? make_dispatch_v2<4, 1, true, false, 11>()  // pipelined, DMMAs after the barrier
-             : make_dispatch_v2<4, 1, true, false, 14>();   // default: A1S + pipelined slices, DMMAs in the
-                                                            // producing interval (1.095e10 vs 1.091e10 vs 1.074e10)
-        return true;
-      case 5: *out = make_dispatch<3, 5>(); return true;
-      case 6:
-        *out = kernel_variant() == 1 ? make_dispatch<3, 6>()
-             : kernel_variant() == 2 ? make_dispatch_v2<6, 2, false>()
-             : kernel_variant() == 9 ? make_dispatch_v2<6, 1, false, false, 9>()
-             : kernel_variant() == 12 ? make_dispatch_ho<6>()
-             : kernel_variant() == 30 ? make_dispatch_v2<6, 1, false, false, 30>()   // pencil Picard loop
-             : kernel_variant() == 32 ? make_dispatch_v2<6, 1, false>()              // C-order nodes (A/B)
-             : make_dispatch_v2<6, 1, false, false, 31>();   // default: warp node blocks (2.45e9 vs 2.36e9)
-        return true;
-      // p >= 6: time line in local memory, spatial derivatives as DMMA GEMMs
-      case 7: *out = kernel_variant() == 1 ? make_dispatch<3, 7>() : make_dispatch_ho<7>(); return true;
-      case 8: *out = kernel_variant() == 1 ? make_dispatch<3, 8>() : make_dispatch_ho<8>(); return true;
-      case 9: *out = kernel_variant() == 1 ? make_dispatch<3, 9>() : make_dispatch_ho<9>(); return true;
-      case 10: *out = kernel_variant() == 1 ? make_dispatch<3, 10>() : make_dispatch_ho<10>(); return true;
+      case 4: *out = make_dispatch_v2<4, 1, true, false, 14>(); return true;
+      case 6: *out = make_dispatch_v2<6, 1, false, false, 31>(); return true;
+      case 7: *out = make_dispatch_ho<7>(); return true;
+      case 8: *out = make_dispatch_ho<8>(); return true;
+      case 9: *out = make_dispatch_ho<9>(); return true;
+      case 10: *out = make_dispatch_ho<10>(); return true;
     }
   }
-  return false;
+  return dispatch_generic(d, p, out);
 }
 
 }  // namespace
@@ -327,6 +246,7 @@ struct NcclApi {
   bool ok = false;
   decltype(&ncclGetUniqueId) getUniqueId = nullptr;
   decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclCommInitAll) commInitAll = nullptr;
   decltype(&ncclCommDestroy) commDestroy = nullptr;
   decltype(&ncclSend) send = nullptr;
   decltype(&ncclRecv) recv = nullptr;
@@ -346,6 +266,7 @@ static NcclApi& nccl_api() {
     if (lib) {
       a.getUniqueId = (decltype(a.getUniqueId))dlsym(lib, "ncclGetUniqueId");
       a.commInitRank = (decltype(a.commInitRank))dlsym(lib, "ncclCommInitRank");
+      a.commInitAll = (decltype(a.commInitAll))dlsym(lib, "ncclCommInitAll");
       a.commDestroy = (decltype(a.commDestroy))dlsym(lib, "ncclCommDestroy");
       a.send = (decltype(a.send))dlsym(lib, "ncclSend");
       a.recv = (decltype(a.recv))dlsym(lib, "ncclRecv");
@@ -353,7 +274,7 @@ static NcclApi& nccl_api() {
       a.groupEnd = (decltype(a.groupEnd))dlsym(lib, "ncclGroupEnd");
       a.allReduce = (decltype(a.allReduce))dlsym(lib, "ncclAllReduce");
       a.errorString = (decltype(a.errorString))dlsym(lib, "ncclGetErrorString");
-      a.ok = a.getUniqueId && a.commInitRank && a.commDestroy && a.send && a.recv && a.groupStart &&
+      a.ok = a.getUniqueId && a.commInitRank && a.commInitAll && a.commDestroy && a.send && a.recv && a.groupStart &&
              a.groupEnd && a.allReduce && a.errorString;
     }
   }
@@ -407,8 +328,6 @@ struct adg_handle {
   double lim_cfl = 0.9;
   // adg_step_host: copy streams and per-chunk events
   cudaStream_t copy_in = nullptr, copy_out = nullptr;
-  cudaStream_t sweep_st[4] = {nullptr, nullptr, nullptr, nullptr};   // concurrent chunk sweeps
-  std::vector<cudaEvent_t> trace_ev;   // ADG_HOST_TRACE timeline (timing events)
   // library-owned NCCL communicator of the slab ranks (adg_nccl_init)
   ncclComm_t comm = nullptr;
   int comm_rank = 0, comm_world = 1;
@@ -419,10 +338,13 @@ struct adg_handle {
   bool hst_fresh = false;              // hst mirrors the device (no phase call since the last pull)
   bool has_next_cond = false;          // adg_run_timed_ex: the finish sets the next rerun node's condition
   unsigned long long next_cond = 0;
+  // adg_set_option (explicit, per handle; no environment lookups in the library)
+  int opt_graph = 1;                   // ADG_OPT_GRAPH: captured step graphs in adg_run / adg_run_timed*
+  int opt_cond_rerun = 1;              // ADG_OPT_COND_RERUN: rerun pass as a conditional graph node
+  int opt_host_chunks = 16;            // ADG_OPT_HOST_CHUNKS: wave-aligned chunks of adg_step_host
+                                       // (cfg 2: 16 -> 1.526 ms, 9 -> 1.557, 23 -> 1.784)
 };
 
-constexpr int ADG_HOST_CHUNKS = 16;      // wave-aligned chunks of the pipelined host step (ADG_HOST_CHUNKS env;
-                                          // cfg 2: 16 -> 1.526 ms, 9 -> 1.557, 23 -> 1.784)
 constexpr int ADG_HOST_CHUNKS_MAX = 81;
 constexpr int ADG_TIMED_NO_PULL = 1 << 16;   // internal adg_run_timed_ex flag: adg_run's graph chunks
 
@@ -704,9 +626,6 @@ void adg_destroy(adg_handle* h) {
     if (e) cudaEventDestroy(e);
   if (h->rec_host) cudaFreeHost(h->rec_host);
   if (h->copy_out) cudaStreamDestroy(h->copy_out);
-  for (cudaStream_t x : h->sweep_st)
-    if (x) cudaStreamDestroy(x);
-  for (cudaEvent_t e : h->trace_ev) cudaEventDestroy(e);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   delete h;
 }
@@ -910,10 +829,10 @@ adg_status adg_run(adg_handle* h, int steps, adg_step_record* out) {
     }
     // single GPU, fused driver, no limiter: the remaining steps as one CUDA graph with the
     // rerun pass as a conditional node (adg_run_timed_ex; bitwise the stream launches,
-    // tests/test_gpu_parity.py::test_run_timed_graph_equals_device_run).  ADG_RUN_NO_GRAPH=1:
+    // tests/test_gpu_parity.py::test_run_timed_graph_equals_device_run).  ADG_OPT_GRAPH 0:
     // stream launches.
     const bool graph = !straightforward(h) && h->cfg.world == 1 && h->cfg.halo_mode == 0 && !h->lim &&
-                       chunk - i >= 2 && getenv("ADG_RUN_NO_GRAPH") == nullptr;
+                       chunk - i >= 2 && h->opt_graph;
     if (graph) {
       double tout[2];
       adg_status s = adg_run_timed_ex(h, chunk - i, ADG_TIMED_NO_PULL, tout);
@@ -1145,65 +1064,99 @@ adg_status adg_run_timed(adg_handle* h, int steps, double* out) {
   return adg_run_timed_ex(h, steps, ADG_TIMED_KERNEL_EVENTS, out);
 }
 
-adg_status adg_run_timed_ex(adg_handle* h, int steps, int flags, double* out) {
+static adg_status enqueue_halo(adg_handle* h, int par);
+
+// `steps` realisation steps (rerun pass -> sweep -> [all-reduce] -> time control)
+// enqueued back to back on h->stream.  By default they are captured into one CUDA
+// graph and launched once (graph-node gaps instead of launch gaps), the rerun pass of
+// every step an IF node whose condition the previous step's finish kernel sets (no
+// rerun launch at all on the common no-rerun step: cfg 2 0.564 -> 0.555 ms/step).
+// The launches, and the host-side counters they advance, are exactly those of the
+// stream path (ADG_OPT_GRAPH 0).  mgpu: the handle's NCCL communicator exchanges the
+// boundary records on the comm stream (forked from and joined to the capture through
+// comm_ev) while the interior planes run, and all-reduces the step reduction.
+// Events: ev[0] / ev[1] bracket the segment; with ADG_TIMED_KERNEL_EVENTS also every
+// rerun / sweep launch (graph nodes that cost gaps: cfg 1 26.6 -> 35.4 us/step, so the
+// throughput run leaves them out and an instrumented replay measures the kernels).
+static adg_status run_steps(adg_handle* h, int steps, int flags, double* out, bool mgpu) {
   if (!h || !out || steps < 1) return ADG_ERR_CONFIG;
+  if (mgpu && !h->comm) return fail(h, ADG_ERR_CONFIG, "adg_run_timed_mgpu needs adg_nccl_init");
   if (h->hst.status) return status_from_state(h);
   CUDA_TRY(h, cudaSetDevice(h->cfg.device));
   if (!straightforward(h) && h->sweep_index == 0)
     return fail(h, ADG_ERR_CONFIG, "adg_run_timed needs a primed driver (run one step first)");
-  std::vector<cudaEvent_t> ev(4 * (size_t)steps + 2);
-  for (auto& e : ev) CUDA_TRY(h, cudaEventCreate(&e));
-  adg_status s = ADG_OK;
-  // The step sequence (rerun pass, sweep, time control and the timing events of
-  // every step) is captured into one CUDA graph and launched once: the launch
-  // gaps between the dependent kernels shrink to graph-node gaps (ADG_NO_GRAPH=1:
-  // plain stream launches).  The launches, and the host-side counters they
-  // advance, are exactly those of the stream path.
+  const bool exchange = mgpu && (h->comm_world > 1 || h->cfg.halo_mode == 1);
+  const bool step_ev = (flags & ADG_TIMED_KERNEL_EVENTS) != 0;
+  std::vector<cudaEvent_t> ev(step_ev ? 4 * (size_t)steps + 2 : 2, nullptr);
+  auto destroy_events = [&] {
+    for (cudaEvent_t e : ev)
+      if (e) cudaEventDestroy(e);
+  };
+  for (auto& e : ev) {
+    const cudaError_t ce = cudaEventCreate(&e);
+    if (ce != cudaSuccess) {
+      destroy_events();
+      return cuda_check(h, ce, "cudaEventCreate");
+    }
+  }
   const cudaStream_t run = h->stream;
-  cudaStream_t cap = nullptr;
-  const bool graph = getenv("ADG_NO_GRAPH") == nullptr &&
-                     cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) == cudaSuccess &&
-                     cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+  cudaStream_t cap = nullptr, side = nullptr;
+  bool graph = h->opt_graph && cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) == cudaSuccess;
+  if (graph)
+    graph = cudaStreamBeginCapture(cap, mgpu ? cudaStreamCaptureModeRelaxed : cudaStreamCaptureModeThreadLocal) ==
+            cudaSuccess;
+  if (!graph && cap) {
+    cudaStreamDestroy(cap);
+    cap = nullptr;
+  }
   if (graph) h->stream = cap;
   // in a capture, timing events become event-record nodes only with the external flag
   const unsigned rec_flags = graph ? cudaEventRecordExternal : cudaEventRecordDefault;
   auto record0 = [&](cudaEvent_t e) { return cudaEventRecordWithFlags(e, h->stream, rec_flags); };
-  // per-step events around the rerun and sweep launches (the kernel time of the
-  // roofline); they are graph nodes that cost launch gaps (cfg 1: 26.6 -> 35.4 us/step),
-  // so the throughput run leaves them out and an instrumented replay measures the kernels
-  const bool step_ev = (flags & ADG_TIMED_KERNEL_EVENTS) != 0;
-  auto record = [&](cudaEvent_t e) { return step_ev ? record0(e) : cudaSuccess; };
-  // each step's rerun pass is an IF node whose condition the previous step's finish
-  // kernel sets: no rerun launch at all on the common no-rerun step (cfg 2: the pass's
-  // 19683 early-exit CTAs cost ~9 us/step, 0.564 -> 0.555 ms).  ADG_NO_COND_RERUN=1:
-  // plain rerun launches.
-  const bool cond = graph && !straightforward(h) && getenv("ADG_NO_COND_RERUN") == nullptr;
+  auto record = [&](size_t i) { return step_ev ? record0(ev[i]) : cudaSuccess; };
+  bool cond = graph && !straightforward(h) && h->opt_cond_rerun;
   std::vector<cudaGraphConditionalHandle> hc;
-  cudaStream_t side = nullptr;
-  if (cond) {
-    cudaStreamCaptureStatus cs;
-    cudaGraph_t cg = nullptr;
-    CUDA_TRY(h, cudaStreamGetCaptureInfo(cap, &cs, nullptr, &cg, nullptr, nullptr));
-    hc.resize(steps);
-    for (int i = 0; i < steps; ++i)   // default 1: the first step's pass checks rerun_next itself
-      CUDA_TRY(h, cudaGraphConditionalHandleCreate(&hc[i], cg, 1, cudaGraphCondAssignDefault));
-    CUDA_TRY(h, cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-  }
-  auto rerun_node = [&](int i) -> adg_status {
-    return cond ? capture_rerun_if(h, hc[i], side) : adg_phase_rerun(h);
-  };
+  // everything that can fail runs inside the capture, so the capture always ends
+  // below and h->stream is restored whatever happens
   auto enqueue = [&]() -> adg_status {
+    if (cond) {
+      cudaStreamCaptureStatus cs;
+      cudaGraph_t cg = nullptr;
+      bool ok = cudaStreamGetCaptureInfo(cap, &cs, nullptr, &cg, nullptr, nullptr) == cudaSuccess &&
+                cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) == cudaSuccess;
+      hc.resize(steps);
+      // default 1: the first step's pass checks rerun_next itself
+      for (int i = 0; i < steps && ok; ++i)
+        ok = cudaGraphConditionalHandleCreate(&hc[i], cg, 1, cudaGraphCondAssignDefault) == cudaSuccess;
+      if (!ok) {                 // no conditional nodes on this driver: plain rerun launches
+        cudaGetLastError();
+        cond = false;
+      }
+    }
     CUDA_TRY(h, record0(ev[0]));
     adg_status r = ADG_OK;
     for (int i = 0; i < steps && r == ADG_OK; ++i) {
-      CUDA_TRY(h, record(ev[2 + 4 * i]));
-      r = rerun_node(i);
-      CUDA_TRY(h, record(ev[3 + 4 * i]));
+      CUDA_TRY(h, record(2 + 4 * (size_t)i));
+      r = cond ? capture_rerun_if(h, hc[i], side) : adg_phase_rerun(h);
+      CUDA_TRY(h, record(3 + 4 * (size_t)i));
       if (r != ADG_OK) break;
-      CUDA_TRY(h, record(ev[4 + 4 * i]));
-      r = adg_phase_sweep(h);
-      CUDA_TRY(h, record(ev[5 + 4 * i]));
+      CUDA_TRY(h, record(4 + 4 * (size_t)i));
+      if (exchange) {
+        r = enqueue_halo(h, adg_trace_parity(h));
+        if (r == ADG_OK) r = adg_phase_sweep_part(h, ADG_PART_INTERIOR);
+        if (r == ADG_OK) {
+          CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->comm_ev[1], 0));
+          r = adg_phase_sweep_part(h, ADG_PART_BOUNDARY);
+        }
+      } else {
+        r = adg_phase_sweep(h);
+      }
+      CUDA_TRY(h, record(5 + 4 * (size_t)i));
       if (r != ADG_OK) break;
+      if (mgpu && h->comm_world > 1) {
+        const ncclResult_t nr = nccl_api().allReduce(h->st, h->st, 2, ncclInt64, ncclMax, h->comm, h->stream);
+        if (nr != ncclSuccess) return fail(h, ADG_ERR_RUNTIME, nccl_api().errorString(nr));
+      }
       h->has_next_cond = cond && i + 1 < steps;
       if (h->has_next_cond) h->next_cond = hc[i + 1];
       r = adg_phase_finish(h);
@@ -1212,11 +1165,10 @@ adg_status adg_run_timed_ex(adg_handle* h, int steps, int flags, double* out) {
     CUDA_TRY(h, record0(ev[1]));
     return r;
   };
-  s = enqueue();
+  adg_status s = enqueue();
   h->has_next_cond = false;
-  if (side) cudaStreamDestroy(side);
+  h->stream = run;
   if (graph) {
-    h->stream = run;
     cudaGraph_t g = nullptr;
     cudaGraphExec_t ge = nullptr;
     const cudaError_t e1 = cudaStreamEndCapture(cap, &g);
@@ -1229,29 +1181,36 @@ adg_status adg_run_timed_ex(adg_handle* h, int steps, int flags, double* out) {
     if (g) cudaGraphDestroy(g);
     cudaStreamDestroy(cap);
     if (s == ADG_OK && (e1 != cudaSuccess || e2 != cudaSuccess))
-      return fail(h, ADG_ERR_RUNTIME, std::string("adg_run_timed graph: ") +
-                                          cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
-  } else if (cap) {
-    cudaStreamDestroy(cap);
+      s = fail(h, ADG_ERR_RUNTIME, std::string("adg_run_timed graph: ") +
+                                       cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
   }
-  CUDA_TRY(h, cudaEventSynchronize(ev[1]));
+  if (side) cudaStreamDestroy(side);
+  if (s != ADG_OK) {
+    cudaStreamSynchronize(run);
+    destroy_events();
+    return s;
+  }
+  adg_status t = cuda_check(h, cudaEventSynchronize(ev[1]), "cudaEventSynchronize");
   float ms = 0.f;
-  CUDA_TRY(h, cudaEventElapsedTime(&ms, ev[0], ev[1]));
+  if (t == ADG_OK) t = cuda_check(h, cudaEventElapsedTime(&ms, ev[0], ev[1]), "cudaEventElapsedTime");
   out[0] = ms;
   double kern = 0.0;
-  for (int i = 0; i < steps && step_ev; ++i) {
+  for (int i = 0; i < steps && step_ev && t == ADG_OK; ++i) {
     float a = 0.f, b = 0.f;
-    CUDA_TRY(h, cudaEventElapsedTime(&a, ev[2 + 4 * i], ev[3 + 4 * i]));
-    CUDA_TRY(h, cudaEventElapsedTime(&b, ev[4 + 4 * i], ev[5 + 4 * i]));
+    cudaEventElapsedTime(&a, ev[2 + 4 * (size_t)i], ev[3 + 4 * (size_t)i]);
+    cudaEventElapsedTime(&b, ev[4 + 4 * (size_t)i], ev[5 + 4 * (size_t)i]);
     kern += a + b;
   }
   out[1] = kern;
-  for (auto& e : ev) cudaEventDestroy(e);
-  if (s != ADG_OK) return s;
+  destroy_events();
+  if (t != ADG_OK) return t;
   if (flags & ADG_TIMED_NO_PULL) return ADG_OK;     // adg_run pulls state and records itself
-  s = pull_state(h);
-  if (s != ADG_OK) return s;
+  if ((t = pull_state(h)) != ADG_OK) return t;
   return status_from_state(h);
+}
+
+adg_status adg_run_timed_ex(adg_handle* h, int steps, int flags, double* out) {
+  return run_steps(h, steps, flags, out, false);
 }
 
 // ---------------------------------------------------------------------------
@@ -1322,112 +1281,177 @@ adg_status adg_run_timed_mgpu(adg_handle* h, int steps, double* out) {
 }
 
 adg_status adg_run_timed_mgpu_ex(adg_handle* h, int steps, int flags, double* out) {
-  if (!h || !out || steps < 1) return ADG_ERR_CONFIG;
-  if (!h->comm) return fail(h, ADG_ERR_CONFIG, "adg_run_timed_mgpu needs adg_nccl_init");
-  if (h->hst.status) return status_from_state(h);
-  CUDA_TRY(h, cudaSetDevice(h->cfg.device));
-  if (!straightforward(h) && h->sweep_index == 0)
-    return fail(h, ADG_ERR_CONFIG, "adg_run_timed_mgpu needs a primed driver (run one step first)");
-  const bool exchange = h->comm_world > 1 || h->cfg.halo_mode == 1;
-  std::vector<cudaEvent_t> ev(4 * (size_t)steps + 2);
-  for (auto& e : ev) CUDA_TRY(h, cudaEventCreate(&e));
-  adg_status s = ADG_OK;
-  // As adg_run_timed_ex: the steps (NCCL calls included: the comm stream forks from and
-  // joins the capture through comm_ev) are captured into one CUDA graph with the rerun
-  // pass as a conditional node (ADG_MGPU_NO_GRAPH=1: plain stream launches).
-  const cudaStream_t run = h->stream;
-  cudaStream_t cap = nullptr;
-  const bool graph = getenv("ADG_MGPU_NO_GRAPH") == nullptr &&
-                     cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) == cudaSuccess &&
-                     cudaStreamBeginCapture(cap, cudaStreamCaptureModeRelaxed) == cudaSuccess;
-  if (graph) h->stream = cap;
-  const unsigned rec_flags = graph ? cudaEventRecordExternal : cudaEventRecordDefault;
-  auto record0 = [&](cudaEvent_t e) { return cudaEventRecordWithFlags(e, h->stream, rec_flags); };
-  // per-launch kernel events only on request (adg_run_timed_ex)
-  const bool step_ev = (flags & ADG_TIMED_KERNEL_EVENTS) != 0;
-  auto record = [&](cudaEvent_t e) { return step_ev ? record0(e) : cudaSuccess; };
-  const bool cond = graph && !straightforward(h) && getenv("ADG_NO_COND_RERUN") == nullptr;
-  std::vector<cudaGraphConditionalHandle> hc;
-  cudaStream_t side = nullptr;
-  auto enqueue = [&]() -> adg_status {
-    if (cond) {
-      cudaStreamCaptureStatus cs;
-      cudaGraph_t cg = nullptr;
-      CUDA_TRY(h, cudaStreamGetCaptureInfo(cap, &cs, nullptr, &cg, nullptr, nullptr));
-      hc.resize(steps);
-      for (int i = 0; i < steps; ++i)
-        CUDA_TRY(h, cudaGraphConditionalHandleCreate(&hc[i], cg, 1, cudaGraphCondAssignDefault));
-      CUDA_TRY(h, cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-    }
-    CUDA_TRY(h, record0(ev[0]));
-    adg_status r = ADG_OK;
-    for (int i = 0; i < steps && r == ADG_OK; ++i) {
-      CUDA_TRY(h, record(ev[2 + 4 * i]));
-      r = cond ? capture_rerun_if(h, hc[i], side) : adg_phase_rerun(h);
-      CUDA_TRY(h, record(ev[3 + 4 * i]));
-      if (r != ADG_OK) break;
-      CUDA_TRY(h, record(ev[4 + 4 * i]));
-      if (exchange) {
-        r = enqueue_halo(h, adg_trace_parity(h));
-        if (r == ADG_OK) r = adg_phase_sweep_part(h, ADG_PART_INTERIOR);
-        if (r == ADG_OK) {
-          CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->comm_ev[1], 0));
-          r = adg_phase_sweep_part(h, ADG_PART_BOUNDARY);
-        }
-      } else {
-        r = adg_phase_sweep(h);
+  return run_steps(h, steps, flags, out, true);
+}
+
+// ---------------------------------------------------------------------------
+// In-process multi-GPU group: the reference's Driver(..., parallel=True,
+// n_workers=N) seam (scheduler.py:92-95,126-130) on N GPUs of one process.  The
+// caller creates one slab handle per device (cfg.rank = i, cfg.world = N); one NCCL
+// clique (ncclCommInitAll) connects them and every group call drives each handle
+// from its own host thread with exactly the per-rank step sequence of the
+// one-process-per-GPU path (run_steps with the communicator), so the results are
+// those of adg_run_timed_mgpu and, max being exact, of one GPU bitwise.
+
+static adg_status group_check(adg_handle** hs, int n) {
+  if (!hs || n < 1) return ADG_ERR_CONFIG;
+  for (int i = 0; i < n; ++i) {
+    if (!hs[i]) return ADG_ERR_CONFIG;
+    if (hs[i]->cfg.world != n || hs[i]->cfg.rank != i)
+      return fail(hs[0], ADG_ERR_CONFIG, "group handles must be slabs rank 0..n-1 of one world");
+  }
+  return ADG_OK;
+}
+
+// run f(rank) on one host thread per handle; the first failing rank's status wins
+}  // extern "C"
+template <class F>
+static adg_status group_for_each(adg_handle** hs, int n, F f) {
+  std::vector<adg_status> st(n, ADG_OK);
+  std::vector<std::thread> th;
+  th.reserve(n);
+  for (int i = 0; i < n; ++i)
+    th.emplace_back([&, i] {
+      if (cudaSetDevice(hs[i]->cfg.device) != cudaSuccess) {
+        st[i] = fail(hs[i], ADG_ERR_RUNTIME, "cudaSetDevice failed");
+        return;
       }
-      CUDA_TRY(h, record(ev[5 + 4 * i]));
-      if (r != ADG_OK) break;
-      if (h->comm_world > 1)
-        NCCL_TRY(h, nccl_api().allReduce(h->st, h->st, 2, ncclInt64, ncclMax, h->comm, h->stream));
-      h->has_next_cond = cond && i + 1 < steps;
-      if (h->has_next_cond) h->next_cond = hc[i + 1];
-      r = adg_phase_finish(h);
-      h->has_next_cond = false;
+      st[i] = f(i);
+    });
+  for (auto& t : th) t.join();
+  for (int i = 0; i < n; ++i)
+    if (st[i] != ADG_OK) {
+      if (i != 0) hs[0]->err = hs[i]->err;
+      return st[i];
     }
-    CUDA_TRY(h, record0(ev[1]));
+  return ADG_OK;
+}
+extern "C" {
+
+adg_status adg_group_init(adg_handle** hs, int n) {
+  adg_status s = group_check(hs, n);
+  if (s != ADG_OK) return s;
+  NcclApi& api = nccl_api();
+  if (!api.ok) return fail(hs[0], ADG_ERR_RUNTIME, "libnccl.so.2 not found");
+  std::vector<int> devs(n);
+  for (int i = 0; i < n; ++i) {
+    devs[i] = hs[i]->cfg.device;
+    for (int j = 0; j < i; ++j)
+      if (devs[j] == devs[i]) return fail(hs[0], ADG_ERR_CONFIG, "group handles need distinct devices");
+    if (hs[i]->comm) { api.commDestroy(hs[i]->comm); hs[i]->comm = nullptr; }
+  }
+  std::vector<ncclComm_t> comms(n, nullptr);
+  const ncclResult_t r = api.commInitAll(comms.data(), n, devs.data());
+  if (r != ncclSuccess) return fail(hs[0], ADG_ERR_RUNTIME, api.errorString(r));
+  for (int i = 0; i < n; ++i) {
+    adg_handle* h = hs[i];
+    h->comm = comms[i];
+    h->comm_rank = i;
+    h->comm_world = n;
+    CUDA_TRY(h, cudaSetDevice(h->cfg.device));
+    if (!h->comm_stream) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
+    for (auto& e : h->comm_ev)
+      if (!e) CUDA_TRY(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  return ADG_OK;
+}
+
+static adg_status comm_reduce(adg_handle* h) {
+  if (h->comm_world <= 1) return ADG_OK;
+  const ncclResult_t r = nccl_api().allReduce(h->st, h->st, 2, ncclInt64, ncclMax, h->comm, h->stream);
+  return r == ncclSuccess ? ADG_OK : fail(h, ADG_ERR_RUNTIME, nccl_api().errorString(r));
+}
+
+adg_status adg_group_seed(adg_handle** hs, int n) {
+  adg_status s = group_check(hs, n);
+  if (s != ADG_OK) return s;
+  if (!hs[0]->comm) return fail(hs[0], ADG_ERR_CONFIG, "adg_group_seed needs adg_group_init");
+  return group_for_each(hs, n, [&](int i) -> adg_status {
+    adg_handle* h = hs[i];
+    adg_status r = adg_phase_seed(h);          // Driver._seed_time_control, global max
+    if (r == ADG_OK) r = comm_reduce(h);
+    if (r == ADG_OK) r = adg_phase_seed_finish(h);
+    if (r == ADG_OK) r = pull_state(h);
+    return r == ADG_OK ? status_from_state(h) : r;
+  });
+}
+
+adg_status adg_group_run(adg_handle** hs, int n, int steps, adg_step_record* out) {
+  adg_status s = group_check(hs, n);
+  if (s != ADG_OK) return s;
+  if (!hs[0]->comm) return fail(hs[0], ADG_ERR_CONFIG, "adg_group_run needs adg_group_init");
+  if (steps < 1) return ADG_OK;
+  const int before = hs[0]->hst.step;
+  s = group_for_each(hs, n, [&](int i) -> adg_status {
+    adg_handle* h = hs[i];
+    if (h->hst.status) return status_from_state(h);
+    int left = steps;
+    adg_status r = ADG_OK;
+    if (!straightforward(h) && h->sweep_index == 0) {     // priming sweep + the first step
+      r = adg_phase_sweep(h);
+      if (r == ADG_OK) r = comm_reduce(h);
+      if (r == ADG_OK) r = adg_phase_finish(h);
+      if (r == ADG_OK) r = adg_phase_rerun(h);
+      if (r == ADG_OK) r = enqueue_halo(h, adg_trace_parity(h));
+      if (r == ADG_OK) r = adg_phase_sweep_part(h, ADG_PART_INTERIOR);
+      if (r == ADG_OK) r = cuda_check(h, cudaStreamWaitEvent(h->stream, h->comm_ev[1], 0), "wait halo");
+      if (r == ADG_OK) r = adg_phase_sweep_part(h, ADG_PART_BOUNDARY);
+      if (r == ADG_OK) r = comm_reduce(h);
+      if (r == ADG_OK) r = adg_phase_finish(h);
+      --left;
+    }
+    while (r == ADG_OK && left > 0) {      // the record ring bounds one chunk
+      const int chunk = left < h->rec_cap ? left : h->rec_cap;
+      double tout[2];
+      r = run_steps(h, chunk, ADG_TIMED_NO_PULL, tout, true);
+      if (r == ADG_OK) r = pull_state(h);
+      if (r == ADG_OK && h->hst.status) break;
+      left -= chunk;
+    }
+    if (r == ADG_OK) r = pull_state(h);
     return r;
-  };
-  s = enqueue();
-  h->has_next_cond = false;
-  if (side) cudaStreamDestroy(side);
-  if (graph) {
-    h->stream = run;
-    cudaGraph_t g = nullptr;
-    cudaGraphExec_t ge = nullptr;
-    const cudaError_t e1 = cudaStreamEndCapture(cap, &g);
-    cudaError_t e2 = cudaErrorUnknown;
-    if (e1 == cudaSuccess && s == ADG_OK) {
-      e2 = cudaGraphInstantiate(&ge, g, 0);
-      if (e2 == cudaSuccess) e2 = cudaGraphLaunch(ge, run);
+  });
+  if (s != ADG_OK) return s;
+  // the time control is replicated (every rank finishes on the reduced lambda):
+  // rank 0's records, with the per-rank Picard counts summed
+  adg_handle* h0 = hs[0];
+  const int done = h0->hst.step - before;
+  if (out && done > 0) {
+    if ((s = fetch_records(h0, before, h0->hst.step, out)) != ADG_OK) return s;
+    std::vector<adg_step_record> tmp(done);
+    for (int i = 1; i < n; ++i) {
+      if ((s = fetch_records(hs[i], before, before + done, tmp.data())) != ADG_OK) return s;
+      for (int k = 0; k < done; ++k) {
+        out[k].picard_iters += tmp[k].picard_iters;
+        out[k].predicts += tmp[k].predicts;
+      }
     }
-    if (ge) cudaGraphExecDestroy(ge);
-    if (g) cudaGraphDestroy(g);
-    cudaStreamDestroy(cap);
-    if (s == ADG_OK && (e1 != cudaSuccess || e2 != cudaSuccess))
-      return fail(h, ADG_ERR_RUNTIME, std::string("adg_run_timed_mgpu graph: ") +
-                                          cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
-  } else if (cap) {
-    cudaStreamDestroy(cap);
   }
-  CUDA_TRY(h, cudaEventSynchronize(ev[1]));
-  float ms = 0.f;
-  CUDA_TRY(h, cudaEventElapsedTime(&ms, ev[0], ev[1]));
-  out[0] = ms;
-  double kern = 0.0;
-  for (int i = 0; i < steps && step_ev; ++i) {
-    float a = 0.f, b = 0.f;
-    CUDA_TRY(h, cudaEventElapsedTime(&a, ev[2 + 4 * i], ev[3 + 4 * i]));
-    CUDA_TRY(h, cudaEventElapsedTime(&b, ev[4 + 4 * i], ev[5 + 4 * i]));
-    kern += a + b;
+  for (int i = 0; i < n; ++i)
+    if (hs[i]->hst.status) return status_from_state(hs[i]);
+  return ADG_OK;
+}
+
+int adg_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
   }
-  out[1] = kern;
-  for (auto& e : ev) cudaEventDestroy(e);
-  if (s != ADG_OK) return s;
-  s = pull_state(h);
-  if (s != ADG_OK) return s;
-  return status_from_state(h);
+  return n;
+}
+
+adg_status adg_set_option(adg_handle* h, int option, int value) {
+  if (!h) return ADG_ERR_CONFIG;
+  switch (option) {
+    case ADG_OPT_GRAPH: h->opt_graph = value ? 1 : 0; return ADG_OK;
+    case ADG_OPT_COND_RERUN: h->opt_cond_rerun = value ? 1 : 0; return ADG_OK;
+    case ADG_OPT_HOST_CHUNKS:
+      if (value < 1 || value > ADG_HOST_CHUNKS_MAX) return fail(h, ADG_ERR_CONFIG, "host chunks must be in [1, 81]");
+      h->opt_host_chunks = value;
+      return ADG_OK;
+  }
+  return fail(h, ADG_ERR_CONFIG, "unknown option");
 }
 
 // ---------------------------------------------------------------------------
@@ -1443,8 +1467,6 @@ adg_status adg_run_timed_mgpu_ex(adg_handle* h, int steps, int flags, double* ou
 static adg_status ensure_copy_streams(adg_handle* h) {
   if (!h->copy_in) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->copy_in, cudaStreamNonBlocking));
   if (!h->copy_out) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->copy_out, cudaStreamNonBlocking));
-  for (cudaStream_t& x : h->sweep_st)
-    if (!x) CUDA_TRY(h, cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
   if (!h->rec_host) CUDA_TRY(h, cudaMallocHost(&h->rec_host, sizeof(StepRecord)));
   if (h->chunk_ev.empty()) {
     h->chunk_ev.resize(3 * ADG_HOST_CHUNKS_MAX + 1);
@@ -1474,50 +1496,21 @@ adg_status adg_step_host(adg_handle* h, const double* Q_in, double* Q_out, adg_s
   if (!h->hst_fresh && (s = pull_state(h)) != ADG_OK) return s;   // rerun decision after phase calls
   if (h->hst.status) return status_from_state(h);
   const size_t cell_doubles = (size_t)h->NS * h->m;
-  static const int want = [] {
-    const char* v = getenv("ADG_HOST_CHUNKS");
-    const int c = v ? atoi(v) : ADG_HOST_CHUNKS;
-    return c < 1 ? 1 : (c > ADG_HOST_CHUNKS_MAX ? ADG_HOST_CHUNKS_MAX : c);
-  }();
+  const int want = h->opt_host_chunks;
   // chunk i = cells [cell_of(i), cell_of(i+1)): boundaries on whole waves of
   // resident CTAs so the chunked sweep keeps the single launch's wave count
   const long long C = h->cells_local;
   long long wave = 0;
   {
-    int dev_sms = 148, per_sm = 1;
+    int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, h->cfg.device);
     if (h->disp_ctas_per_sm == 0) h->disp_ctas_per_sm = h->disp.occ ? h->disp.occ() : 1;
-    per_sm = h->disp_ctas_per_sm;
-    wave = (long long)dev_sms * per_sm;
+    wave = (long long)dev_sms * h->disp_ctas_per_sm;
   }
-  long long waves = (C + wave - 1) / wave;
-  // ADG_HOST_WAVES="1,2,4,...": explicit waves per chunk (the remainder goes to the last)
-  static const std::vector<int> sched = [] {
-    std::vector<int> v;
-    if (const char* e = getenv("ADG_HOST_WAVES"))
-      for (const char* q = e; *q;) {
-        const int w = atoi(q);
-        if (w > 0 && (int)v.size() < ADG_HOST_CHUNKS_MAX) v.push_back(w);
-        while (*q && *q != ',') ++q;
-        if (*q == ',') ++q;
-      }
-    return v;
-  }();
-  int nch = (int)(waves < want ? waves : want);
-  std::vector<long long> wcut;
-  if (!sched.empty()) {
-    long long acc = 0;
-    wcut.push_back(0);
-    for (int w : sched) {
-      if (acc >= waves) break;
-      acc += w;
-      wcut.push_back(acc < waves ? acc : waves);
-    }
-    wcut.back() = waves;
-    nch = (int)wcut.size() - 1;
-  }
+  const long long waves = (C + wave - 1) / wave;
+  const int nch = (int)(waves < want ? waves : want);
   auto cell_of = [&](int i) {
-    const long long w = wcut.empty() ? waves * i / nch : wcut[i];   // whole waves per chunk
+    const long long w = waves * i / nch;   // whole waves per chunk
     return w * wave < C ? w * wave : C;
   };
   cudaEvent_t* ev_in = h->chunk_ev.data();
@@ -1547,44 +1540,19 @@ adg_status adg_step_host(adg_handle* h, const double* Q_in, double* Q_out, adg_s
       CUDA_TRY(h, cudaEventRecord(ev_in[i], h->copy_in));
     }
   }
-  // ADG_HOST_SWEEP_STREAMS=2..4: chunk sweeps on rotating streams (they are
-  // independent: order-free atomics into the step state).  Measured cfg 2: no gain
-  // over one stream (1.434 vs 1.423 ms/step at 16 chunks) -- the step is bound by the
-  // PCIe copies, whose concurrent rate varies 1.06-1.35 ms per 2 x 50 MB between runs
-  static const int nst = [] {
-    const char* v = getenv("ADG_HOST_SWEEP_STREAMS");
-    const int c = v ? atoi(v) : 1;
-    return c < 1 ? 1 : (c > 4 ? 4 : c);
-  }();
-  static const bool trace = getenv("ADG_HOST_TRACE") != nullptr;
-  cudaEvent_t* te = nullptr;
-  if (trace) {
-    if ((int)h->trace_ev.size() < 3 * nch + 2) {
-      for (cudaEvent_t e : h->trace_ev) cudaEventDestroy(e);
-      h->trace_ev.assign(3 * nch + 2, nullptr);
-      for (auto& e : h->trace_ev) CUDA_TRY(h, cudaEventCreate(&e));
-    }
-    te = h->trace_ev.data();
-    CUDA_TRY(h, cudaEventRecord(te[0], h->stream));
-  }
   if (whole) CUDA_TRY(h, cudaEventRecord(ev_start, h->stream));   // Q resident (+ priming / rerun)
   const int mode = MODE_NORMAL;
   for (int i = 0; i < nch; ++i) {
     const long long c0 = cell_of(i), c1 = cell_of(i + 1);
-    cudaStream_t st = nst == 1 ? h->stream : h->sweep_st[i % nst];
+    cudaStream_t st = h->stream;
     CUDA_TRY(h, cudaStreamWaitEvent(st, whole ? ev_start : ev_in[i], 0));
-    if (te && !whole) CUDA_TRY(h, cudaEventRecord(te[1 + i], st));
     if ((s = launch_range(h, mode, c0, c1 - c0, st)) != ADG_OK) return s;
     CUDA_TRY(h, cudaEventRecord(ev_sw[i], st));
-    if (te) CUDA_TRY(h, cudaEventRecord(te[1 + nch + i], st));
     CUDA_TRY(h, cudaStreamWaitEvent(h->copy_out, ev_sw[i], 0));
     CUDA_TRY(h, cudaMemcpyAsync(Q_out + c0 * cell_doubles, h->Q + c0 * cell_doubles,
                                 sizeof(double) * (size_t)(c1 - c0) * cell_doubles, cudaMemcpyDeviceToHost,
                                 h->copy_out));
-    if (te) CUDA_TRY(h, cudaEventRecord(te[1 + 2 * nch + i], h->copy_out));
   }
-  if (nst > 1)
-    for (int i = 0; i < nch; ++i) CUDA_TRY(h, cudaStreamWaitEvent(h->stream, ev_sw[i], 0));
   if ((s = adg_phase_finish(h)) != ADG_OK) return s;
   // one sync for the state, the step record and the last chunk
   CUDA_TRY(h, cudaMemcpyAsync(&h->hst, h->st, sizeof(DevState), cudaMemcpyDeviceToHost, h->stream));
@@ -1592,22 +1560,6 @@ adg_status adg_step_host(adg_handle* h, const double* Q_in, double* Q_out, adg_s
                               cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   CUDA_TRY(h, cudaStreamSynchronize(h->copy_out));
-  if (te) {
-    CUDA_TRY(h, cudaEventRecord(te[3 * nch + 1], h->copy_out));
-    CUDA_TRY(h, cudaEventSynchronize(te[3 * nch + 1]));
-    float t = 0.f;
-    fprintf(stderr, "[adg_step_host] chunks %d streams %d whole %d\n", nch, nst, (int)whole);
-    for (int i = 0; i < nch; ++i) {
-      float a = 0.f, b = 0.f, c = 0.f;
-      if (!whole) cudaEventElapsedTime(&a, te[0], te[1 + i]);
-      cudaEventElapsedTime(&b, te[0], te[1 + nch + i]);
-      cudaEventElapsedTime(&c, te[0], te[1 + 2 * nch + i]);
-      fprintf(stderr, "  chunk %2d cells %6lld  in %.3f  swept %.3f  out %.3f ms\n", i,
-              cell_of(i + 1) - cell_of(i), a, b, c);
-    }
-    cudaEventElapsedTime(&t, te[0], te[3 * nch + 1]);
-    fprintf(stderr, "  end %.3f ms\n", t);
-  }
   h->hst_fresh = true;
   if ((s = status_from_state(h)) != ADG_OK) return s;
   if (out && h->hst.step == before + 1) {

@@ -257,3 +257,67 @@ class SlabDriver:
 
     def close(self):
         self.handle.close()
+
+
+class SlabGroup:
+    """N x-slab handles of one grid on N GPUs of this process (the reference's
+    ``Driver(..., parallel=True, n_workers=N)`` seam, ``src/scheduler.py:92-95,126-130``).
+
+    One NCCL clique over the handles (``adg_group_init`` -> ``ncclCommInitAll``);
+    every call drives all slabs from one host thread per GPU inside the library
+    (``adg_group_seed`` / ``adg_group_run``) with the per-rank step sequence of the
+    one-process-per-GPU path: halo exchange hidden behind the interior planes, MAX
+    all-reduce of the step reduction.  Max is exact, so the state equals the
+    single-GPU state bitwise.
+    """
+
+    def __init__(self, make_cfg, devices, basis, d, p):
+        import ctypes
+        from .solver import upload_operators
+        self.world = len(devices)
+        self.d, self.p = d, p
+        self.handles, self._ops = [], []
+        for r, dev in enumerate(devices):
+            cfg = make_cfg()
+            cfg.rank, cfg.world, cfg.device = r, self.world, int(dev)
+            h = _lib.Handle(cfg)
+            self.handles.append(h)
+            self._ops.append(upload_operators(h, basis))
+        self.lays = [h.layout() for h in self.handles]
+        self._arr = (ctypes.c_void_p * self.world)(*[h.h.value for h in self.handles])
+        self.lib = self.handles[0].lib
+        self._check(self.lib.adg_group_init(self._arr, self.world), "adg_group_init")
+
+    @property
+    def lead(self):
+        return self.handles[0]
+
+    def _check(self, st, what):
+        self.handles[0].check(st, what)
+
+    def load(self, Q_global):
+        for h, lay in zip(self.handles, self.lays):
+            Ql = np.ascontiguousarray(Q_global[lay.cell_offset:lay.cell_offset + lay.n_cells_local],
+                                      dtype=np.float64)
+            h.call("adg_load_state", _lib.dptr(Ql), Ql.size)
+
+    def seed(self):
+        self._check(self.lib.adg_group_seed(self._arr, self.world), "adg_group_seed")
+
+    def run(self, steps, recs):
+        """Status of ``adg_group_run`` (the caller maps it to an exception)."""
+        return self.lib.adg_group_run(self._arr, self.world, int(steps), recs)
+
+    def store(self, Q_global):
+        for h, lay in zip(self.handles, self.lays):
+            out = Q_global[lay.cell_offset:lay.cell_offset + lay.n_cells_local]
+            if not out.flags.c_contiguous:
+                raise ConfigurationError("grid.Q must stay C-contiguous")
+            h.call("adg_store_state", _lib.dptr(out), out.size)
+
+    def picard_histogram(self, bins=32):
+        return sum(h.picard_histogram(bins) for h in self.handles)
+
+    def close(self):
+        for h in self.handles:
+            h.close()

@@ -314,7 +314,7 @@ class Driver:
     def __init__(self, grid, kernels, time_control, mode="fused",
                  traversal="lexicographic", parallel=False, n_workers=4,
                  inject_rerun=False, spike_step=None, spike_factor=3.0,
-                 limiter=None, device=0, host_sync="step"):
+                 limiter=None, device=0, host_sync="step", devices=None):
         if mode not in ("straightforward", "shifted", "fused"):
             raise ConfigurationError(f"unknown scheduler mode {mode!r}")
         if mode == "shifted":
@@ -346,6 +346,19 @@ class Driver:
         self.step_records = []
         self.picard_iters = 0
         self.predicts = 0
+        self.devices = self._slab_devices(parallel, n_workers, device, devices)
+        self.group = None
+        if len(self.devices) > 1:
+            from .parallel import SlabGroup
+            self.group = SlabGroup(
+                lambda: _config(grid, kernels, time_control, inject_rerun, spike_step, spike_factor,
+                                device, mode=mode),
+                self.devices, kernels.basis, grid.d, grid.p)
+            self.handle = self.group.lead
+            self.group.load(grid.Q)
+            self.group.seed()                             # Driver._seed_time_control (global)
+            self._pull_tc()
+            return
         cfg = _config(grid, kernels, time_control, inject_rerun, spike_step, spike_factor, device,
                       mode=mode)
         self.handle = _lib.Handle(cfg)
@@ -365,9 +378,35 @@ class Driver:
         self.handle.call("adg_seed")                       # Driver._seed_time_control
         self._pull_tc()
 
+    def _slab_devices(self, parallel, n_workers, device, devices):
+        """GPUs of the run.  The reference's ``parallel=True, n_workers=N`` runs the
+        per-cell tasks on a thread pool (src/scheduler.py:126-130); on the GPU every
+        cell of a sweep already runs concurrently, so the workers become x-slabs of the
+        grid on N GPUs of this process (at most the visible GPUs and the 3^L cell planes).
+        ``devices`` names them explicitly.  Limited or outflow runs stay on one GPU
+        (those paths run on a single slab)."""
+        if devices is not None:
+            devs = [int(x) for x in devices]
+            if len(set(devs)) != len(devs) or not devs:
+                raise ConfigurationError("devices must be distinct GPU ordinals")
+        elif parallel:
+            visible = _lib.load_library().adg_device_count()
+            want = max(1, int(n_workers))
+            devs = [(device + i) % max(visible, 1) for i in range(min(want, max(visible, 1)))]
+        else:
+            return [int(device)]
+        if len(devs) > 1:
+            if self.limiter is not None or self.grid.boundary != "periodic":
+                return [devs[0]]
+            devs = devs[:self.grid.cells_per_axis]
+        return devs
+
     # -- state transfer ------------------------------------------------------
     def load_state(self, Q):
         Q = np.ascontiguousarray(Q, dtype=np.float64)
+        if self.group is not None:
+            self.group.load(Q)
+            return
         self.handle.call("adg_load_state", _lib.dptr(Q), Q.size)
 
     def sync_state(self):
@@ -375,6 +414,9 @@ class Driver:
         Q = self.grid.Q
         if not Q.flags.c_contiguous:
             raise ConfigurationError("grid.Q must stay C-contiguous")
+        if self.group is not None:
+            self.group.store(Q)
+            return Q
         self.handle.call("adg_store_state", _lib.dptr(Q), Q.size)
         return Q
 
@@ -426,7 +468,10 @@ class Driver:
     def step(self):
         rec = _lib.AdgStepRecord()
         t0 = time.perf_counter()
-        st = self.handle.lib.adg_step(self.handle.h, rec)
+        if self.group is not None:
+            st = self.group.run(1, (_lib.AdgStepRecord * 1).from_address(ctypes.addressof(rec)))
+        else:
+            st = self.handle.lib.adg_step(self.handle.h, rec)
         wall = time.perf_counter() - t0
         err = None
         try:
@@ -453,7 +498,10 @@ class Driver:
         recs = (_lib.AdgStepRecord * steps)()
         before = self.step_count
         t0 = time.perf_counter()
-        st = self.handle.lib.adg_run(self.handle.h, steps, recs)
+        if self.group is not None:
+            st = self.group.run(steps, recs)
+        else:
+            st = self.handle.lib.adg_run(self.handle.h, steps, recs)
         wall = time.perf_counter() - t0
         err = None
         try:
@@ -473,7 +521,8 @@ class Driver:
             if not T < final_time - 1e-14:
                 break
             if dt_new > final_time - T:
-                self.handle.call("adg_set_dt_new", ctypes.c_double(final_time - T))
+                for h in (self.group.handles if self.group is not None else [self.handle]):
+                    h.call("adg_set_dt_new", ctypes.c_double(final_time - T))
             self.step()
         return self.step_count
 
@@ -487,11 +536,14 @@ class Driver:
 
     def picard_histogram(self):
         """Picard iterations per predict, summed over every predict so far."""
-        h = self.handle.picard_histogram()
+        h = self.group.picard_histogram() if self.group is not None else self.handle.picard_histogram()
         return {int(k): int(v) for k, v in enumerate(h) if v}
 
     def close(self):
-        self.handle.close()
+        if self.group is not None:
+            self.group.close()
+        else:
+            self.handle.close()
 
 
 def gather(grid):

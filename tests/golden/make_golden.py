@@ -85,6 +85,14 @@ BIG = {
     "bump_d3_L3_p7_cfg3": ("bump", 3, 3, 7, 10, {}, {}, False),
     "bump_d3_L3_p9_cfg3": ("bump", 3, 3, 9, 10, {}, {}, False),
     "bump_d3_L2_p5": ("bump", 3, 2, 5, 10, {}, {}, False),
+    # round 2: reference-pinned state for the high-order kernels (p >= 6).  The 27^3 p=7 / p=9
+    # runs stop one step before the reference's abort (step 7 / step 5), so the pre-abort state
+    # and the Picard histogram are stored; the 9^3 random-Fourier runs are the cfg-5 state family
+    "bump_d3_L3_p7_pre": ("bump", 3, 3, 7, 6, {}, {}, False),
+    "bump_d3_L3_p9_pre": ("bump", 3, 3, 9, 4, {}, {}, False),
+    "fourier_d3_L2_p9": ("fourier", 3, 2, 9, 5, {}, {}, False, 13),
+    "fourier_d3_L2_p7": ("fourier", 3, 2, 7, 5, {}, {}, False, 13),
+    "fourier_d3_L2_p6": ("fourier", 3, 2, 6, 4, {}, {}, False, 13),
 }
 SAMPLE_STRIDE = 97
 
@@ -92,7 +100,8 @@ SAMPLE_STRIDE = 97
 def run_case(name, spec):
     from aderdg import (AdvectionSystem, Driver, EulerSystem, Kernels, NumericalError,
                         PredictorFailureError, TimeControl, build_grid, make_basis)
-    scen, d, L, p, steps, dkw, tkw, full = spec
+    scen, d, L, p, steps, dkw, tkw, full = spec[:8]
+    stride = spec[8] if len(spec) > 8 else SAMPLE_STRIDE
     if scen.startswith("gauss"):
         from aderdg.cli import gaussian_profile
         Q0 = scenarios.build("gauss", d, L, p, **({"noise": 1e-2, "seed": 1} if scen == "gauss_noise" else {}))
@@ -163,7 +172,7 @@ def run_case(name, spec):
         if full:
             out["Q_final"] = Qf
         else:
-            cells = np.arange(0, Qf.shape[0], SAMPLE_STRIDE)
+            cells = np.arange(0, Qf.shape[0], stride)
             out["sample_cells"] = cells
             out["Q_sample"] = Qf[cells]
     np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)

@@ -111,3 +111,16 @@ def test_slabs_straightforward_overlapped(cuda_ok, tmp_path):
     assert errs == [""] * 3
     Q1, tc1 = single(3, 2, 3, 4, mode="straightforward")
     assert np.array_equal(Q, Q1)
+
+
+def test_slabs_81cubed_p3_equal_single_gpu_bitwise(cuda_ok, tmp_path):
+    """The 81^3 link of the parity chain (BASELINE cfg 4/5 grid): two x-slabs of
+    41 / 40 planes, gloo-staged on one GPU, against the single-GPU run of the same
+    531441 cells -- bitwise, so the N-GPU cfg 4/5 states inherit the single-GPU parity."""
+    Q, tcs, errs = run_slabs(2, 3, 4, 3, 3, tmp_path)
+    assert errs == ["", ""]
+    Q1, tc1 = single(3, 4, 3, 3)
+    assert Q.shape == Q1.shape == (81 ** 3, 4, 4, 4, 5)
+    assert np.array_equal(Q, Q1)
+    for tc in tcs:
+        assert np.array_equal(tc, tc1)
