@@ -375,8 +375,7 @@ def main():
         rerun_launches.clear()
         remaining, first, started = K, True, False
         while remaining > 0:
-            if not first:
-                drv.load(Q0)
+            drv.load(Q0)                  # every episode restarts from the seeded state
             warm = args.warmup if first else 1
             for _ in range(warm):
                 drv.enqueue_step()

@@ -12,7 +12,7 @@ There is no host evaluation path for the limiter itself.
 
 import numpy as np
 
-from .basis import lagrange_eval
+from .basis import subcell_operators
 from .errors import ConfigurationError
 
 DMP_ABS = 1e-3      # src/limiter.py:23 (compiled into lim_detect_kernel)
@@ -21,12 +21,8 @@ DMP_REL = 1e-2      # src/limiter.py:24
 
 def subcell_average_matrix(basis):
     """src/limiter.py:26-34: ``P[s, i]`` = average of Lagrange polynomial i over
-    subcell s of the unit interval split into 2p+1 equal parts."""
-    ns = 2 * basis.p + 1
-    P = np.empty((ns, basis.n))
-    for s in range(ns):
-        P[s, :] = basis.weights @ lagrange_eval(basis.nodes, (s + basis.nodes) / ns)
-    return P
+    subcell s of the unit interval split into 2p+1 equal parts (tabulated)."""
+    return subcell_operators(basis.p)[0]
 
 
 class SubcellLimiter:
@@ -41,8 +37,7 @@ class SubcellLimiter:
         self.cfl = cfl
         self.ns = 2 * basis.p + 1
         self.h_sub = grid.h / self.ns
-        self.P = subcell_average_matrix(basis)
-        self.R = np.linalg.solve(self.P.T @ self.P, self.P.T)      # src/limiter.py:99
+        self.P, self.R = subcell_operators(basis.p)                # src/limiter.py:26-34,99
         w = basis.weights
         W = np.ones((basis.n,) * grid.d)
         for a in range(grid.d):
