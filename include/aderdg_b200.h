@@ -57,7 +57,10 @@ typedef enum {
   ADG_EK_INADMISSIBLE = 3,      /* "inadmissible state in cell {c} at step {s}" scheduler.py:429-432 */
   ADG_EK_PREDICTOR = 4,         /* PredictorFailureError(c)                   kernels.py:80-100 */
   ADG_EK_DEGENERATE = 5,        /* "admissible step degenerated to {dt_adm}"  scheduler.py:81-82 */
-  ADG_EK_SUBCELL = 6            /* "subcell update left cell {c} inadmissible" limiter.py:214-216 */
+  ADG_EK_SUBCELL = 6,           /* "subcell update left cell {c} inadmissible" limiter.py:214-216 */
+  ADG_EK_STALE = 7,             /* debug library: a face record with the wrong sweep stamp was read
+                                   (the reference's stale-hull checks, kernels.py:158-170,196-200) */
+  ADG_EK_BOUNDS = 8             /* debug library: cell / record slot index out of bounds */
 } adg_error_kind;
 
 typedef struct {

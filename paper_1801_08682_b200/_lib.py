@@ -15,6 +15,10 @@ from .errors import (ConfigurationError, DeviceError, NumericalError,
 
 LIB_NAME = "libaderdg_b200.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+# the same sources built with ADG_DEBUG_CHECKS (build.py): record stamps, bounds,
+# poisoned shared memory, jittered barriers, reversed cell order
+DEBUG_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libaderdg_b200_debug.so")
+_debug_lib = None
 
 ADG_OK, ADG_ERR_CONFIG, ADG_ERR_NUMERICAL, ADG_ERR_RUNTIME, ADG_ERR_PREDICTOR = 0, 2, 3, 4, 5
 ADG_BUF_Q, ADG_BUF_D, ADG_BUF_TRACE0, ADG_BUF_TRACE1, ADG_BUF_REDUCE = range(5)
@@ -86,9 +90,13 @@ def _preload_nccl():
         pass
 
 
-def load_library(path=None):
+def load_library(path=None, debug=False):
     """Load (once) and prototype the CUDA library; raise if it is missing."""
-    global _lib
+    global _lib, _debug_lib
+    if debug:
+        if _debug_lib is None:
+            _debug_lib = load_library(DEBUG_LIB_PATH)
+        return _debug_lib
     if _lib is not None and path is None:
         return _lib
     p = path or LIB_PATH
@@ -168,8 +176,8 @@ def dptr(a):
 class Handle:
     """Owning wrapper of one ``adg_handle``; maps status codes to exceptions."""
 
-    def __init__(self, cfg):
-        self.lib = load_library()
+    def __init__(self, cfg, debug=False):
+        self.lib = load_library(debug=debug)
         self.h = ctypes.c_void_p()
         st = self.lib.adg_create(ctypes.byref(cfg), ctypes.byref(self.h))
         self.check(st, "adg_create")

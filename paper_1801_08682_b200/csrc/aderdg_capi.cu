@@ -397,6 +397,7 @@ static SweepParams sweep_params(adg_handle* h, int mode) {
   P.cell_a = 0;
   P.blk_split = INT_MAX;
   P.cell_jump = 0;
+  P.sweep = h->sweep_index;
   P.outflow = h->cfg.boundary == 1 ? 1 : 0;
   // limiter hooks: the corrector of step s snapshots prev_Q into lim_prev[s & 1]
   P.lim_troubled = h->lim ? h->lim_troubled : nullptr;
@@ -530,6 +531,14 @@ static adg_status status_from_state(adg_handle* h) {
     case ADG_EK_SUBCELL:
       snprintf(buf, sizeof buf, "subcell update left cell %lld inadmissible", s.err_cell);
       return fail(h, ADG_ERR_NUMERICAL, buf);
+    case ADG_EK_STALE:
+      snprintf(buf, sizeof buf, "stale face record read by cell %lld at step %d (debug check)", s.err_cell,
+               s.err_step);
+      return fail(h, ADG_ERR_RUNTIME, buf);
+    case ADG_EK_BOUNDS:
+      snprintf(buf, sizeof buf, "cell / record slot out of bounds in cell %lld at step %d (debug check)",
+               s.err_cell, s.err_step);
+      return fail(h, ADG_ERR_RUNTIME, buf);
   }
   return fail(h, ADG_ERR_RUNTIME, "unknown device status");
 }

@@ -176,6 +176,7 @@ template <class PDE, int DIM>
 __global__ void __launch_bounds__(256) lim_detect_kernel(const LimParams L) {
   constexpr int M = PDE::M;
   extern __shared__ double sm[];
+  ADG_DEBUG_POISON();
   DevState* st = L.st;
   if (st->status != 0 || st->reduce[1] != 0) return;
   const int cell = blockIdx.x;

@@ -167,6 +167,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
   double* sFace = smem + S::OFF_FACE;
   double* sDH = smem + S::OFF_DH;     // [k][c][THREADS*NPT] (DH_SMEM)
   int* sTab = reinterpret_cast<int*>(smem + S::OFF_TAB);   // [axis][RP]: c*SC + ib*sb + ic*sc2
+  ADG_DEBUG_POISON();
 
   DevState* st = P.st;
   if (st->status != 0) return;
@@ -229,6 +230,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
         nb_slot[f] = (long long)(plane + 1) * P.plane_cells + rest + (ja - ia) * st_a;
       }
     }
+    if (tid == 0) debug_check_records<DIM>(P, st, cell, gcell, own_slot, nb_slot, REC, 2 * NF * M);
     for (int e = tid; e < 2 * DIM * NF * M; e += THREADS) {
       const int f = e / (NF * M), yc = e % (NF * M);
       const double* own = P.tr_in + ((long long)f * P.slots + own_slot) * REC;
@@ -803,7 +805,7 @@ if constexpr (FA) {
   if (tid < 2 * DIM) {
     double* rec = P.tr_out + ((long long)tid * P.slots + own_slot) * REC;
     rec[2 * NF * M] = __longlong_as_double((long long)sSmax[tid]);
-    rec[2 * NF * M + 1] = 0.0;
+    rec[2 * NF * M + 1] = record_stamp(P);
   }
 }
 

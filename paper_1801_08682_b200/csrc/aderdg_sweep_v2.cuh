@@ -220,6 +220,7 @@ sweep_kernel_v2(const SweepParams P) {
   double* sF = sU;                                     // predictor: [TS][DS][M][PS]
   double* sDiv = sU + (S::R_F > S::R_FB ? S::R_F : S::R_FB);   // [NQ][M][NSP]
   double* sFace = smem + S::OFF_FACE;
+  ADG_DEBUG_POISON();
 
   DevState* st = P.st;
   if (st->status != 0) return;
@@ -263,6 +264,7 @@ sweep_kernel_v2(const SweepParams P) {
     bulk_g2s(sQ, Qg, NS * M * 8, bar);
     if (mode_corrects(mode)) {
       bulk_g2s(sD, Dg, NS * M * 8, bar);
+      long long nbs[2 * DIM];
       for (int f = 0; f < 2 * DIM; ++f) {
         const int a = f >> 1;
         const int dir = (f & 1) ? 1 : -1;
@@ -280,7 +282,9 @@ sweep_kernel_v2(const SweepParams P) {
         bulk_g2s(sRec + f * REC, P.tr_in + ((long long)f * P.slots + own_slot) * REC, REC * 8, bar);
         bulk_g2s(sRec + (2 * DIM + f) * REC, P.tr_in + ((long long)(f ^ 1) * P.slots + nb) * REC, REC * 8,
                  bar);
+        nbs[f] = nb;
       }
+      debug_check_records<DIM>(P, st, cell, gcell, own_slot, nbs, REC, 2 * NF * M);
     }
   }
   // predictor setup that needs no cell data, while the bulk copies land
@@ -1081,7 +1085,7 @@ sweep_kernel_v2(const SweepParams P) {
   if (tid < 2 * DIM) {
     double* rec = P.tr_out + ((long long)tid * P.slots + own_slot) * REC;
     rec[2 * NF * M] = __longlong_as_double((long long)sSmax[tid]);
-    rec[2 * NF * M + 1] = 0.0;
+    rec[2 * NF * M + 1] = record_stamp(P);
   }
 }
 

@@ -128,7 +128,7 @@ class SlabDriver:
     def __init__(self, Q_global, d, L, p, rank, world, device, cfl=0.9, c_dt=0.99,
                  averaging="strict", forced_dt=None, inject_rerun=False,
                  spike_step=None, spike_factor=3.0, group=None, staged=False, halo_mode=0,
-                 mode="fused", overlap=True):
+                 mode="fused", overlap=True, debug_checks=False):
         import torch
         from .basis import make_basis
         from .solver import upload_operators
@@ -149,7 +149,7 @@ class SlabDriver:
         cfg.driver_mode = 1 if mode == "straightforward" else 0
         self.mode = mode
         self.overlap = bool(overlap)
-        self.handle = _lib.Handle(cfg)
+        self.handle = _lib.Handle(cfg, debug=debug_checks)
         self._ops = upload_operators(self.handle, make_basis(p))
         self.lay = lay = self.handle.layout()
         self.stream = torch.cuda.current_stream(self.dev)

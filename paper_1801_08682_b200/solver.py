@@ -314,7 +314,7 @@ class Driver:
     def __init__(self, grid, kernels, time_control, mode="fused",
                  traversal="lexicographic", parallel=False, n_workers=4,
                  inject_rerun=False, spike_step=None, spike_factor=3.0,
-                 limiter=None, device=0, host_sync="step", devices=None):
+                 limiter=None, device=0, host_sync="step", devices=None, debug_checks=False):
         if mode not in ("straightforward", "shifted", "fused"):
             raise ConfigurationError(f"unknown scheduler mode {mode!r}")
         if mode == "shifted":
@@ -361,7 +361,9 @@ class Driver:
             return
         cfg = _config(grid, kernels, time_control, inject_rerun, spike_step, spike_factor, device,
                       mode=mode)
-        self.handle = _lib.Handle(cfg)
+        # debug_checks: the ADG_DEBUG_CHECKS build of the same kernels (stale-record and
+        # bounds checks, poisoned shared memory, jittered barriers; DeviceError on a hit)
+        self.handle = _lib.Handle(cfg, debug=debug_checks)
         self._ops = upload_operators(self.handle, kernels.basis)
         if limiter is not None:
             # SubcellLimiter operators + the traversal that fixes whose prev_Q the
