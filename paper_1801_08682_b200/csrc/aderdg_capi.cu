@@ -23,6 +23,7 @@
 #include "aderdg_kernels.cuh"
 #include "aderdg_sweep_v2.cuh"
 #include "aderdg_sweep_ho.cuh"
+#include "aderdg_sweep_p5.cuh"
 #include "aderdg_limiter.cuh"
 
 using namespace adg;
@@ -139,6 +140,20 @@ Dispatch make_dispatch_ho() {
   return Dispatch{&launch_sweep_ho<NQ>, ShapeHO<NQ>::REC, &occ_ho<NQ>};
 }
 
+// 3D p = 5: Picard derivatives on DMMA, two CTAs per SM (aderdg_sweep_p5.cuh)
+void launch_sweep_p5(const SweepParams& P, unsigned grid, cudaStream_t s) {
+  static std::atomic<unsigned long long> optin{0};
+  ensure_smem_optin(sweep_kernel_p5, ShapeP5::SMEM_BYTES, optin);
+  sweep_kernel_p5<<<grid, ShapeP5::THREADS, ShapeP5::SMEM_BYTES, s>>>(P);
+}
+
+int occ_p5() { return occupancy_of(sweep_kernel_p5, ShapeP5::THREADS, ShapeP5::SMEM_BYTES); }
+
+Dispatch make_dispatch_p5() {
+  static_assert(ShapeP5::REC == Shape<3, 6>::REC, "record layout must match");
+  return Dispatch{&launch_sweep_p5, ShapeP5::REC, &occ_p5};
+}
+
 template <int NQ, int TS, bool DMMA, bool ROLLED, int MB>
 int occ_v2() {
   using S = ShapeV2<NQ, TS, DMMA, ROLLED, MB>;
@@ -228,7 +243,7 @@ bool dispatch_for(int d, int p, int system, Dispatch* out) {
   if (d == 3) {
     switch (n) {
       case 4: *out = make_dispatch_v2<4, 1, true, false, 14>(); return true;
-      case 6: *out = make_dispatch_v2<6, 1, false, false, 31>(); return true;
+      case 6: *out = make_dispatch_p5(); return true;
       case 7: *out = make_dispatch_ho<7>(); return true;
       case 8: *out = make_dispatch_ho<8>(); return true;
       case 9: *out = make_dispatch_ho<9>(); return true;

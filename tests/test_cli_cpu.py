@@ -110,3 +110,28 @@ def test_traffic_models():
     assert metrics.traffic_model("fused", 3, 3, 5, 1.0) == 51 * 5 * 64
     assert metrics.footprint_ratio(3, 3) == metrics.Fraction(20, 35)
     assert metrics.rerun_upper_bound(3.0, 1.5, 1.2, 0.9) == 2.0
+
+
+@pytest.mark.skipif(not os.path.isdir("/root/reference/pkg/src"), reason="reference not present")
+@pytest.mark.parametrize("d,L,p", [(2, 1, 2), (2, 2, 3), (3, 1, 4)])
+def test_l2_error_matches_reference(d, L, p):
+    """The convergence study's L2 error (host post-processing) against the reference's
+    l2_error (src/cli.py:256-275) on a perturbed advection state."""
+    import sys
+    sys.path.insert(0, "/root/reference/pkg/src")
+    from aderdg import cli as rcli
+    from aderdg.basis import make_basis as rbasis
+    from aderdg.mesh import build_grid as rgrid
+    from aderdg.pde import AdvectionSystem as RAdv
+    from paper_1801_08682_b200 import AdvectionSystem
+    from paper_1801_08682_b200.cli import cell_node_coordinates, gaussian_profile, l2_error
+    rng = np.random.default_rng(4)
+    basis = rbasis(p)
+    x = cell_node_coordinates(d, L, basis.nodes)
+    Q = gaussian_profile(x)[..., None] + 1e-3 * rng.standard_normal(x.shape[:-1] + (1,))
+    ours = l2_error(Q, d, L, p, AdvectionSystem(d, (1.0, 0.5, 0.25)[:d], profile=gaussian_profile), 0.03)
+    grid = rgrid(d, L, p, 1, budget_bytes=1 << 40)
+    for c in grid.cells:
+        c.Q[...] = Q[c.index]
+    ref = rcli.l2_error(grid, basis, RAdv(d, (1.0, 0.5, 0.25)[:d], profile=rcli.gaussian_profile), 0.03)
+    assert abs(ours - ref) <= 1e-12 * ref
