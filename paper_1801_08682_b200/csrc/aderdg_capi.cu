@@ -45,6 +45,9 @@ void ensure_smem_optin(K kernel, size_t bytes, std::atomic<unsigned long long>& 
   const unsigned long long bit = 1ull << (dev & 63);
   if (done.load(std::memory_order_relaxed) & bit) return;
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  // the whole unified L1 / shared array as shared memory: a kernel node of a captured
+  // graph otherwise keeps the default carveout, which holds fewer of these CTAs per SM
+  cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
   done.fetch_or(bit, std::memory_order_relaxed);
 }
 
@@ -243,7 +246,11 @@ bool dispatch_for(int d, int p, int system, Dispatch* out) {
   if (d == 3) {
     switch (n) {
       case 4: *out = make_dispatch_v2<4, 1, true, false, 14>(); return true;
+#ifdef ADG_AB_P5_V2
+      case 6: *out = make_dispatch_v2<6, 1, false, false, 31>(); return true;   // A/B builds only
+#else
       case 6: *out = make_dispatch_p5(); return true;
+#endif
       case 7: *out = make_dispatch_ho<7>(); return true;
       case 8: *out = make_dispatch_ho<8>(); return true;
       case 9: *out = make_dispatch_ho<9>(); return true;

@@ -54,13 +54,49 @@ __device__ __forceinline__ void tmem_dealloc_cols(uint32_t t) {
   asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(t), "n"(COLS) : "memory");
 }
 
+// six doubles at 12 consecutive columns: one .x8 and one .x4 access (the column
+// address needs no alignment to the access width, tools/tmem_align.cu)
+__device__ __forceinline__ void tmem_ld6(uint32_t a, double (&v)[6]) {
+  uint32_t r[12];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(a));
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11])
+               : "r"(a + 8));
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11])::"memory");
+#pragma unroll
+  for (int i = 0; i < 6; ++i) v[i] = __hiloint2double((int)r[2 * i + 1], (int)r[2 * i]);
+}
+__device__ __forceinline__ void tmem_st6(uint32_t a, const double (&v)[6]) {
+  uint32_t r[12];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    r[2 * i] = (uint32_t)__double2loint(v[i]);
+    r[2 * i + 1] = (uint32_t)__double2hiint(v[i]);
+  }
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(a), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(a + 8), "r"(r[8]), "r"(r[9]),
+               "r"(r[10]), "r"(r[11])
+               : "memory");
+}
+
 struct ShapeP5 {
   static constexpr int DIM = 3, M = 5, NQ = 6;
   static constexpr int NS = 216, NF = 36;
   static constexpr int THREADS = 224, NW = 7;
   static constexpr int REC = 2 * NF * M + 2;
   // DMMA operand arrays [slice parity][axis][j][STR]
-  static constexpr int NCOL = 180, NTILE = 23, STR = 196;
+  static constexpr int NCOL = 180, NTILE = 23;
+#ifndef ADG_P5_STR
+  static constexpr int STR = 200;
+#else
+  static constexpr int STR = ADG_P5_STR;
+#endif
   static constexpr int ABUF = NQ * STR;
   static constexpr int FBUF = DIM * ABUF;
   static constexpr int TILES = DIM * NTILE;
@@ -82,10 +118,10 @@ struct ShapeP5 {
   static constexpr int TOTAL = OFF_U + R_U;
   static constexpr size_t SMEM_BYTES = sizeof(double) * TOTAL;
   static_assert(SMEM_BYTES <= 112 * 1024, "two CTAs per SM");
-  static_assert(STR >= NTILE * 8 && STR % 16 == 4, "B-fragment bank layout");
+  static_assert(STR >= NTILE * 8 && STR % 2 == 0, "operand row layout");
 };
 
-__global__ void __maxnreg__(144) sweep_kernel_p5(const SweepParams P) {
+__global__ void __launch_bounds__(ShapeP5::THREADS, 2) sweep_kernel_p5(const SweepParams P) {
   using S = ShapeP5;
   constexpr int DIM = 3, M = 5, NQ = 6, NS = S::NS, NF = S::NF, REC = S::REC, NW = S::NW;
   constexpr int THREADS = S::THREADS, STR = S::STR, ABUF = S::ABUF, FBUF = S::FBUF;
@@ -165,10 +201,14 @@ __global__ void __maxnreg__(144) sweep_kernel_p5(const SweepParams P) {
   const int fr = lane >> 2, fk = lane & 3;
   const double a_lo = (fr < NQ) ? P.ops.diff[fr][fk] : 0.0;
   const double a_hi = (fr < NQ && fk < 2) ? P.ops.diff[fr][fk + 4] : 0.0;
+  // lane offsets inside a tile: B fragment rows k / k + 4 at column n, D row r columns 2k, 2k+1
+  const int lb0 = fk * STR + fr, lb1 = (fk + 4) * STR + fr, lbd = fr * STR + 2 * fk;
   // owner offsets into one slice buffer: axis a, row i_a, column (other two indices)
-  const int own0 = 0 * ABUF + i0 * STR + i1 * NQ + i2;
-  const int own1 = 1 * ABUF + i1 * STR + i0 * NQ + i2;
-  const int own2 = 2 * ABUF + i2 * STR + i0 * NQ + i1;
+  // (columns: components 0,1 interleaved over the 36 positions, then 2,3, then 4:
+  //  col = 2o + c | 72 + 2o + (c - 2) | 144 + o, so an owner moves (F_0, F_1) and
+  //  (F_2, F_3) with one 16-byte access each)
+  const int rb[3] = {0 * ABUF + i0 * STR, 1 * ABUF + i1 * STR, 2 * ABUF + i2 * STR};
+  const int ob[3] = {i1 * NQ + i2, i0 * NQ + i2, i0 * NQ + i1};
 
   mbar_wait(bar, 0);
 
@@ -293,7 +333,7 @@ __global__ void __maxnreg__(144) sweep_kernel_p5(const SweepParams P) {
 #pragma unroll
   for (int t = 0; t < NQ; ++t)
 #pragma unroll
-    for (int c = 0; c < M; ++c) tmem_st_d(tq + 2 * (M * t + c), Qx[c]);
+    for (int c = 0; c < M; ++c) tmem_st_d(tq + 12 * c + 2 * t, Qx[c]);
   tmem_wait_st();
 
   int iters = 0;
@@ -305,55 +345,76 @@ __global__ void __maxnreg__(144) sweep_kernel_p5(const SweepParams P) {
       double* B = sU + (k & 1) * FBUF;
       {
         double qk[M], F[DIM][M];
-        tmem_ld_doubles<M>(tq + 2 * M * k, 2, qk);
+        tmem_ld_doubles<M>(tq + 2 * k, 12, qk);
         flux<DIM>(qk, F);
         if (act) {
 #pragma unroll
-          for (int c = 0; c < M; ++c) {
-            B[own0 + c * 36] = F[0][c];
-            B[own1 + c * 36] = F[1][c];
-            B[own2 + c * 36] = F[2][c];
+          for (int a = 0; a < DIM; ++a) {
+            *reinterpret_cast<double2*>(B + rb[a] + 2 * ob[a]) = make_double2(F[a][0], F[a][1]);
+            *reinterpret_cast<double2*>(B + rb[a] + 72 + 2 * ob[a]) = make_double2(F[a][2], F[a][3]);
+            B[rb[a] + 144 + ob[a]] = F[a][4];
           }
         }
       }
       __syncthreads();
       // Out_a = diff . F_a on the tensor cores, in place, tile by tile
+      {
+        // warp w takes tiles w, w + 7, ... (tile = axis * 23 + n-tile): the operand
+        // offset advances by 7 n-tiles and wraps into the next axis block
+        int nt = warp, off = warp * 8;
 #pragma unroll 2
-      for (int tile = warp; tile < S::TILES; tile += NW) {
-        const int a = tile >= 2 * S::NTILE ? 2 : (tile >= S::NTILE ? 1 : 0);
-        double* base = B + a * ABUF + (tile - a * S::NTILE) * 8;
-        const double b0 = base[fk * STR + fr];
-        const double b1 = (fk < 2) ? base[(fk + 4) * STR + fr] : 0.0;
-        double d0, d1;
-        dmma_nv(d0, d1, a_lo, b0, 0.0, 0.0);
-        dmma_nv(d0, d1, a_hi, b1, d0, d1);
-        if (lane < 4 * NQ) *reinterpret_cast<double2*>(base + fr * STR + 2 * fk) = make_double2(d0, d1);
+        for (int tile = warp; tile < S::TILES; tile += NW) {
+          double* base = B + off;
+          const double b0 = base[lb0];
+          const double b1 = (fk < 2) ? base[lb1] : 0.0;
+          double d0, d1;
+          dmma_nv(d0, d1, a_lo, b0, 0.0, 0.0);
+          dmma_nv(d0, d1, a_hi, b1, d0, d1);
+          if (lane < 4 * NQ) *reinterpret_cast<double2*>(base + lbd) = make_double2(d0, d1);
+          nt += NW;
+          off += NW * 8;
+          if (nt >= S::NTILE) {
+            nt -= S::NTILE;
+            off += ABUF - S::NTILE * 8;
+          }
+        }
       }
       __syncthreads();
       // the node's divergence of slice k (idle lanes read a real node's sums and discard them)
+      {
+        double o[DIM][M];
 #pragma unroll
-      for (int c = 0; c < M; ++c)
-        tmem_st_d(td + 2 * (M * k + c), (B[own0 + c * 36] + B[own1 + c * 36]) + B[own2 + c * 36]);
+        for (int a = 0; a < DIM; ++a) {
+          const double2 u = *reinterpret_cast<const double2*>(B + rb[a] + 2 * ob[a]);
+          const double2 v = *reinterpret_cast<const double2*>(B + rb[a] + 72 + 2 * ob[a]);
+          o[a][0] = u.x; o[a][1] = u.y; o[a][2] = v.x; o[a][3] = v.y;
+          o[a][4] = B[rb[a] + 144 + ob[a]];
+        }
+#pragma unroll
+        for (int c = 0; c < M; ++c) tmem_st_d(td + 12 * c + 2 * k, (o[0][c] + o[1][c]) + o[2][c]);
+      }
     }
     tmem_wait_st();
-    // time contraction of the divergence history + Picard update (kernels.py:86-97);
-    // convergence from the bit patterns of |q_new - q|
-    double dvh[NQ * M];
-    tmem_ld_doubles<NQ * M>(td, 2, dvh);
+    // time contraction of the divergence history + Picard update (kernels.py:86-97),
+    // one component at a time (its six divergences and six old levels); convergence
+    // from the bit patterns of |q_new - q|
     BitMax bm;
 #pragma unroll
-    for (int t = 0; t < NQ; ++t) {
-      double qo[M];
-      tmem_ld_doubles<M>(tq + 2 * M * t, 2, qo);
+    for (int c = 0; c < M; ++c) {
+      double dk[NQ], qo[NQ];
+      tmem_ld6(td + 12 * c, dk);
+      tmem_ld6(tq + 12 * c, qo);
+      const double qc = sQ[x * M + c];
+      double qn[NQ];
 #pragma unroll
-      for (int c = 0; c < M; ++c) {
-        double acc = P.ops.integ[t][0] * dvh[c];
+      for (int t = 0; t < NQ; ++t) {
+        double acc = P.ops.integ[t][0] * dk[0];
 #pragma unroll
-        for (int k = 1; k < NQ; ++k) acc = fma(P.ops.integ[t][k], dvh[M * k + c], acc);
-        const double qn = sQ[x * M + c] - scale * acc;
-        bm.add(fabs(qn - qo[c]));
-        tmem_st_d(tq + 2 * (M * t + c), qn);
+        for (int k = 1; k < NQ; ++k) acc = fma(P.ops.integ[t][k], dk[k], acc);
+        qn[t] = qc - scale * acc;
+        bm.add(fabs(qn[t] - qo[t]));
       }
+      tmem_st6(tq + 12 * c, qn);
     }
     tmem_wait_st();
     iters = it + 1;
@@ -362,22 +423,25 @@ __global__ void __maxnreg__(144) sweep_kernel_p5(const SweepParams P) {
     if (fl & 1) break;
   }
 
-  // final flux: time average (fbar) + finiteness; q of every level back to registers
-  double q[NQ][M];
+  // final flux: time average (fbar) + finiteness, level by level from TMEM; every
+  // level of q (for the space-time trace speeds) and qbar into shared memory (the
+  // operand buffers are free: the last slice's owner loads precede the convergence
+  // barrier)
+  double fb[DIM][M], qb[M];
 #pragma unroll
-  for (int t = 0; t < NQ; ++t) tmem_ld_doubles<M>(tq + 2 * M * t, 2, q[t]);
-  tmem_fence_before();
-  double fb[DIM][M];
+  for (int c = 0; c < M; ++c) {
+    qb[c] = 0.0;
 #pragma unroll
-  for (int a = 0; a < DIM; ++a)
+    for (int a = 0; a < DIM; ++a) fb[a][c] = 0.0;
+  }
+  bool bad = false;
 #pragma unroll
-    for (int c = 0; c < M; ++c) fb[a][c] = 0.0;
-  if (!failed) {
-    bool bad = false;
-#pragma unroll
-    for (int t = 0; t < NQ; ++t) {
+  for (int t = 0; t < NQ; ++t) {
+    double qt[M];
+    tmem_ld_doubles<M>(tq + 2 * t, 12, qt);
+    if (!failed) {
       double F[DIM][M];
-      flux<DIM>(q[t], F);
+      flux<DIM>(qt, F);
 #pragma unroll
       for (int a = 0; a < DIM; ++a)
 #pragma unroll
@@ -386,10 +450,14 @@ __global__ void __maxnreg__(144) sweep_kernel_p5(const SweepParams P) {
           fb[a][c] = fma(P.ops.w[t], F[a][c], fb[a][c]);
         }
     }
-    failed = __syncthreads_or(act && bad);
-  } else {
-    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+      if (act) sQt[(t * M + c) * NS + x] = qt[c];
+      qb[c] = fma(P.ops.w[t], qt[c], qb[c]);
+    }
   }
+  tmem_fence_before();
+  failed = __syncthreads_or(act && bad) || failed;
   // every TMEM access of the CTA precedes the barrier above: release the columns
   tmem_fence_after();
   if (warp == 0) tmem_dealloc_cols<256>(s_tmem);
@@ -406,18 +474,10 @@ __global__ void __maxnreg__(144) sweep_kernel_p5(const SweepParams P) {
     atomicAdd((unsigned long long*)&st->hist[iters < HIST_BINS ? iters : HIST_BINS - 1], 1ull);
   }
 
-  // every time level of q, qbar and fbar in C-order node layout (the operand buffers
-  // are free: the last slice's owner loads precede the convergence barrier)
   if (act) {
 #pragma unroll
     for (int c = 0; c < M; ++c) {
-      double v = 0.0;
-#pragma unroll
-      for (int t = 0; t < NQ; ++t) {
-        sQt[(t * M + c) * NS + x] = q[t][c];
-        v = fma(P.ops.w[t], q[t][c], v);
-      }
-      sQb[c * NS + x] = v;
+      sQb[c * NS + x] = qb[c];
 #pragma unroll
       for (int a = 0; a < DIM; ++a) sFb[(a * M + c) * NS + x] = fb[a][c];
     }
