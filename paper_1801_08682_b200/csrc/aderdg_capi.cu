@@ -24,6 +24,7 @@
 #include "aderdg_sweep_v2.cuh"
 #include "aderdg_sweep_ho.cuh"
 #include "aderdg_sweep_p5.cuh"
+#include "aderdg_sweep_p9.cuh"
 #include "aderdg_limiter.cuh"
 
 using namespace adg;
@@ -157,6 +158,20 @@ Dispatch make_dispatch_p5() {
   return Dispatch{&launch_sweep_p5, ShapeP5::REC, &occ_p5};
 }
 
+// 3D p = 9: the Picard state of the cell in TMEM + shared memory (aderdg_sweep_p9.cuh)
+void launch_sweep_p9(const SweepParams& P, unsigned grid, cudaStream_t s) {
+  static std::atomic<unsigned long long> optin{0};
+  ensure_smem_optin(sweep_kernel_p9, ShapeP9::SMEM_BYTES, optin);
+  sweep_kernel_p9<<<grid, ShapeP9::THREADS, ShapeP9::SMEM_BYTES, s>>>(P);
+}
+
+int occ_p9() { return occupancy_of(sweep_kernel_p9, ShapeP9::THREADS, ShapeP9::SMEM_BYTES); }
+
+Dispatch make_dispatch_p9() {
+  static_assert(ShapeP9::REC == Shape<3, 10>::REC, "record layout must match");
+  return Dispatch{&launch_sweep_p9, ShapeP9::REC, &occ_p9};
+}
+
 template <int NQ, int TS, bool DMMA, bool ROLLED, int MB>
 int occ_v2() {
   using S = ShapeV2<NQ, TS, DMMA, ROLLED, MB>;
@@ -254,7 +269,11 @@ bool dispatch_for(int d, int p, int system, Dispatch* out) {
       case 7: *out = make_dispatch_ho<7>(); return true;
       case 8: *out = make_dispatch_ho<8>(); return true;
       case 9: *out = make_dispatch_ho<9>(); return true;
-      case 10: *out = make_dispatch_ho<10>(); return true;
+#ifdef ADG_AB_P9_HO
+      case 10: *out = make_dispatch_ho<10>(); return true;                       // A/B builds only
+#else
+      case 10: *out = make_dispatch_p9(); return true;
+#endif
     }
   }
   return dispatch_generic(d, p, out);
@@ -680,6 +699,19 @@ adg_status adg_set_operators(adg_handle* h, const double* nodes, const double* w
       // kvol[i, j] = diff[j, i] * w[j] / w[i]     kernels.py:56
       h->ops.kvol[i][j] = (diff[j * n + i] * weights[j]) / weights[i];
     }
+  }
+  if (n % 2 == 0) {
+    // even / odd blocks of diff (exact for a centro-antisymmetric matrix,
+    // diff[n-1-i][n-1-j] = -diff[i][j]; the reference's operators satisfy it to
+    // rounding): averaged over the two mirror rows
+    const int hn = n / 2;
+    for (int i = 0; i < hn; ++i)
+      for (int j = 0; j < hn; ++j) {
+        const double a = diff[i * n + j], b = diff[i * n + (n - 1 - j)];
+        const double am = -diff[(n - 1 - i) * n + (n - 1 - j)], bm = -diff[(n - 1 - i) * n + j];
+        h->ops.eo_e[i][j] = 0.25 * ((a + b) + (am + bm));
+        h->ops.eo_o[i][j] = 0.25 * ((a - b) + (am - bm));
+      }
   }
   h->ops_set = true;
   return ADG_OK;
