@@ -24,6 +24,7 @@
 #include "aderdg_sweep_v2.cuh"
 #include "aderdg_sweep_ho.cuh"
 #include "aderdg_sweep_p5.cuh"
+#include "aderdg_sweep_p7.cuh"
 #include "aderdg_sweep_p9.cuh"
 #include "aderdg_limiter.cuh"
 
@@ -158,6 +159,20 @@ Dispatch make_dispatch_p5() {
   return Dispatch{&launch_sweep_p5, ShapeP5::REC, &occ_p5};
 }
 
+// 3D p = 7: Picard state in TMEM + shared memory, exact DMMA tiles (aderdg_sweep_p7.cuh)
+void launch_sweep_p7(const SweepParams& P, unsigned grid, cudaStream_t s) {
+  static std::atomic<unsigned long long> optin{0};
+  ensure_smem_optin(sweep_kernel_p7, ShapeP7::SMEM_BYTES, optin);
+  sweep_kernel_p7<<<grid, ShapeP7::THREADS, ShapeP7::SMEM_BYTES, s>>>(P);
+}
+
+int occ_p7() { return occupancy_of(sweep_kernel_p7, ShapeP7::THREADS, ShapeP7::SMEM_BYTES); }
+
+Dispatch make_dispatch_p7() {
+  static_assert(ShapeP7::REC == Shape<3, 8>::REC, "record layout must match");
+  return Dispatch{&launch_sweep_p7, ShapeP7::REC, &occ_p7};
+}
+
 // 3D p = 9: the Picard state of the cell in TMEM + shared memory (aderdg_sweep_p9.cuh)
 void launch_sweep_p9(const SweepParams& P, unsigned grid, cudaStream_t s) {
   static std::atomic<unsigned long long> optin{0};
@@ -253,7 +268,8 @@ bool dispatch_generic(int d, int p, Dispatch* out) {
 
 // The product kernel of every (system, d, p): one instantiation each, no run-time
 // variant selection.  3D Euler: p = 3 sweep_kernel_v2 (DMMA axes 1-2, pipelined
-// slices), p = 5 sweep_kernel_v2 node blocks, p = 6..9 sweep_kernel_ho; the rest
+// slices), p = 5 sweep_kernel_p5, p = 7 sweep_kernel_p7, p = 9 sweep_kernel_p9,
+// p = 6, 8 sweep_kernel_ho; the rest
 // (2D, 3D p <= 2, p = 4) run the generic kernel.
 bool dispatch_for(int d, int p, int system, Dispatch* out) {
   const int n = p + 1;
@@ -267,7 +283,11 @@ bool dispatch_for(int d, int p, int system, Dispatch* out) {
       case 6: *out = make_dispatch_p5(); return true;
 #endif
       case 7: *out = make_dispatch_ho<7>(); return true;
-      case 8: *out = make_dispatch_ho<8>(); return true;
+#ifdef ADG_AB_P7_HO
+      case 8: *out = make_dispatch_ho<8>(); return true;                         // A/B builds only
+#else
+      case 8: *out = make_dispatch_p7(); return true;
+#endif
       case 9: *out = make_dispatch_ho<9>(); return true;
 #ifdef ADG_AB_P9_HO
       case 10: *out = make_dispatch_ho<10>(); return true;                       // A/B builds only

@@ -401,8 +401,11 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
   };
 #pragma unroll 1
   for (int it = 0; it < cap; ++it) {
+    // first iteration: q_t = Q at every time level, so its NQ slices are identical —
+    // one is computed and its divergence stored for every k
+    const int nsl = (FA && it == 0) ? 1 : NQ;
 #pragma unroll 1
-    for (int k = 0; k < NQ; ++k) {
+    for (int k = 0; k < nsl; ++k) {
       double F[NPT][DIM][M];
 #pragma unroll
       for (int n = 0; n < NPT; ++n) {
@@ -495,7 +498,13 @@ if constexpr (FA) {
           for (int c = 0; c < M; ++c) {
             const double v = (sFA[c * SC + pn[n]] + sFA[S::R_FA + c * SC + pn[n]]) +
                              sFA[2 * S::R_FA + c * SC + pn[n]];
-            if (TM == 2 && n == 0) tmem_st_d(tq + 2 * (NQ * c + k), v);
+            if (it == 0) {
+#pragma unroll
+              for (int kk = 0; kk < NQ; ++kk) {
+                if (TM == 2 && n == 0) tmem_st_d(tq + 2 * (NQ * c + kk), v);
+                else dhp(n, kk, c) = v;
+              }
+            } else if (TM == 2 && n == 0) tmem_st_d(tq + 2 * (NQ * c + k), v);
             else dhp(n, k, c) = v;
           }
       } else {

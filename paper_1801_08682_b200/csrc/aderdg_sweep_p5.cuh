@@ -1,10 +1,10 @@
 // aderdg_sweep_p5.cuh — the fused 3D sweep at p = 5 with the Picard derivatives
 // on the FP64 tensor cores.
 //
-// One CTA per cell, 224 threads (7 warps; thread = spatial node in the p = 5 warp
-// blocks of block_map_p5), two CTAs per SM (<= 144 registers, 104 KB of shared
-// memory).  The per-node time line q[t][c] and the Picard accumulator acc[t][c]
-// stay in registers, so the time contraction (integ) is register-local DFMA work.
+// One CTA per cell, 224 threads (7 warps; thread = spatial node, block_map_p5b), two
+// CTAs per SM (128 registers, 104 KB of shared memory, 256 TMEM columns each).  The
+// per-node time line q[t][c] and the divergence history dv[k][c] live in tensor memory
+// (tcgen05.ld/st 32x32b), so the time contraction (integ) is register-local DFMA work.
 // The spatial derivatives of a time slice are three small GEMMs per slice,
 //
 //     Out_a[i][col] = sum_j diff[i][j] F_a[j][col],   col = c*36 + (other two indices)
@@ -14,18 +14,22 @@
 // and columns 6..7 zero) and the flux as the B operand straight from shared memory;
 // each tile writes its 6 useful output rows back in place over its own columns
 // (a tile's outputs depend only on its own columns), and the node owner sums the
-// three axes.  Per slice: flux -> 15 owner stores -> barrier -> 69 tiles over the 7
-// warps -> barrier -> 15 owner loads + 30 FMAs of the time contraction; the operand
-// arrays are double-buffered by slice parity, so two barriers per slice.
+// three axes.
+//
+// Slice pipeline (one barrier per slice): the operand arrays are double-buffered by
+// slice parity; the interval that runs the tiles of slice k also stages the flux of
+// slice k + 1, and the first Picard iteration (q_t = Q at every level: six identical
+// slices) computes one slice.
+//
+// Shared-memory layout (the kernel is bound by shared-memory wavefronts: r02 ncu,
+// 67 % of the LSU peak at 1.5-2x the ideal wavefront count before this layout): row
+// stride 200 with rows 2, 3 shifted by 4 doubles, thread blocks of 2x2x2 nodes per
+// quarter-warp grouped into warps by a search (block_map_p5b) — every shared access of
+// the Picard loop then takes its minimum number of wavefronts.
 //
 // The rest (TMA bulk staging of Q, D and the 4d face records, Riemann, corrector,
 // calc_time_step, final flux, volume integral, face traces, s_max) follows
-// sweep_kernel_v2 with the node layout in C order.
-//
-// Row stride STR = 196 == 4 (mod 16): a B-fragment load (4 rows x 8 columns) hits 32
-// distinct bank pairs per half-warp pair (two wavefronts, the minimum); the owner
-// stores / loads of the warp blocks cost 2.4 wavefronts per instruction (model,
-// tools/p5_banks.py).
+// sweep_kernel_v2.
 //
 // Reference (src/ = /root/reference/pkg/src/aderdg/): kernels.py:68-229 (predict,
 // extrapolate, integrate_volume, solve_riemann, integrate_face, update,
@@ -85,6 +89,24 @@ __device__ __forceinline__ void tmem_st6(uint32_t a, const double (&v)[6]) {
                : "memory");
 }
 
+// Thread -> node map of the p = 5 kernel.  Eight consecutive lanes own a 2x2x2 node
+// block (lane bits 2,1,0 = the i0, i1, i2 offsets); a warp owns four of the 27 blocks
+// (the last warp three), grouped so that with the operand row offsets below
+//   * a 16-byte owner access of a quarter-warp (one block) touches eight distinct
+//     16-byte bank groups along all three axes, and
+//   * an 8-byte owner access of a warp touches every 8-byte bank at most twice
+// (the minimum for 32 distinct doubles).  The grouping comes from an exhaustive search
+// over the partitions of the 3x3x3 block grid (block code = 9 B0 + 3 B1 + B2).
+__device__ __forceinline__ void block_map_p5b(int tid, int& i0, int& i1, int& i2, bool& act) {
+  constexpr unsigned char kBlock[28] = {2, 4, 5, 19, 6, 7, 8, 10, 9, 11, 15, 17, 12, 13, 16, 20, 14, 18, 21, 24, 22, 23, 25, 26, 0, 1, 3, 0};
+  const int blk = tid >> 3;
+  act = blk < 27;
+  const int code = kBlock[blk];
+  i0 = 2 * (code / 9) + ((tid >> 2) & 1);
+  i1 = 2 * ((code / 3) % 3) + ((tid >> 1) & 1);
+  i2 = 2 * (code % 3) + (tid & 1);
+}
+
 struct ShapeP5 {
   static constexpr int DIM = 3, M = 5, NQ = 6;
   static constexpr int NS = 216, NF = 36;
@@ -92,13 +114,15 @@ struct ShapeP5 {
   static constexpr int REC = 2 * NF * M + 2;
   // DMMA operand arrays [slice parity][axis][j][STR]
   static constexpr int NCOL = 180, NTILE = 23;
-#ifndef ADG_P5_STR
   static constexpr int STR = 200;
-#else
-  static constexpr int STR = ADG_P5_STR;
-#endif
   static constexpr int ABUF = NQ * STR;
   static constexpr int FBUF = DIM * ABUF;
+  // operand row j starts at j * STR + 4 for j = 2, 3: with STR == 8 (mod 16) the rows sit
+  // at bank offsets (0, 8, 4, 12, 0, 8) (8-byte banks): the four k rows of a B-fragment
+  // load are disjoint (2 wavefronts), rows 4, 5 of the second chunk too (1), and the row
+  // pairs (0,1), (2,3), (4,5) that a quarter-warp touches with 16-byte accesses (D store,
+  // owner blocks) lie 64 bytes apart (mod 128)
+  __host__ __device__ static constexpr int rowoff(int j) { return j * STR + ((j == 2 || j == 3) ? 4 : 0); }
   static constexpr int TILES = DIM * NTILE;
   static constexpr int R_PRED = 2 * FBUF;
   // after the Picard loop: q of every time level [t][c][NS] | qbar [c][NS] | fbar [a][c][NS]
@@ -118,7 +142,7 @@ struct ShapeP5 {
   static constexpr int TOTAL = OFF_U + R_U;
   static constexpr size_t SMEM_BYTES = sizeof(double) * TOTAL;
   static_assert(SMEM_BYTES <= 112 * 1024, "two CTAs per SM");
-  static_assert(STR >= NTILE * 8 && STR % 2 == 0, "operand row layout");
+  static_assert(STR >= NTILE * 8 + 4 && STR % 16 == 8, "operand row layout");
 };
 
 __global__ void __launch_bounds__(ShapeP5::THREADS, 2) sweep_kernel_p5(const SweepParams P) {
@@ -150,7 +174,7 @@ __global__ void __launch_bounds__(ShapeP5::THREADS, 2) sweep_kernel_p5(const Swe
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int i0, i1, i2;
   bool act;
-  block_map_p5(tid, i0, i1, i2, act);
+  block_map_p5b(tid, i0, i1, i2, act);
   const int x = (i0 * NQ + i1) * NQ + i2;
   const long long cell = sweep_cell(P);
   const long long gcell = cell + P.cell_offset;
@@ -202,12 +226,12 @@ __global__ void __launch_bounds__(ShapeP5::THREADS, 2) sweep_kernel_p5(const Swe
   const double a_lo = (fr < NQ) ? P.ops.diff[fr][fk] : 0.0;
   const double a_hi = (fr < NQ && fk < 2) ? P.ops.diff[fr][fk + 4] : 0.0;
   // lane offsets inside a tile: B fragment rows k / k + 4 at column n, D row r columns 2k, 2k+1
-  const int lb0 = fk * STR + fr, lb1 = (fk + 4) * STR + fr, lbd = fr * STR + 2 * fk;
+  const int lb0 = S::rowoff(fk) + fr, lb1 = S::rowoff(fk < 2 ? fk + 4 : 4) + fr, lbd = S::rowoff(fr < NQ ? fr : 0) + 2 * fk;
   // owner offsets into one slice buffer: axis a, row i_a, column (other two indices)
   // (columns: components 0,1 interleaved over the 36 positions, then 2,3, then 4:
   //  col = 2o + c | 72 + 2o + (c - 2) | 144 + o, so an owner moves (F_0, F_1) and
   //  (F_2, F_3) with one 16-byte access each)
-  const int rb[3] = {0 * ABUF + i0 * STR, 1 * ABUF + i1 * STR, 2 * ABUF + i2 * STR};
+  const int rb[3] = {0 * ABUF + S::rowoff(i0), 1 * ABUF + S::rowoff(i1), 2 * ABUF + S::rowoff(i2)};
   const int ob[3] = {i1 * NQ + i2, i0 * NQ + i2, i0 * NQ + i1};
 
   mbar_wait(bar, 0);
@@ -310,7 +334,8 @@ __global__ void __launch_bounds__(ShapeP5::THREADS, 2) sweep_kernel_p5(const Swe
   // ---------------- predictor (kernels.py:68-105) ----------------
   const double scale = (mode == MODE_RERUN) ? st->scale_old : st->scale_new;   // dt / h (SF: dt_new)
   // the 4 pad columns (180..183) of every operand row are read by the last n-tile: zero
-  for (int e = tid; e < 2 * DIM * NQ * 4; e += THREADS) sU[(e >> 2) * STR + S::NCOL + (e & 3)] = 0.0;
+  for (int e = tid; e < 2 * DIM * NQ * 4; e += THREADS)
+    sU[((e >> 2) / NQ) * ABUF + S::rowoff((e >> 2) % NQ) + S::NCOL + (e & 3)] = 0.0;
   // Per-thread time line in tensor memory: 256 columns per CTA (two CTAs per SM fill
   // the 512), warp w on lanes 32*(w%4) and columns (w/4)*128.. : q[t][c] at column
   // 2(5t+c), the slice divergences dv[k][c] at 64 + 2(5k+c)
@@ -338,60 +363,93 @@ __global__ void __launch_bounds__(ShapeP5::THREADS, 2) sweep_kernel_p5(const Swe
 
   int iters = 0;
   bool failed = false;
+  // Software-pipelined slice loop, one barrier per slice.  The interval that runs the
+  // DMMA tiles of slice k (operand buffer k & 1) also computes the flux of slice k + 1
+  // into the other buffer: that buffer's last tile readers (slice k - 1) passed the
+  // previous barrier, and an owner reads back and rewrites only its own addresses, in
+  // program order.  Two independent chains (TMEM load -> flux -> stores, operand loads
+  // -> DMMA -> stores) share every interval.  The flux of the next iteration's slice 0
+  // is staged before the convergence vote, whose barrier publishes it (wasted once,
+  // when the vote ends the iteration).
+  auto stage_flux = [&](int k, const double (&qk)[M]) {
+    double* B = sU + (k & 1) * FBUF;
+    double F[DIM][M];
+    flux<DIM>(qk, F);
+    if (act) {
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) {
+        *reinterpret_cast<double2*>(B + rb[a] + 2 * ob[a]) = make_double2(F[a][0], F[a][1]);
+        *reinterpret_cast<double2*>(B + rb[a] + 72 + 2 * ob[a]) = make_double2(F[a][2], F[a][3]);
+        B[rb[a] + 144 + ob[a]] = F[a][4];
+      }
+    }
+  };
+  // Out_a = diff . F_a on the tensor cores, in place, tile by tile: warp w takes tiles
+  // w, w + 7, ... (tile = axis * 23 + n-tile): the operand offset advances by 7 n-tiles
+  // and wraps into the next axis block
+  auto run_tiles = [&](int k) {
+    double* B = sU + (k & 1) * FBUF;
+    int nt = warp, off = warp * 8;
+#pragma unroll 2
+    for (int tile = warp; tile < S::TILES; tile += NW) {
+      double* base = B + off;
+      const double b0 = base[lb0];
+      const double b1 = (fk < 2) ? base[lb1] : 0.0;
+      double d0, d1;
+      dmma_nv(d0, d1, a_lo, b0, 0.0, 0.0);
+      dmma_nv(d0, d1, a_hi, b1, d0, d1);
+      if (lane < 4 * NQ) *reinterpret_cast<double2*>(base + lbd) = make_double2(d0, d1);
+      nt += NW;
+      off += NW * 8;
+      if (nt >= S::NTILE) {
+        nt -= S::NTILE;
+        off += ABUF - S::NTILE * 8;
+      }
+    }
+  };
+  // the node's divergence of slice k into its TMEM column (idle lanes read a real
+  // node's sums and discard them); the first iteration's slice stands for every k
+  auto read_back = [&](int k, bool every_k) {
+    const double* B = sU + (k & 1) * FBUF;
+    double o[DIM][M];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+      const double2 u = *reinterpret_cast<const double2*>(B + rb[a] + 2 * ob[a]);
+      const double2 v = *reinterpret_cast<const double2*>(B + rb[a] + 72 + 2 * ob[a]);
+      o[a][0] = u.x; o[a][1] = u.y; o[a][2] = v.x; o[a][3] = v.y;
+      o[a][4] = B[rb[a] + 144 + ob[a]];
+    }
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+      const double dvc = (o[0][c] + o[1][c]) + o[2][c];
+      if (every_k) {
+#pragma unroll
+        for (int kk = 0; kk < NQ; ++kk) tmem_st_d(td + 12 * c + 2 * kk, dvc);
+      } else {
+        tmem_st_d(td + 12 * c + 2 * k, dvc);
+      }
+    }
+  };
+  stage_flux(0, Qx);
+  __syncthreads();
 #pragma unroll 1
   for (int it = 0; it < cap; ++it) {
-#pragma unroll
-    for (int k = 0; k < NQ; ++k) {
-      double* B = sU + (k & 1) * FBUF;
-      {
-        double qk[M], F[DIM][M];
-        tmem_ld_doubles<M>(tq + 2 * k, 12, qk);
-        flux<DIM>(qk, F);
-        if (act) {
-#pragma unroll
-          for (int a = 0; a < DIM; ++a) {
-            *reinterpret_cast<double2*>(B + rb[a] + 2 * ob[a]) = make_double2(F[a][0], F[a][1]);
-            *reinterpret_cast<double2*>(B + rb[a] + 72 + 2 * ob[a]) = make_double2(F[a][2], F[a][3]);
-            B[rb[a] + 144 + ob[a]] = F[a][4];
-          }
-        }
-      }
+    if (it == 0) {
+      // q_t = Q at every time level: the NQ slices are identical, one is computed
+      run_tiles(0);
       __syncthreads();
-      // Out_a = diff . F_a on the tensor cores, in place, tile by tile
-      {
-        // warp w takes tiles w, w + 7, ... (tile = axis * 23 + n-tile): the operand
-        // offset advances by 7 n-tiles and wraps into the next axis block
-        int nt = warp, off = warp * 8;
-#pragma unroll 2
-        for (int tile = warp; tile < S::TILES; tile += NW) {
-          double* base = B + off;
-          const double b0 = base[lb0];
-          const double b1 = (fk < 2) ? base[lb1] : 0.0;
-          double d0, d1;
-          dmma_nv(d0, d1, a_lo, b0, 0.0, 0.0);
-          dmma_nv(d0, d1, a_hi, b1, d0, d1);
-          if (lane < 4 * NQ) *reinterpret_cast<double2*>(base + lbd) = make_double2(d0, d1);
-          nt += NW;
-          off += NW * 8;
-          if (nt >= S::NTILE) {
-            nt -= S::NTILE;
-            off += ABUF - S::NTILE * 8;
-          }
-        }
-      }
-      __syncthreads();
-      // the node's divergence of slice k (idle lanes read a real node's sums and discard them)
-      {
-        double o[DIM][M];
+      read_back(0, true);
+    } else {
 #pragma unroll
-        for (int a = 0; a < DIM; ++a) {
-          const double2 u = *reinterpret_cast<const double2*>(B + rb[a] + 2 * ob[a]);
-          const double2 v = *reinterpret_cast<const double2*>(B + rb[a] + 72 + 2 * ob[a]);
-          o[a][0] = u.x; o[a][1] = u.y; o[a][2] = v.x; o[a][3] = v.y;
-          o[a][4] = B[rb[a] + 144 + ob[a]];
+      for (int k = 0; k < NQ; ++k) {
+        if (k + 1 < NQ) {
+          double qk[M];
+          tmem_ld_doubles<M>(tq + 2 * (k + 1), 12, qk);
+          stage_flux(k + 1, qk);
         }
-#pragma unroll
-        for (int c = 0; c < M; ++c) tmem_st_d(td + 12 * c + 2 * k, (o[0][c] + o[1][c]) + o[2][c]);
+        run_tiles(k);
+        __syncthreads();
+        read_back(k, false);
       }
     }
     tmem_wait_st();
@@ -399,6 +457,7 @@ __global__ void __launch_bounds__(ShapeP5::THREADS, 2) sweep_kernel_p5(const Swe
     // one component at a time (its six divergences and six old levels); convergence
     // from the bit patterns of |q_new - q|
     BitMax bm;
+    double q0n[M];
 #pragma unroll
     for (int c = 0; c < M; ++c) {
       double dk[NQ], qo[NQ];
@@ -414,10 +473,12 @@ __global__ void __launch_bounds__(ShapeP5::THREADS, 2) sweep_kernel_p5(const Swe
         qn[t] = qc - scale * acc;
         bm.add(fabs(qn[t] - qo[t]));
       }
+      q0n[c] = qn[0];
       tmem_st6(tq + 12 * c, qn);
     }
     tmem_wait_st();
     iters = it + 1;
+    if (it + 1 < cap) stage_flux(0, q0n);        // slice 0 of the next iteration
     const int fl = block_flags<NW>(!act || bm.conv(tol), act && bm.bad(), sFlags, it & 1);
     if (fl & 2) { failed = true; break; }
     if (fl & 1) break;

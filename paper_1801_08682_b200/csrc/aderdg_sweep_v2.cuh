@@ -669,35 +669,71 @@ sweep_kernel_v2(const SweepParams P) {
     // and issues its axis-1 DMMA, so two independent dependency chains share every
     // barrier interval.  PIPE2 also issues the slice's axis-2 DMMA (C = 0) there and
     // transposes the axis-1 result back, leaving only the axis-0 gather after the barrier.
+    auto produce = [&](int sl, double (&f2)[M], double (&d1)[M]) {
+      double F[DIM][M];
+      flux<DIM>(q[sl], F);
+      double* sFn = sF + (sl & 1) * (DS * M * PS);
+      if (act) {
+#pragma unroll
+        for (int c = 0; c < M; ++c) sFn[c * PS + px] = F[0][c];
+      }
+#pragma unroll
+      for (int c = 0; c < M; ++c) {
+        const double a1 = __shfl_sync(0xffffffffu, F[1][c], sig);
+        double z1;
+        dmma_8x8x4(d1[c], z1, a1, bfrag, 0.0, 0.0);
+        if (S::PIPE2) dmma_8x8x4(f2[c], z1, F[2][c], bfrag, 0.0, 0.0);
+        else f2[c] = F[2][c];
+      }
+    };
+    auto finish_produce = [&](double (&d1)[M]) {
+      if (S::PIPE2) {
+#pragma unroll
+        for (int c = 0; c < M; ++c) d1[c] = __shfl_sync(0xffffffffu, d1[c], sig);
+      }
+    };
+    bool first_done = false;
+    // First iteration: q_t = Q at every time level, so its NQ slices are identical —
+    // one slice is computed and its divergence contracted against every integ column
+    // (the same operations in the same order as NQ equal slices).
+    {
+      double F2c[M], d1c[M];
+      produce(0, F2c, d1c);
+      finish_produce(d1c);
+      __syncthreads();
+      BitMax bm;
+#pragma unroll
+      for (int c = 0; c < M; ++c) {
+        const double* b = sF + c * PS + gbase[0];
+        double v = 0.0;
+#pragma unroll
+        for (int j = 0; j < NQ; ++j) v = fma(drow[0][j], b[j * gstr[0]], v);
+        double dv = S::PIPE2 ? (v + d1c[c]) + F2c[c] : v + __shfl_sync(0xffffffffu, d1c[c], sig);
+        if (!S::PIPE2) {
+          double d1;
+          dmma_8x8x4(dv, d1, F2c[c], bfrag, dv, 0.0);
+        }
+#pragma unroll
+        for (int t = 0; t < NQ; ++t) {
+          double a = P.ops.integ[t][0] * dv;
+#pragma unroll
+          for (int k = 1; k < NQ; ++k) a = fma(P.ops.integ[t][k], dv, a);
+          const double qn = Qx[c] - scale * a;
+          bm.add(fabs(qn - q[t][c]));
+          q[t][c] = qn;
+        }
+      }
+      iters = 1;
+      const int fl = block_flags<NW>(!act || bm.conv(tol), act && bm.bad(), sFlags, 0);
+      if (fl & 2) failed = true;
+      first_done = fl != 0;
+    }
 #pragma unroll 1
-    for (int it = 0; it < cap; ++it) {
+    for (int it = 1; it < cap && !first_done; ++it) {
       double accr[NQ][M];
       double dvp[M];
       double F2c[M], d1c[M];           // current slice: axis-2 flux (A operand) / PIPE2: axis-2 result,
                                        // axis-1 DMMA result (PIPE2: transposed back)
-      auto produce = [&](int sl, double (&f2)[M], double (&d1)[M]) {
-        double F[DIM][M];
-        flux<DIM>(q[sl], F);
-        double* sFn = sF + (sl & 1) * (DS * M * PS);
-        if (act) {
-#pragma unroll
-          for (int c = 0; c < M; ++c) sFn[c * PS + px] = F[0][c];
-        }
-#pragma unroll
-        for (int c = 0; c < M; ++c) {
-          const double a1 = __shfl_sync(0xffffffffu, F[1][c], sig);
-          double z1;
-          dmma_8x8x4(d1[c], z1, a1, bfrag, 0.0, 0.0);
-          if (S::PIPE2) dmma_8x8x4(f2[c], z1, F[2][c], bfrag, 0.0, 0.0);
-          else f2[c] = F[2][c];
-        }
-      };
-      auto finish_produce = [&](double (&d1)[M]) {
-        if (S::PIPE2) {
-#pragma unroll
-          for (int c = 0; c < M; ++c) d1[c] = __shfl_sync(0xffffffffu, d1[c], sig);
-        }
-      };
       produce(0, F2c, d1c);
       finish_produce(d1c);
 #pragma unroll

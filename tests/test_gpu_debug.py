@@ -53,8 +53,9 @@ def _run(d, L, p, steps, mode="fused", debug=False, system=None, scen="bump", li
 CASES = [
     dict(d=3, L=2, p=3, steps=5, inject_rerun=True),           # sweep_kernel_v2 p=3, graph + rerun nodes
     dict(d=3, L=1, p=5, steps=3),                              # p=5 kernel
-    dict(d=3, L=1, p=7, steps=2),                              # sweep_kernel_ho, TMEM time line
-    dict(d=3, L=1, p=9, steps=2),                              # sweep_kernel_ho, line engine
+    dict(d=3, L=1, p=7, steps=2),                              # p=7 kernel (TMEM + smem state, DMMA tiles)
+    dict(d=3, L=1, p=6, steps=2),                              # sweep_kernel_ho, TMEM time line
+    dict(d=3, L=1, p=9, steps=2),                              # p=9 kernel (TMEM + smem state, line engine)
     dict(d=2, L=2, p=3, steps=5, spike_step=3),                # generic 2D kernel + speed spike
     dict(d=3, L=1, p=4, steps=3),                              # generic 3D kernel
     dict(d=3, L=2, p=3, steps=4, mode="straightforward"),      # straightforward passes

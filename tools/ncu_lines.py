@@ -4,6 +4,9 @@
 
 Maps SASS addresses of the ncu source page onto `nvdisasm -g` line info of the
 in-tree library's cubin (the report must come from the same build)."""
+import os as _os, sys as _sys
+_sys.path.insert(0, _os.path.dirname(_os.path.abspath(__file__)))
+import _ncu_io
 import csv
 import os
 import re
@@ -33,8 +36,7 @@ for l in lines[start + 1:]:
     m = re.search(r"/\*([0-9a-f]{4,})\*/", l)
     if m and cur:
         a2l[int(m.group(1), 16)] = cur
-src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                     capture_output=True, text=True).stdout
+src = _ncu_io.page(rep, "sass")
 rows = list(csv.reader(src.splitlines()))
 h = rows[1]
 ai, ws, ie = h.index("Address"), h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")

@@ -1,5 +1,8 @@
 """Per-source-line shared-memory wavefronts of one kernel (run here, no GPU).
     python tools/ncu_smem_lines.py <report.ncu-rep> <mangled kernel name> [top]"""
+import os as _os, sys as _sys
+_sys.path.insert(0, _os.path.dirname(_os.path.abspath(__file__)))
+import _ncu_io
 import csv, os, re, subprocess, sys, tempfile
 from collections import defaultdict
 rep, kname = sys.argv[1], sys.argv[2]
@@ -20,7 +23,7 @@ for l in dis[start + 1:]:
     m = re.search(r"/\*([0-9a-f]{4,})\*/", l)
     if m and cur:
         a2l[int(m.group(1), 16)] = cur
-src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True, text=True).stdout
+src = _ncu_io.page(rep, "sass")
 rows = list(csv.reader(src.splitlines()))
 h = rows[1]
 ai, wf, wi, sa = h.index("Address"), h.index("L1 Wavefronts Shared"), h.index("L1 Wavefronts Shared Ideal"), h.index("Source")

@@ -1,12 +1,15 @@
 """Summarise an ncu --set full report of the sweep kernel (run here, no GPU):
     python tools/ncu_summary.py gpurun_out/x.ncu-rep [--sass]"""
+import os as _os, sys as _sys
+_sys.path.insert(0, _os.path.dirname(_os.path.abspath(__file__)))
+import _ncu_io
 import csv
 import subprocess
 import sys
 from collections import Counter
 
 rep = sys.argv[1]
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+raw = _ncu_io.page(rep, "raw")
 r = list(csv.reader(raw.splitlines()))
 h, u, v = r[0], r[1], r[2]
 want = ["gpu__time_duration.sum", "launch__registers_per_thread", "sm__warps_active.avg.per_cycle_active",
@@ -35,8 +38,7 @@ for i, name in enumerate(h):
             pass
 print("stalls (cycles per issued instruction):", ", ".join(f"{n}={x:.2f}" for x, n in sorted(items, reverse=True)[:9]))
 if "--sass" in sys.argv:
-    src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                         capture_output=True, text=True).stdout
+    src = _ncu_io.page(rep, "sass")
     rows = list(csv.reader(src.splitlines()))
     hh = rows[1]
     si, ie = hh.index("Source"), hh.index("Instructions Executed")
