@@ -112,11 +112,11 @@ struct ShapeP5 {
   static constexpr int NS = 216, NF = 36;
   static constexpr int THREADS = 224, NW = 7;
   static constexpr int REC = 2 * NF * M + 2;
-  // DMMA operand arrays [slice parity][axis][j][STR]
-  static constexpr int NCOL = 180, NTILE = 23;
-  static constexpr int STR = 200;
-  static constexpr int ABUF = NQ * STR;
-  static constexpr int FBUF = DIM * ABUF;
+  // DMMA operand arrays [slice parity][j][axis][184]: tile t of the slice (t = axis * 23 +
+  // n-tile) starts at column 8 t of every row
+  static constexpr int NCOL = 180, NTILE = 23, ACOL = NTILE * 8;
+  static constexpr int STR = DIM * ACOL + 16;
+  static constexpr int FBUF = NQ * STR;
   // operand row j starts at j * STR + 4 for j = 2, 3: with STR == 8 (mod 16) the rows sit
   // at bank offsets (0, 8, 4, 12, 0, 8) (8-byte banks): the four k rows of a B-fragment
   // load are disjoint (2 wavefronts), rows 4, 5 of the second chunk too (1), and the row
@@ -142,13 +142,13 @@ struct ShapeP5 {
   static constexpr int TOTAL = OFF_U + R_U;
   static constexpr size_t SMEM_BYTES = sizeof(double) * TOTAL;
   static_assert(SMEM_BYTES <= 112 * 1024, "two CTAs per SM");
-  static_assert(STR >= NTILE * 8 + 4 && STR % 16 == 8, "operand row layout");
+  static_assert(STR >= DIM * ACOL + 4 && STR % 16 == 8 && ACOL % 16 == 8, "operand row layout");
 };
 
 __global__ void __launch_bounds__(ShapeP5::THREADS, 2) sweep_kernel_p5(const SweepParams P) {
   using S = ShapeP5;
   constexpr int DIM = 3, M = 5, NQ = 6, NS = S::NS, NF = S::NF, REC = S::REC, NW = S::NW;
-  constexpr int THREADS = S::THREADS, STR = S::STR, ABUF = S::ABUF, FBUF = S::FBUF;
+  constexpr int THREADS = S::THREADS, ACOL = S::ACOL, FBUF = S::FBUF;
 
   extern __shared__ __align__(16) double smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR);
@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(ShapeP5::THREADS, 2) sweep_kernel_p5(const Swe
   // (columns: components 0,1 interleaved over the 36 positions, then 2,3, then 4:
   //  col = 2o + c | 72 + 2o + (c - 2) | 144 + o, so an owner moves (F_0, F_1) and
   //  (F_2, F_3) with one 16-byte access each)
-  const int rb[3] = {0 * ABUF + S::rowoff(i0), 1 * ABUF + S::rowoff(i1), 2 * ABUF + S::rowoff(i2)};
+  const int rb[3] = {0 * ACOL + S::rowoff(i0), 1 * ACOL + S::rowoff(i1), 2 * ACOL + S::rowoff(i2)};
   const int ob[3] = {i1 * NQ + i2, i0 * NQ + i2, i0 * NQ + i1};
 
   mbar_wait(bar, 0);
@@ -334,8 +334,10 @@ __global__ void __launch_bounds__(ShapeP5::THREADS, 2) sweep_kernel_p5(const Swe
   // ---------------- predictor (kernels.py:68-105) ----------------
   const double scale = (mode == MODE_RERUN) ? st->scale_old : st->scale_new;   // dt / h (SF: dt_new)
   // the 4 pad columns (180..183) of every operand row are read by the last n-tile: zero
-  for (int e = tid; e < 2 * DIM * NQ * 4; e += THREADS)
-    sU[((e >> 2) / NQ) * ABUF + S::rowoff((e >> 2) % NQ) + S::NCOL + (e & 3)] = 0.0;
+  for (int e = tid; e < 2 * DIM * NQ * 4; e += THREADS) {   // e = ((buffer * 3 + axis) * 6 + row) * 4 + pad
+    const int r = (e >> 2) % NQ, ab = (e >> 2) / NQ;
+    sU[(ab / DIM) * FBUF + S::rowoff(r) + (ab % DIM) * ACOL + S::NCOL + (e & 3)] = 0.0;
+  }
   // Per-thread time line in tensor memory: 256 columns per CTA (two CTAs per SM fill
   // the 512), warp w on lanes 32*(w%4) and columns (w/4)*128.. : q[t][c] at column
   // 2(5t+c), the slice divergences dv[k][c] at 64 + 2(5k+c)
@@ -385,26 +387,19 @@ __global__ void __launch_bounds__(ShapeP5::THREADS, 2) sweep_kernel_p5(const Swe
     }
   };
   // Out_a = diff . F_a on the tensor cores, in place, tile by tile: warp w takes tiles
-  // w, w + 7, ... (tile = axis * 23 + n-tile): the operand offset advances by 7 n-tiles
-  // and wraps into the next axis block
+  // w, w + 7, ... of the 69 (constant offsets from one base address)
   auto run_tiles = [&](int k) {
-    double* B = sU + (k & 1) * FBUF;
-    int nt = warp, off = warp * 8;
-#pragma unroll 2
-    for (int tile = warp; tile < S::TILES; tile += NW) {
-      double* base = B + off;
+    double* base0 = sU + (k & 1) * FBUF + warp * 8;
+#pragma unroll
+    for (int i = 0; i < (S::TILES + NW - 1) / NW; ++i) {
+      if (i * NW + NW > S::TILES && warp + i * NW >= S::TILES) break;
+      double* base = base0 + i * NW * 8;
       const double b0 = base[lb0];
       const double b1 = (fk < 2) ? base[lb1] : 0.0;
       double d0, d1;
       dmma_nv(d0, d1, a_lo, b0, 0.0, 0.0);
       dmma_nv(d0, d1, a_hi, b1, d0, d1);
       if (lane < 4 * NQ) *reinterpret_cast<double2*>(base + lbd) = make_double2(d0, d1);
-      nt += NW;
-      off += NW * 8;
-      if (nt >= S::NTILE) {
-        nt -= S::NTILE;
-        off += ABUF - S::NTILE * 8;
-      }
     }
   };
   // the node's divergence of slice k into its TMEM column (idle lanes read a real

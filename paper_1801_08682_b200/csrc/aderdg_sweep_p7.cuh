@@ -1,7 +1,7 @@
 // aderdg_sweep_p7.cuh — the fused 3D sweep at p = 7 (n = 8) with the whole Picard
 // state of the cell on chip and the derivatives as exact m8n8k4 DMMA tiles.
 //
-// One CTA of 512 threads per cell (thread = spatial node, C order), one CTA per SM.
+// One CTA of 512 threads per cell (thread = spatial node), one CTA per SM.
 //   * Picard state: the node's time line q[c][t] (40 doubles) and the divergence
 //     history dv[c][k] (40 doubles) never touch local memory: q and dv of components
 //     0..2 live in tensor memory (128 columns = 64 doubles per thread, tcgen05.ld/st
@@ -9,13 +9,16 @@
 //   * derivatives: per time slice three GEMMs Out_a[i][col] = sum_j diff[i][j] F_a[j][col],
 //     col = c*64 + (the two other node indices): 40 n-tiles of 8 columns per axis, K = 8
 //     = two m8n8k4 DMMAs per tile with no padding.  A = diff (constant fragments), B = the
-//     flux from shared memory [axis][j][STR]; a tile writes its 8 x 8 outputs back in
+//     flux from shared memory [j][axis][col]; a tile writes its 8 x 8 outputs back in
 //     place (its outputs depend only on its own columns), the node owner sums the axes.
-//   * bank layout: STR = 324 == 4 (mod 16) puts the four k rows of a B-fragment load on
+//   * bank layout: row stride 964 == 4 (mod 16) puts the four k rows of a B-fragment load on
 //     disjoint bank groups (2 wavefronts, the minimum for 256 bytes); the A rows are
 //     permuted (0,2,1,3,4,6,5,7) so that the two output rows a quarter-warp stores as
 //     16-byte pairs lie 2 rows = 64 bytes (mod 128) apart (4 wavefronts, the minimum);
-//     the owner stores / loads are 2 wavefronts each along all three axes.
+//     a half-warp owns a 2 x 2 x 4 node box, so its 8-byte owner stores / loads fall on 16
+//     distinct banks along all three axes (the pipe serves 8-byte accesses per half-warp).
+//   * time contraction k-outermost over groups of 3 + 2 components: FP64 instructions take
+//     no constant operand, so every integ[t][k] fetched feeds 3 (2) FMAs.
 //   * software-pipelined slices, one barrier per slice: the interval that runs the tiles
 //     of slice k (operand buffer k & 1) also stages the flux of slice k + 1 in the other
 //     buffer (its last tile readers passed the previous barrier; an owner reads back and
@@ -32,6 +35,7 @@
 // extrapolate, integrate_volume, solve_riemann, integrate_face, update,
 // calc_time_step), scheduler.py:370-449 (fused sweep).
 #pragma once
+#include <type_traits>
 #include "aderdg_sweep_p5.cuh"   // dmma_nv, TMEM helpers
 
 namespace adg {
@@ -41,11 +45,11 @@ struct ShapeP7 {
   static constexpr int NS = 512, NF = 64;
   static constexpr int THREADS = 512, NW = 16;
   static constexpr int REC = 2 * NF * M + 2;
-  // DMMA operand arrays [slice parity][axis][j][STR]
+  // DMMA operand arrays [slice parity][j][axis][NCOL] (+ 4 pad doubles per row): tile t of the
+  // slice (t = axis * 40 + n-tile) starts at column 8 t of every row
   static constexpr int NCOL = M * NF, NTILE = NCOL / 8;
-  static constexpr int STR = 324;
-  static constexpr int ABUF = NQ * STR;
-  static constexpr int FBUF = DIM * ABUF;
+  static constexpr int STR = DIM * NCOL + 4;
+  static constexpr int FBUF = NQ * STR;
   static constexpr int TILES = DIM * NTILE;
   static constexpr int R_PRED = 2 * FBUF;
   static constexpr int CS = 2;                               // dv components in shared memory (3, 4)
@@ -59,7 +63,7 @@ struct ShapeP7 {
   static constexpr int TOTAL = OFF_DV + R_DV;
   static constexpr size_t SMEM_BYTES = sizeof(double) * TOTAL;
   static_assert(R_PRED >= R_NODE && R_PRED >= R_FACE, "aliased tail / corrector buffers");
-  static_assert(NCOL % 8 == 0 && STR >= NCOL && STR % 16 == 4, "operand row layout");
+  static_assert(NCOL % 16 == 0 && STR % 16 == 4, "operand row layout");
   static_assert(SMEM_BYTES <= 232448, "shared memory per CTA");
 };
 
@@ -92,10 +96,33 @@ __device__ __forceinline__ void tmem_st8(uint32_t a, const double (&v)[8]) {
       : "memory");
 }
 
+// three doubles at 6 consecutive columns (one .x4 and one .x2 access), issue and wait apart
+__device__ __forceinline__ void tmem_ld3_issue(uint32_t a, uint32_t (&r)[6]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(a));
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(r[4]), "=r"(r[5]) : "r"(a + 4));
+}
+__device__ __forceinline__ void tmem_ld3_wait(uint32_t (&r)[6], double (&v)[3]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5])::"memory");
+#pragma unroll
+  for (int i = 0; i < 3; ++i) v[i] = __hiloint2double((int)r[2 * i + 1], (int)r[2 * i]);
+}
+__device__ __forceinline__ void tmem_st3(uint32_t a, double v0, double v1, double v2) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(a),
+               "r"((uint32_t)__double2loint(v0)), "r"((uint32_t)__double2hiint(v0)),
+               "r"((uint32_t)__double2loint(v1)), "r"((uint32_t)__double2hiint(v1))
+               : "memory");
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(a + 4),
+               "r"((uint32_t)__double2loint(v2)), "r"((uint32_t)__double2hiint(v2))
+               : "memory");
+}
+
 __global__ void __launch_bounds__(ShapeP7::THREADS, 1) sweep_kernel_p7(const SweepParams P) {
   using S = ShapeP7;
   constexpr int DIM = 3, M = 5, NQ = 8, NS = S::NS, NF = S::NF, REC = S::REC, NW = S::NW;
-  constexpr int THREADS = S::THREADS, STR = S::STR, ABUF = S::ABUF, FBUF = S::FBUF, CS = S::CS;
+  constexpr int THREADS = S::THREADS, STR = S::STR, NCOL = S::NCOL, FBUF = S::FBUF, CS = S::CS;
 
   extern __shared__ __align__(16) double smem[];
   double* sRed = smem + S::OFF_RED;
@@ -114,8 +141,15 @@ __global__ void __launch_bounds__(ShapeP7::THREADS, 1) sweep_kernel_p7(const Swe
   if (mode_corrects(mode) && st->reduce[1] != 0) return;   // a predict pass already failed
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int x = tid;
-  const int i0 = x >> 6, i1 = (x >> 3) & 7, i2 = x & 7;
+  // Thread -> node map: a half-warp owns a 2 x 2 x 4 node box (lane bits 0-1: i2 & 3, bit 2:
+  // i0 & 1, bit 3: i1 & 1), lane bit 4 selects i2 >= 4, the warp index holds i0 / 2 and
+  // i1 / 2.  The shared-memory pipe serves an 8-byte access per half-warp: with the operand
+  // rows at bank offsets 4 i_a (STR == 4 mod 16) the 16 owner addresses of a half-warp fall
+  // on 16 distinct banks along all three axes (axis 2 with the column map below).
+  const int i0 = 2 * (warp >> 2) + ((lane >> 2) & 1);
+  const int i1 = 2 * (warp & 3) + ((lane >> 3) & 1);
+  const int i2 = (lane & 3) | ((lane >> 4) << 2);
+  const int x = (i0 * NQ + i1) * NQ + i2;
   const long long cell = sweep_cell(P);
   const long long gcell = cell + P.cell_offset;
   const int plane = (int)(cell / P.plane_cells);
@@ -234,7 +268,7 @@ __global__ void __launch_bounds__(ShapeP7::THREADS, 1) sweep_kernel_p7(const Swe
   const double tol = 1e-10 * (1.0 + block_max<NW>(am, sRed));
   tmem_fence_after();
   // warp w: TMEM lanes 32 (w % 4).., columns 128 (w / 4)..: q[c][t] at column 2 (8c + t),
-  // dv[c][k] (c < 3) at column 80 + 2 (8c + k)
+  // dv[k][c] (c < 3) at column 80 + 2 (3k + c)
   const uint32_t tq = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 128);
   const uint32_t td = tq + 80;
   double* sDt = sDv + tid;
@@ -249,8 +283,10 @@ __global__ void __launch_bounds__(ShapeP7::THREADS, 1) sweep_kernel_p7(const Swe
   // lane offsets inside a tile: B rows k / k + 4 at column n = fr; D row pi(fr), columns 2k, 2k + 1
   const int lb0 = fk * STR + fr, lb1 = (fk + 4) * STR + fr, lbd = prow * STR + 2 * fk;
   // owner offsets into one slice buffer: axis a, row i_a, column (other two indices) (+ c * 64)
-  const int ow[3] = {0 * ABUF + i0 * STR + i1 * NQ + i2, 1 * ABUF + i1 * STR + i0 * NQ + i2,
-                     2 * ABUF + i2 * STR + i0 * NQ + i1};
+  // (axis 2: column (i0 & 1) + 2 (i1 & 1) + 4 (i0 / 2) + 16 (i1 / 2) — the GEMM columns are
+  //  independent, any bijection of (i0, i1) onto 0..63 will do)
+  const int ow[3] = {0 * NCOL + i0 * STR + i1 * NQ + i2, 1 * NCOL + i1 * STR + i0 * NQ + i2,
+                     2 * NCOL + i2 * STR + (i0 & 1) + 2 * (i1 & 1) + 4 * (i0 >> 1) + 16 * (i1 >> 1)};
 
 #pragma unroll
   for (int c = 0; c < M; ++c) {
@@ -270,13 +306,14 @@ __global__ void __launch_bounds__(ShapeP7::THREADS, 1) sweep_kernel_p7(const Swe
 #pragma unroll
       for (int c = 0; c < M; ++c) B[ow[a] + c * NF] = F[a][c];
   };
-  // Out_a = diff . F_a, in place: warp w takes tiles w, w + 16, ... (tile = axis * 40 + n-tile)
+  // Out_a = diff . F_a, in place: warp w takes tiles w, w + 16, ... of the 120 (constant
+  // offsets from one base address)
   auto run_tiles = [&](int k) {
-    double* B = sU + (k & 1) * FBUF;
-#pragma unroll 2
-    for (int tile = warp; tile < S::TILES; tile += NW) {
-      const int a = (tile >= 2 * S::NTILE) ? 2 : (tile >= S::NTILE) ? 1 : 0;
-      double* base = B + a * ABUF + (tile - a * S::NTILE) * 8;
+    double* base0 = sU + (k & 1) * FBUF + warp * 8;
+#pragma unroll
+    for (int i = 0; i < (S::TILES + NW - 1) / NW; ++i) {
+      if (i * NW + NW > S::TILES && warp + i * NW >= S::TILES) break;
+      double* base = base0 + i * NW * 8;
       const double b0 = base[lb0];
       const double b1 = base[lb1];
       double d0, d1;
@@ -289,19 +326,59 @@ __global__ void __launch_bounds__(ShapeP7::THREADS, 1) sweep_kernel_p7(const Swe
   // the first iteration's slice stands for every k
   auto read_back = [&](int k, bool every_k) {
     const double* B = sU + (k & 1) * FBUF;
+    double dvc[M];
 #pragma unroll
-    for (int c = 0; c < M; ++c) {
-      const double dvc = (B[ow[0] + c * NF] + B[ow[1] + c * NF]) + B[ow[2] + c * NF];
-      if (every_k) {
+    for (int c = 0; c < M; ++c) dvc[c] = (B[ow[0] + c * NF] + B[ow[1] + c * NF]) + B[ow[2] + c * NF];
+    if (every_k) {
 #pragma unroll
-        for (int kk = 0; kk < NQ; ++kk) {
-          if (c < M - CS) tmem_st_d(td + 16 * c + 2 * kk, dvc);
-          else sDt[((c - (M - CS)) * NQ + kk) * THREADS] = dvc;
-        }
-      } else {
-        if (c < M - CS) tmem_st_d(td + 16 * c + 2 * k, dvc);
-        else sDt[((c - (M - CS)) * NQ + k) * THREADS] = dvc;
+      for (int kk = 0; kk < NQ; ++kk) {
+        tmem_st3(td + 6 * kk, dvc[0], dvc[1], dvc[2]);
+#pragma unroll
+        for (int c = M - CS; c < M; ++c) sDt[((c - (M - CS)) * NQ + kk) * THREADS] = dvc[c];
       }
+    } else {
+      tmem_st3(td + 6 * k, dvc[0], dvc[1], dvc[2]);
+#pragma unroll
+      for (int c = M - CS; c < M; ++c) sDt[((c - (M - CS)) * NQ + k) * THREADS] = dvc[c];
+    }
+  };
+  // Time contraction + Picard update (kernels.py:86-97) of NC components at a time, k
+  // outermost: every integ[t][k] is fetched from the constant bank once per group (FP64
+  // instructions take no constant operand), the accumulators become the new time line in
+  // place; convergence from the bit patterns of |q_new - q|.
+  BitMax bm;
+  auto contract = [&](auto c0_, auto nc_) {
+    constexpr int C0 = decltype(c0_)::value, NC = decltype(nc_)::value;
+    double acc[NC][NQ];
+    uint32_t rr[6];
+    if (C0 == 0) tmem_ld3_issue(td, rr);
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) {
+      double d[3];
+      if (C0 == 0) {
+        tmem_ld3_wait(rr, d);
+        if (k + 1 < NQ) tmem_ld3_issue(td + 6 * (k + 1), rr);
+      } else {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) d[c] = sDt[((C0 + c - (M - CS)) * NQ + k) * THREADS];
+      }
+#pragma unroll
+      for (int t = 0; t < NQ; ++t) {
+        const double g = P.ops.integ[t][k];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[c][t] = (k == 0) ? g * d[c] : fma(g, d[c], acc[c][t]);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      double qo[NQ];
+      tmem_ld8(tq + 16 * (C0 + c), qo);
+#pragma unroll
+      for (int t = 0; t < NQ; ++t) {
+        acc[c][t] = Qx[C0 + c] - scale * acc[c][t];
+        bm.add(fabs(acc[c][t] - qo[t]));
+      }
+      tmem_st8(tq + 16 * (C0 + c), acc[c]);
     }
   };
 
@@ -316,7 +393,7 @@ __global__ void __launch_bounds__(ShapeP7::THREADS, 1) sweep_kernel_p7(const Swe
       __syncthreads();
       read_back(0, true);
     } else {
-#pragma unroll 1
+#pragma unroll
       for (int k = 0; k < NQ; ++k) {
         if (k + 1 < NQ) {
           double qk[M];
@@ -329,31 +406,9 @@ __global__ void __launch_bounds__(ShapeP7::THREADS, 1) sweep_kernel_p7(const Swe
       }
     }
     tmem_wait_st();
-    // time contraction of the divergence history + Picard update (kernels.py:86-97), one
-    // component at a time; convergence from the bit patterns of |q_new - q|
-    BitMax bm;
-#pragma unroll 1
-    for (int c = 0; c < M; ++c) {
-      double dk[NQ], qo[NQ];
-      if (c < M - CS) {
-        tmem_ld8(td + 16 * c, dk);
-      } else {
-#pragma unroll
-        for (int k = 0; k < NQ; ++k) dk[k] = sDt[((c - (M - CS)) * NQ + k) * THREADS];
-      }
-      tmem_ld8(tq + 16 * c, qo);
-      const double qc = (c == 0) ? Qx[0] : (c == 1) ? Qx[1] : (c == 2) ? Qx[2] : (c == 3) ? Qx[3] : Qx[4];
-      double qn[NQ];
-#pragma unroll
-      for (int t = 0; t < NQ; ++t) {
-        double acc = P.ops.integ[t][0] * dk[0];
-#pragma unroll
-        for (int k = 1; k < NQ; ++k) acc = fma(P.ops.integ[t][k], dk[k], acc);
-        qn[t] = qc - scale * acc;
-        bm.add(fabs(qn[t] - qo[t]));
-      }
-      tmem_st8(tq + 16 * c, qn);
-    }
+    bm = BitMax();
+    contract(std::integral_constant<int, 0>(), std::integral_constant<int, 3>());
+    contract(std::integral_constant<int, 3>(), std::integral_constant<int, 2>());
     tmem_wait_st();
     iters = it + 1;
     if (it + 1 < cap) {                          // slice 0 of the next iteration
