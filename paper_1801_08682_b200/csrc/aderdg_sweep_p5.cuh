@@ -124,15 +124,19 @@ __device__ __forceinline__ void tmem_ldn_wait(uint32_t (&r)[6], double (&v)[3]) 
 }
 
 // Thread -> node map of the p = 5 kernel.  Eight consecutive lanes own a 2x2x2 node
-// block (lane bits 2,1,0 = the i0, i1, i2 offsets); a warp owns four of the 27 blocks
-// (the last warp three), grouped so that with the operand row offsets below
+// block (lane bits 2,1,0 = the i0, i1, i2 offsets); a half-warp owns two of the 27 blocks.
+// The shared-memory pipe serves 16-byte accesses per quarter-warp and 8-byte accesses per
+// half-warp (r02 ncu: the wavefront counts of the p = 9 line engine match that model
+// exactly), so with the operand row offsets below
 //   * a 16-byte owner access of a quarter-warp (one block) touches eight distinct
 //     16-byte bank groups along all three axes, and
-//   * an 8-byte owner access of a warp touches every 8-byte bank at most twice
-// (the minimum for 32 distinct doubles).  The grouping comes from an exhaustive search
-// over the partitions of the 3x3x3 block grid (block code = 9 B0 + 3 B1 + B2).
+//   * an 8-byte owner access of a half-warp touches 16 distinct banks along all three
+//     axes when its two blocks' column bases differ by 4 (mod 8): a maximum matching of the
+//     3x3x3 block grid under that condition pairs 22 of the 27 blocks (11 of 14 half-warps).
+// Block code = 9 B0 + 3 B1 + B2.
 __device__ __forceinline__ void block_map_p5b(int tid, int& i0, int& i1, int& i2, bool& act) {
-  constexpr unsigned char kBlock[28] = {2, 4, 5, 19, 6, 7, 8, 10, 9, 11, 15, 17, 12, 13, 16, 20, 14, 18, 21, 24, 22, 23, 25, 26, 0, 1, 3, 0};
+  constexpr unsigned char kBlock[28] = {0, 8, 1, 10, 2, 6, 3, 12, 4, 13, 5, 14, 7, 16, 9, 17, 11, 15, 18, 26, 20, 24,
+                                          19, 22, 21, 23, 25, 0};
   const int blk = tid >> 3;
   act = blk < 27;
   const int code = kBlock[blk];

@@ -47,8 +47,12 @@ struct ShapeP9 {
   static constexpr int THREADS = 512, NW = 16;
   static constexpr int NB = NS - THREADS;                     // threads with a node B
   static constexpr int REC = 2 * NF * M + 2;
-  // padded natural node layout of the flux slab (strides of ShapeHO<10>)
-  static constexpr int P0 = 111, P1 = 10, SC = 1124;
+  // padded natural node layout of the flux slab.  The shared-memory pipe serves an 8-byte
+  // access per half-warp (one wavefront per 16 lanes on 16 distinct banks; r02 ncu: the old
+  // strides 111 / 1124 cost 1.58x the ideal line wavefronts, exactly the half-warp model's
+  // 152 : 96).  P0 = 113, SC = 1133 with the line -> thread map below (component fastest)
+  // come from a search over strides and digit orders: 104 : 96.
+  static constexpr int P0 = 113, P1 = 10, SC = 1133;
   static constexpr int R_RED = 4 * NW + 2 * DIM + 4;          // block_max | s_max | vote flags
   static constexpr int R_SLAB = M * SC;                       // one axis' flux / derivative (>= M*NS: tail staging)
   static constexpr int CB = 4;                                // node-B components in shared memory
@@ -307,10 +311,10 @@ __global__ void __launch_bounds__(ShapeP9::THREADS, 1) sweep_kernel_p9(const Swe
   double* ln2;
   {
     const int l = has_line ? tid : 0;
-    const int c = l / NF, y = l % NF, ib = y / NQ, ic = y % NQ;
-    ln0 = sSlab + c * SC + ib * P1 + ic;          // stride P0
-    ln1 = sSlab + c * SC + ib * P0 + ic;          // stride P1
-    ln2 = sSlab + c * SC + ib * P0 + ic * P1;     // stride 1
+    const int c = l % M, r0 = (l / M) % NQ, r1 = l / (M * NQ);
+    ln0 = sSlab + c * SC + r1 * P1 + r0;          // line (i1, i2) = (r1, r0), stride P0
+    ln1 = sSlab + c * SC + r0 * P0 + r1;          // line (i0, i2) = (r0, r1), stride P1
+    ln2 = sSlab + c * SC + r0 * P0 + r1 * P1;     // line (i0, i1) = (r0, r1), stride 1
   }
 
   // the convergence test's copy of the previous iterate and the initial state, indexed

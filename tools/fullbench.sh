@@ -1,13 +1,12 @@
-# full measurement pass: default bench line, reference arm, every BASELINE config on 1 GPU
+# full measurement pass (run under gpurun, one GPU): the default bench line, the reference arm,
+# every BASELINE config on one GPU -> gpurun_out/full/
 mkdir -p gpurun_out/full
 timeout 900 python bench.py > gpurun_out/full/bench_default.json 2> gpurun_out/full/bench_default.err; echo "default rc=$?"
 timeout 600 python bench.py --impl reference > gpurun_out/full/bench_reference.json 2> gpurun_out/full/bench_reference.err; echo "reference rc=$?"
-timeout 600 python bench.py --config cfg1 --no-cpu-baseline > gpurun_out/full/bench_cfg1.json 2>&1; echo "cfg1 rc=$?"
-timeout 600 python bench.py --config cfg3_p5 --steps 7 --no-cpu-baseline > gpurun_out/full/bench_cfg3_p5.json 2>&1; echo "p5 rc=$?"
-timeout 600 python bench.py --config cfg3_p7 --steps 3 --no-cpu-baseline > gpurun_out/full/bench_cfg3_p7.json 2>&1; echo "p7 rc=$?"
-timeout 600 python bench.py --config cfg3_p9 --steps 1 --no-cpu-baseline > gpurun_out/full/bench_cfg3_p9.json 2>&1; echo "p9 rc=$?"
-timeout 900 python bench.py --config cfg4 --steps 7 --no-cpu-baseline --no-e2e > gpurun_out/full/bench_cfg4.json 2>&1; echo "cfg4 rc=$?"
-timeout 1200 python bench.py --config cfg5_1gpu --steps 2 --no-cpu-baseline --no-e2e > gpurun_out/full/bench_cfg5_1gpu.json 2>&1; echo "cfg5 rc=$?"
+for c in cfg1 cfg2 cfg3_p5 cfg3_p7 cfg3_p9; do
+  timeout 600 python bench.py --config $c --no-cpu-baseline > gpurun_out/full/bench_$c.json 2> gpurun_out/full/bench_$c.err; echo "$c rc=$?"
+done
+timeout 1200 python bench.py --config cfg5 --no-cpu-baseline --no-e2e > gpurun_out/full/bench_cfg5_1gpu.json 2> gpurun_out/full/bench_cfg5_1gpu.err; echo "cfg5 rc=$?"
 for f in gpurun_out/full/*.json; do python -c "
 import json,sys
 try:
