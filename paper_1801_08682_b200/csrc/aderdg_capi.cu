@@ -21,7 +21,7 @@
 
 #include "../../include/aderdg_b200.h"
 #include "aderdg_kernels.cuh"
-#include "aderdg_sweep_v2.cuh"
+#include "aderdg_sweep_p3.cuh"
 #include "aderdg_sweep_ho.cuh"
 #include "aderdg_sweep_p5.cuh"
 #include "aderdg_sweep_p7.cuh"
@@ -59,14 +59,6 @@ void launch_sweep(const SweepParams& P, unsigned grid, cudaStream_t s) {
   static std::atomic<unsigned long long> optin{0};
   ensure_smem_optin(sweep_kernel<PDE, DIM, NQ>, S::SMEM_BYTES, optin);
   sweep_kernel<PDE, DIM, NQ><<<grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
-}
-
-template <int NQ, int TS, bool DMMA, bool ROLLED = (NQ == 4), int MB = 0>
-void launch_sweep_v2(const SweepParams& P, unsigned grid, cudaStream_t s) {
-  using S = ShapeV2<NQ, TS, DMMA, ROLLED, MB>;
-  static std::atomic<unsigned long long> optin{0};
-  ensure_smem_optin(sweep_kernel_v2<NQ, TS, DMMA, ROLLED, MB>, S::SMEM_BYTES, optin);
-  sweep_kernel_v2<NQ, TS, DMMA, ROLLED, MB><<<grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
 }
 
 typedef int (*occupancy_fn)();
@@ -187,19 +179,19 @@ Dispatch make_dispatch_p9() {
   return Dispatch{&launch_sweep_p9, ShapeP9::REC, &occ_p9};
 }
 
-template <int NQ, int TS, bool DMMA, bool ROLLED, int MB>
-int occ_v2() {
-  using S = ShapeV2<NQ, TS, DMMA, ROLLED, MB>;
-  return occupancy_of(sweep_kernel_v2<NQ, TS, DMMA, ROLLED, MB>, S::THREADS, S::SMEM_BYTES);
+// 3D p = 3: DMMA axes 1-2 from registers, pipelined slices (aderdg_sweep_p3.cuh)
+void launch_sweep_p3(const SweepParams& P, unsigned grid, cudaStream_t s) {
+  static std::atomic<unsigned long long> optin{0};
+  ensure_smem_optin(sweep_kernel_p3, ShapeP3::SMEM_BYTES, optin);
+  sweep_kernel_p3<<<grid, ShapeP3::THREADS, ShapeP3::SMEM_BYTES, s>>>(P);
 }
 
-template <int NQ, int TS, bool DMMA, bool ROLLED = (NQ == 4), int MB = 0>
-Dispatch make_dispatch_v2() {
-  static_assert(ShapeV2<NQ, TS, DMMA, ROLLED, MB>::REC == Shape<3, NQ>::REC, "record layout must match");
-  return Dispatch{&launch_sweep_v2<NQ, TS, DMMA, ROLLED, MB>, ShapeV2<NQ, TS, DMMA, ROLLED, MB>::REC,
-                  &occ_v2<NQ, TS, DMMA, ROLLED, MB>};
-}
+int occ_p3() { return occupancy_of(sweep_kernel_p3, ShapeP3::THREADS, ShapeP3::SMEM_BYTES); }
 
+Dispatch make_dispatch_p3() {
+  static_assert(ShapeP3::REC == Shape<3, 4>::REC, "record layout must match");
+  return Dispatch{&launch_sweep_p3, ShapeP3::REC, &occ_p3};
+}
 
 // subcell limiter kernels (aderdg_limiter.cuh), per PDE plug-in and dimension
 struct LimDispatch {
@@ -267,7 +259,7 @@ bool dispatch_generic(int d, int p, Dispatch* out) {
 }
 
 // The product kernel of every (system, d, p): one instantiation each, no run-time
-// variant selection.  3D Euler: p = 3 sweep_kernel_v2 (DMMA axes 1-2, pipelined
+// variant selection.  3D Euler: p = 3 sweep_kernel_p3 (DMMA axes 1-2, pipelined
 // slices), p = 5 sweep_kernel_p5, p = 7 sweep_kernel_p7, p = 9 sweep_kernel_p9,
 // p = 6, 8 sweep_kernel_ho; the rest
 // (2D, 3D p <= 2, p = 4) run the generic kernel.
@@ -276,12 +268,8 @@ bool dispatch_for(int d, int p, int system, Dispatch* out) {
   if (system == 1) return d == 2 ? dispatch_adv<2>(n, out) : d == 3 ? dispatch_adv<3>(n, out) : false;
   if (d == 3) {
     switch (n) {
-      case 4: *out = make_dispatch_v2<4, 1, true, false, 14>(); return true;
-#ifdef ADG_AB_P5_V2
-      case 6: *out = make_dispatch_v2<6, 1, false, false, 31>(); return true;   // A/B builds only
-#else
+      case 4: *out = make_dispatch_p3(); return true;
       case 6: *out = make_dispatch_p5(); return true;
-#endif
       case 7: *out = make_dispatch_ho<7>(); return true;
 #ifdef ADG_AB_P7_HO
       case 8: *out = make_dispatch_ho<8>(); return true;                         // A/B builds only

@@ -29,7 +29,7 @@
 // scheduler.py:370-449 (same tasks as sweep_kernel).
 #pragma once
 #include "aderdg_kernels.cuh"
-#include "aderdg_sweep_v2.cuh"
+#include "aderdg_sweep_p3.cuh"   // TMA / mbarrier / DMMA helpers
 
 namespace adg {
 

@@ -29,7 +29,7 @@
 //
 // The rest (TMA bulk staging of Q, D and the 4d face records, Riemann, corrector,
 // calc_time_step, final flux, volume integral, face traces, s_max) follows
-// sweep_kernel_v2.
+// sweep_kernel_p3.
 //
 // Reference (src/ = /root/reference/pkg/src/aderdg/): kernels.py:68-229 (predict,
 // extrapolate, integrate_volume, solve_riemann, integrate_face, update,

@@ -51,7 +51,7 @@ def _run(d, L, p, steps, mode="fused", debug=False, system=None, scen="bump", li
 
 
 CASES = [
-    dict(d=3, L=2, p=3, steps=5, inject_rerun=True),           # sweep_kernel_v2 p=3, graph + rerun nodes
+    dict(d=3, L=2, p=3, steps=5, inject_rerun=True),           # sweep_kernel_p3, graph + rerun nodes
     dict(d=3, L=1, p=5, steps=3),                              # p=5 kernel
     dict(d=3, L=1, p=7, steps=2),                              # p=7 kernel (TMEM + smem state, DMMA tiles)
     dict(d=3, L=1, p=6, steps=2),                              # sweep_kernel_ho, TMEM time line

@@ -4,9 +4,8 @@
     python tools/sanitize_case.py <case>
 
 Cases cover every default kernel instantiation and launch structure:
-p3 (sweep_kernel_v2 MB14, graph steps + conditional rerun, inject_rerun), p5
-(sweep_kernel_v2 MB31), p7 (sweep_kernel_ho TMEM time line), p9 (sweep_kernel_ho
-line engine), gen2d (generic 2D kernel), p4 (generic 3D kernel), sf (straightforward
+p3 (sweep_kernel_p3, graph steps + conditional rerun, inject_rerun), p5
+(sweep_kernel_p5), p7 (sweep_kernel_p7), p9 (sweep_kernel_p9), gen2d (generic 2D kernel), p4 (generic 3D kernel), sf (straightforward
 passes), adv (advection plug-in), lim (subcell limiter: detect / apply / lambda),
 host (adg_step_host chunked H2D / sweep / D2H pipeline), stream (adg_run without graphs).
 """
