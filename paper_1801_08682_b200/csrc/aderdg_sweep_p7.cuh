@@ -54,7 +54,10 @@ struct ShapeP7 {
   static constexpr int R_PRED = 2 * FBUF;
   static constexpr int CS = 2;                               // dv components in shared memory (3, 4)
   static constexpr int R_DV = CS * NQ * THREADS;
-  static constexpr int R_NODE = M * NS;                      // node staging of the tail
+  // node staging of the tail: node (i0, i1, i2) at 72 i0 + 9 i1 + i2 (the face-trace gathers
+  // of a half-warp then fall on distinct banks along all three axes)
+  static constexpr int T1 = NQ + 1, T0 = NQ * T1, NSP = NQ * T0;
+  static constexpr int R_NODE = M * NSP;
   static constexpr int R_FACE = 2 * DIM * NF * M;            // corrector: signed F* per face
   static constexpr int R_RED = 4 * NW + 2 * DIM + 4;         // block_max | s_max | vote flags
   static constexpr int OFF_RED = 0;
@@ -130,7 +133,7 @@ __global__ void __launch_bounds__(ShapeP7::THREADS, 1) sweep_kernel_p7(const Swe
   unsigned* sFlags = reinterpret_cast<unsigned*>(sRed + 2 * NW + 2 * DIM);   // 2 * NW words
   double* sU = smem + S::OFF_U;         // operand buffers of the Picard loop
   double* sFace = sU;                   // corrector: signed F* per face
-  double* sN = sU;                      // [M][NS] node staging of the tail
+  double* sN = sU;                      // [M][NSP] node staging of the tail (padded)
   double* sDv = smem + S::OFF_DV;       // [c - 3][k][tid] divergence history of components 3, 4
   ADG_DEBUG_POISON();
 
@@ -150,6 +153,7 @@ __global__ void __launch_bounds__(ShapeP7::THREADS, 1) sweep_kernel_p7(const Swe
   const int i1 = 2 * (warp & 3) + ((lane >> 3) & 1);
   const int i2 = (lane & 3) | ((lane >> 4) << 2);
   const int x = (i0 * NQ + i1) * NQ + i2;
+  const int xp = i0 * S::T0 + i1 * S::T1 + i2;       // padded node index of the tail staging
   const long long cell = sweep_cell(P);
   const long long gcell = cell + P.cell_offset;
   const int plane = (int)(cell / P.plane_cells);
@@ -479,16 +483,16 @@ __global__ void __launch_bounds__(ShapeP7::THREADS, 1) sweep_kernel_p7(const Swe
   for (int a = 0; a < DIM; ++a) {
     if (a > 0) __syncthreads();
 #pragma unroll
-    for (int c = 0; c < M; ++c) sN[c * NS + x] = fb[a][c];
+    for (int c = 0; c < M; ++c) sN[c * S::NSP + xp] = fb[a][c];
     __syncthreads();
-    const int sa = (a == 0) ? NQ * NQ : (a == 1) ? NQ : 1;
+    const int sa = (a == 0) ? S::T0 : (a == 1) ? S::T1 : 1;
     const int ia = (a == 0) ? i0 : (a == 1) ? i1 : i2;
-    const int base = x - ia * sa;
+    const int base = xp - ia * sa;
 #pragma unroll
     for (int c = 0; c < M; ++c) {
       double s = Dv[c];
 #pragma unroll
-      for (int j = 0; j < NQ; ++j) s = fma(P.ops.kvol[ia][j], sN[c * NS + base + j * sa], s);
+      for (int j = 0; j < NQ; ++j) s = fma(P.ops.kvol[ia][j], sN[c * S::NSP + base + j * sa], s);
       Dv[c] = s;
     }
     // f-bar face traces of axis a, both sides (side fastest: the two lanes of a pair
@@ -499,10 +503,10 @@ __global__ void __launch_bounds__(ShapeP7::THREADS, 1) sweep_kernel_p7(const Swe
       const int c = (e >> 1) / NF;
       const double* vec = side ? P.ops.right : P.ops.left;
       const int ya = y / NQ, yb = y % NQ;
-      const int xb = (a == 0) ? ya * NQ + yb : (a == 1) ? ya * NQ * NQ + yb : (ya * NQ + yb) * NQ;
+      const int xb = (a == 0) ? ya * S::T1 + yb : (a == 1) ? ya * S::T0 + yb : ya * S::T0 + yb * S::T1;
       double v = 0.0;
 #pragma unroll
-      for (int i = 0; i < NQ; ++i) v = fma(vec[i], sN[c * NS + xb + i * sa], v);
+      for (int i = 0; i < NQ; ++i) v = fma(vec[i], sN[c * S::NSP + xb + i * sa], v);
       P.tr_out[((long long)(2 * a + side) * P.slots + own_slot) * REC + NF * M + y * M + c] = v;
     }
   }
@@ -512,7 +516,7 @@ __global__ void __launch_bounds__(ShapeP7::THREADS, 1) sweep_kernel_p7(const Swe
   // ---------------- q-bar face traces ----------------
   __syncthreads();
 #pragma unroll
-  for (int c = 0; c < M; ++c) sN[c * NS + x] = qb[c];
+  for (int c = 0; c < M; ++c) sN[c * S::NSP + xp] = qb[c];
   if (tid < 2 * DIM) sSmax[tid] = 0ull;
   __syncthreads();
   for (int e = tid; e < 2 * DIM * NF * M; e += THREADS) {
@@ -523,11 +527,11 @@ __global__ void __launch_bounds__(ShapeP7::THREADS, 1) sweep_kernel_p7(const Swe
     const int a = f >> 1;
     const double* vec = (f & 1) ? P.ops.right : P.ops.left;
     const int ya = y / NQ, yb = y % NQ;
-    const int sa = (a == 0) ? NQ * NQ : (a == 1) ? NQ : 1;
-    const int xb = (a == 0) ? ya * NQ + yb : (a == 1) ? ya * NQ * NQ + yb : (ya * NQ + yb) * NQ;
+    const int sa = (a == 0) ? S::T0 : (a == 1) ? S::T1 : 1;
+    const int xb = (a == 0) ? ya * S::T1 + yb : (a == 1) ? ya * S::T0 + yb : ya * S::T0 + yb * S::T1;
     double v = 0.0;
 #pragma unroll
-    for (int i = 0; i < NQ; ++i) v = fma(vec[i], sN[c * NS + xb + i * sa], v);
+    for (int i = 0; i < NQ; ++i) v = fma(vec[i], sN[c * S::NSP + xb + i * sa], v);
     P.tr_out[((long long)f * P.slots + own_slot) * REC + y * M + c] = v;
   }
   // ---------------- s_max over the space-time traces, one time level at a time ----------------
@@ -538,7 +542,7 @@ __global__ void __launch_bounds__(ShapeP7::THREADS, 1) sweep_kernel_p7(const Swe
     tmem_ld_doubles<M>(tq + 2 * t, 16, qt);
     __syncthreads();
 #pragma unroll
-    for (int c = 0; c < M; ++c) sN[c * NS + x] = qt[c];
+    for (int c = 0; c < M; ++c) sN[c * S::NSP + xp] = qt[c];
     __syncthreads();
     if (tid < 2 * DIM * NF) {
       const int e = tid;
@@ -547,14 +551,14 @@ __global__ void __launch_bounds__(ShapeP7::THREADS, 1) sweep_kernel_p7(const Swe
       const int a = f >> 1;
       const double* vec = (f & 1) ? P.ops.right : P.ops.left;
       const int ya = y / NQ, yb = y % NQ;
-      const int sa = (a == 0) ? NQ * NQ : (a == 1) ? NQ : 1;
-      const int xb = (a == 0) ? ya * NQ + yb : (a == 1) ? ya * NQ * NQ + yb : (ya * NQ + yb) * NQ;
+      const int sa = (a == 0) ? S::T0 : (a == 1) ? S::T1 : 1;
+      const int xb = (a == 0) ? ya * S::T1 + yb : (a == 1) ? ya * S::T0 + yb : ya * S::T0 + yb * S::T1;
       double qs[M];
 #pragma unroll
       for (int c = 0; c < M; ++c) {
         double v = 0.0;
 #pragma unroll
-        for (int i = 0; i < NQ; ++i) v = fma(vec[i], sN[c * NS + xb + i * sa], v);
+        for (int i = 0; i < NQ; ++i) v = fma(vec[i], sN[c * S::NSP + xb + i * sa], v);
         qs[c] = v;
       }
       bool adm;
