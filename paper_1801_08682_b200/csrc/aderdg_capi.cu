@@ -1592,31 +1592,40 @@ adg_status adg_step_host(adg_handle* h, const double* Q_in, double* Q_out, adg_s
   CUDA_TRY(h, cudaEventRecord(ev_start, h->stream));
   CUDA_TRY(h, cudaStreamWaitEvent(h->copy_in, ev_start, 0));
   CUDA_TRY(h, cudaStreamWaitEvent(h->copy_out, ev_start, 0));
-  const bool whole = (h->sweep_index == 0) || h->hst.rerun_next;
-  if (whole) {
-    // priming and / or rerun read every cell's Q: upload all of it first
+  const bool priming = h->sweep_index == 0;
+  const bool rerun = !priming && h->hst.rerun_next;
+  auto chunk_off = [&](int i) { return (size_t)cell_of(i) * cell_doubles; };
+  auto chunk_len = [&](int i) { return (size_t)(cell_of(i + 1) - cell_of(i)) * cell_doubles; };
+  if (priming) {
+    // the priming sweep predicts every cell before any cell is corrected: upload all of Q first
     CUDA_TRY(h, cudaMemcpyAsync(h->Q, Q_in, sizeof(double) * cell_doubles * h->cells_local,
                                 cudaMemcpyHostToDevice, h->stream));
-    if (h->sweep_index == 0) {
-      if ((s = adg_phase_sweep(h)) != ADG_OK) return s;
-      if ((s = adg_phase_finish(h)) != ADG_OK) return s;
-    }
+    if ((s = adg_phase_sweep(h)) != ADG_OK) return s;
+    if ((s = adg_phase_finish(h)) != ADG_OK) return s;
     if ((s = adg_phase_rerun(h)) != ADG_OK) return s;
   } else {
     for (int i = 0; i < nch; ++i) {
-      const size_t off = (size_t)cell_of(i) * cell_doubles;
-      const size_t n = (size_t)(cell_of(i + 1) - cell_of(i)) * cell_doubles;
-      CUDA_TRY(h, cudaMemcpyAsync(h->Q + off, Q_in + off, sizeof(double) * n, cudaMemcpyHostToDevice,
-                                  h->copy_in));
+      CUDA_TRY(h, cudaMemcpyAsync(h->Q + chunk_off(i), Q_in + chunk_off(i), sizeof(double) * chunk_len(i),
+                                  cudaMemcpyHostToDevice, h->copy_in));
       CUDA_TRY(h, cudaEventRecord(ev_in[i], h->copy_in));
     }
+    if (rerun) {
+      // the rerun pass re-predicts a cell from its own Q only: chunk i runs as soon as its
+      // part of Q has landed, so the upload hides behind it; the corrector chunks below
+      // follow in stream order (they read the re-predicted records of every neighbour)
+      h->hst_fresh = false;
+      for (int i = 0; i < nch; ++i) {
+        CUDA_TRY(h, cudaStreamWaitEvent(h->stream, ev_in[i], 0));
+        if ((s = launch_range(h, MODE_RERUN, cell_of(i), cell_of(i + 1) - cell_of(i), h->stream)) != ADG_OK)
+          return s;
+      }
+    }
   }
-  if (whole) CUDA_TRY(h, cudaEventRecord(ev_start, h->stream));   // Q resident (+ priming / rerun)
   const int mode = MODE_NORMAL;
   for (int i = 0; i < nch; ++i) {
     const long long c0 = cell_of(i), c1 = cell_of(i + 1);
     cudaStream_t st = h->stream;
-    CUDA_TRY(h, cudaStreamWaitEvent(st, whole ? ev_start : ev_in[i], 0));
+    if (!priming && !rerun) CUDA_TRY(h, cudaStreamWaitEvent(st, ev_in[i], 0));
     if ((s = launch_range(h, mode, c0, c1 - c0, st)) != ADG_OK) return s;
     CUDA_TRY(h, cudaEventRecord(ev_sw[i], st));
     CUDA_TRY(h, cudaStreamWaitEvent(h->copy_out, ev_sw[i], 0));

@@ -7,7 +7,7 @@ import csv, os, re, subprocess, sys, tempfile
 from collections import defaultdict
 rep, kname = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
-lib = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1801_08682_b200", "libaderdg_b200.so")
+lib = os.environ.get("ADG_PROFILE_LIB") or os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1801_08682_b200", "libaderdg_b200.so")
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", lib], cwd=tmp, capture_output=True)
 cub = [f for f in os.listdir(tmp) if f.endswith(".cubin")][0]
