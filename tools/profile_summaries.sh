@@ -5,7 +5,7 @@
 # samples and by shared-memory wavefronts.
 cd "$(dirname "$0")/.."
 SRC=$1; OUT=$2
-[ -n "$3" ] && export ADG_PROFILE_LIB=$3
+[ -n "$3" ] && export ADG_PROFILE_LIB=$(realpath $3)
 mkdir -p $OUT
 declare -A K=( [cfg2]=_ZN3adg15sweep_kernel_p3ENS_11SweepParamsE [cfg3_p5]=_ZN3adg15sweep_kernel_p5ENS_11SweepParamsE
                [cfg4]=_ZN3adg15sweep_kernel_p5ENS_11SweepParamsE [cfg3_p7]=_ZN3adg15sweep_kernel_p7ENS_11SweepParamsE
