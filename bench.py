@@ -441,11 +441,16 @@ def main():
     achieved_tf = max_over_ranks(-achieved_tf) * -1 if world > 1 else achieved_tf   # slowest rank
     dfma, dmma, hbm = load_peaks()
     peak_tf = dmma or dfma or 37.1
-    traffic = None
+    # ncu DRAM bytes of one full sweep launch (profiles/r02/sweep_traffic.json) x the sweep
+    # passes per timed step (1 + the share of steps that rerun), like `achieved`
+    traffic = traffic_launch = None
     try:
         with open(NCU_TRAFFIC_FILE) as fh:
-            traffic = json.load(fh).get(args.config, {}).get("dram_bytes_per_step")
-    except (OSError, ValueError):
+            t = json.load(fh).get(args.config)
+        if t and world == 1:
+            traffic_launch = t["dram_bytes_per_step"] / t["full_sweep_launches_per_step"]
+            traffic = traffic_launch * preds / (local_cells * K)
+    except (OSError, ValueError, KeyError, ZeroDivisionError):
         pass
     bytes_alg = roofline.bytes_step(d, p, local_cells, preds // K)
     hbm_frac = (bytes_alg / (kern_ms_per_step * 1e-3) / 1e9) / hbm if hbm else None
@@ -536,8 +541,9 @@ def main():
                          "flops_per_step_per_gpu": flops_total / K,
                          "peak_source": "profiles/fp64_peaks_r01.jsonl (measured DMMA m8n8k4; "
                                         f"DFMA {dfma} TF/s) — MEASURED_PEAKS.json has no fp64 entry",
-                         "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum of the sweep "
-                                           "launches of one step, profiles/r02/sweep_traffic.json",
+                         "traffic_per_sweep_launch": traffic_launch,
+                         "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum of one full sweep "
+                                           "launch (profiles/r02/sweep_traffic.json) x sweep passes per timed step",
                          "hbm_alg_bytes_per_step": bytes_alg, "hbm_frac_of_measured": hbm_frac},
             "gpu_launches": launches,
             "clocks": clk,
