@@ -113,22 +113,18 @@ bool dispatch_adv(int n, Dispatch* out) {
   return false;
 }
 
-// High-order engine (3D, p = 6..9).  Derivative engine and time-line placement per
-// order, measured on cfg 3: DMMA tiles at n <= 9, the constant-bank
-// line engine at n = 10; the first node's old iterate in TMEM at n <= 8.
+// 3D p = 6 and p = 8 (aderdg_sweep_ho.cuh): DMMA tiles, time line in local memory (+ TMEM)
 template <int NQ>
 void launch_sweep_ho(const SweepParams& P, unsigned grid, cudaStream_t s) {
   using S = ShapeHO<NQ>;
-  constexpr int LN = (NQ == 10 ? 1 : 0), TM = (NQ <= 8 ? 1 : 0);
   static std::atomic<unsigned long long> optin{0};
-  ensure_smem_optin(sweep_kernel_ho<NQ, true, LN, TM>, S::SMEM_BYTES, optin);
-  sweep_kernel_ho<NQ, true, LN, TM><<<grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
+  ensure_smem_optin(sweep_kernel_ho<NQ>, S::SMEM_BYTES, optin);
+  sweep_kernel_ho<NQ><<<grid, S::THREADS, S::SMEM_BYTES, s>>>(P);
 }
 
 template <int NQ>
 int occ_ho() {
-  constexpr int LN = (NQ == 10 ? 1 : 0), TM = (NQ <= 8 ? 1 : 0);
-  return occupancy_of(sweep_kernel_ho<NQ, true, LN, TM>, ShapeHO<NQ>::THREADS, ShapeHO<NQ>::SMEM_BYTES);
+  return occupancy_of(sweep_kernel_ho<NQ>, ShapeHO<NQ>::THREADS, ShapeHO<NQ>::SMEM_BYTES);
 }
 
 template <int NQ>
@@ -271,17 +267,9 @@ bool dispatch_for(int d, int p, int system, Dispatch* out) {
       case 4: *out = make_dispatch_p3(); return true;
       case 6: *out = make_dispatch_p5(); return true;
       case 7: *out = make_dispatch_ho<7>(); return true;
-#ifdef ADG_AB_P7_HO
-      case 8: *out = make_dispatch_ho<8>(); return true;                         // A/B builds only
-#else
       case 8: *out = make_dispatch_p7(); return true;
-#endif
       case 9: *out = make_dispatch_ho<9>(); return true;
-#ifdef ADG_AB_P9_HO
-      case 10: *out = make_dispatch_ho<10>(); return true;                       // A/B builds only
-#else
       case 10: *out = make_dispatch_p9(); return true;
-#endif
     }
   }
   return dispatch_generic(d, p, out);

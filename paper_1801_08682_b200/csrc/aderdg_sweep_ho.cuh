@@ -1,29 +1,21 @@
-// aderdg_sweep_ho.cuh — high-order fused sweep kernel (3D, p = 6..9).
+// aderdg_sweep_ho.cuh — fused sweep kernel of the 3D orders without a dedicated kernel
+// (p = 6 and p = 8), and the tensor-memory helpers the dedicated kernels share.
 //
-// At p >= 6 one cell's space-time predictor (n^4 * 5 doubles: 96 KB at p=6,
-// 400 KB at p=9) no longer fits a thread-per-node register file, and the
-// unblocked shared-memory derivative gathers (n loads per output per axis)
-// would make the kernel shared-memory bound.  This kernel therefore:
-//   * runs 512 threads per cell, each owning NPT = ceil(n^3/512) nodes;
-//   * keeps the per-node time line (old iterate qo[t][c], divergence history
-//     dh[k][c]) in thread-private local memory (L1/L2 backed, coalesced);
-//   * computes the spatial derivative of every time slice as three GEMMs on
-//     the FP64 tensor cores: Out_a[i'][r] = sum_j diff[i'][j] F_a[j][r], with
-//     r = (the two other node indices, component).  A = diff (constant
-//     fragments in registers), B = the flux staged in shared memory with the
-//     contraction index fastest (row stride JS = 12 doubles: a B-fragment load
-//     of a warp touches every 8-byte bank exactly twice).  At p = 7 (n = 8) the
-//     m8n8k4 tiles fit exactly (no padding); at p = 9, M pads 10 -> 16 and
-//     K 10 -> 12.
-//   * derivative engines (template LN): DMMA tiles (default, n <= 9), or one
-//     line per thread with diff from the constant bank (n = 10: no M/K
-//     padding; measured 6.89 vs 6.54 TF/s at p = 9), or lane groups with
-//     diff rows in registers (A/B only: register pressure at n = 10);
-//   * the time contraction reads each node's divergence history once per
-//     component and forms every time level from registers;
-//   * everything else (Riemann, corrector, calc_time_step, final flux, volume
-//     integral, face traces, s_max) follows sweep_kernel, staged per axis /
-//     per time level through one shared node buffer.
+//   * 512 threads per cell, each owning NPT = ceil(n^3/512) nodes;
+//   * per-node time line (old iterate, divergence history) in thread-private local memory
+//     (L1/L2 backed, coalesced); at n <= 8 the first node's old iterate lives in tensor
+//     memory instead (tcgen05.alloc of all 512 columns, released before the CTA exits);
+//   * the spatial derivatives of a time slice as three GEMMs on the FP64 tensor cores,
+//     Out_a[i'][r] = sum_j diff[i'][j] F_a[j][r], r = (the two other node indices,
+//     component): A = diff (constant fragments in registers), B = the flux of all three
+//     axes staged at once in a padded natural layout, every tile written back in place (a
+//     tile's outputs depend only on its own columns): two barriers per slice;
+//   * the first Picard iteration (q_t = Q at every level) computes one slice;
+//   * the time contraction reads each node's divergence history once per component and
+//     forms every time level from registers;
+//   * everything else (Riemann, corrector, calc_time_step, final flux, volume integral,
+//     face traces, s_max) staged per axis / per time level through one shared node buffer.
+// The BASELINE orders p = 3, 5, 7, 9 have their own kernels (aderdg_sweep_p{3,5,7,9}.cuh).
 //
 // Reference (src/ = /root/reference/pkg/src/aderdg/): kernels.py:68-229,
 // scheduler.py:370-449 (same tasks as sweep_kernel).
@@ -33,7 +25,7 @@
 
 namespace adg {
 
-template <int NQ, bool FA = true>
+template <int NQ>
 struct ShapeHO {
   static constexpr int DIM = 3, M = 5;
   static constexpr int NS = NQ * NQ * NQ;
@@ -47,42 +39,28 @@ struct ShapeHO {
   static constexpr int NT = (RR + 7) / 8;                    // n-tiles
   static constexpr int RP = NT * 8;
   // padded natural node layout [c][SC]: strides searched against a wavefront model of
-  // this kernel's accesses (8-byte loads: one wavefront per 16 distinct doubles in
-  // distinct bank pairs).  n = 8: P0 100, P1 12, SC 800 make the node stores and the
-  // DMMA B loads conflict-free (C scatters 1.67x); n = 10: P0 111, P1 10, SC 1124 for
-  // the line engine (model: 4620 vs 5750 wavefronts per slice, 21 KB less shared memory)
+  // this kernel's accesses (n = 8: node stores and DMMA B loads conflict-free)
   static constexpr int P1 = (NQ == 10) ? 10 : (NQ == 6) ? 6 : (NQ == 8) ? 12 : 11;
   static constexpr int P0 = (NQ == 6) ? 36 : (NQ == 7) ? 77 : (NQ == 8) ? 100 : (NQ == 9) ? 107 : 111;
   static constexpr int SC = (NQ == 6) ? 217 : (NQ == 7) ? 541 : (NQ == 8) ? 800 : (NQ == 9) ? 965 : 1124;
   static constexpr int REC = 2 * NF * M + 2;
+  // TM: the first node's old iterate in tensor memory (measured: a gain at n <= 8 only)
+  static constexpr bool TM = (NQ <= 8);
   // shared memory (doubles)
   static constexpr int R_RED = 2 * NW + 2 * DIM + 4;
   static constexpr int R_FA = M * SC;                        // flux of one axis (padded natural layout)
-  static constexpr int R_DV = M * SC;                        // derivative accumulator (same layout)
-  static constexpr int R_NODE = M * NS;                      // per-node staging (q_t / qbar / fbar_a / D / Q)
+  static constexpr int R_NODE = M * NS;                      // per-node staging (q_t / qbar / fbar_a)
   static constexpr int R_FACE = 2 * DIM * NF * M;
-  // divergence history dh[k][c][x] of the Picard iteration: in shared memory when
-  // it fits next to the GEMM buffers (n <= 8), aliasing the corrector (sFace) and
-  // tail (sN) buffers, otherwise in thread-private local memory
-  static constexpr int R_DH = NQ * M * THREADS * NPT;
-  // FA (fused axes): the flux of all three axes is staged at once and every
-  // GEMM of the slice runs between one barrier pair, writing D_a F_a in place
-  // (a tile's outputs only depend on its own columns): 2 barriers per slice.
-  // Otherwise one axis at a time (6 barriers) with the history in smem (n <= 8).
-  static constexpr bool DH_SMEM = !FA && (NQ <= 8);
-  static constexpr int R_ALIAS = DH_SMEM ? R_DH : (R_NODE + R_FACE);
-  static constexpr int R_OFF = (3 * RP + 1) / 2;            // int column-offset table (3 axes)
+  static constexpr int R_OFF = (3 * RP + 1) / 2;             // int column-offset table (3 axes)
   static constexpr int OFF_RED = 0;
   static constexpr int OFF_TAB = (R_RED + 1) & ~1;
   static constexpr int OFF_FA = OFF_TAB + ((R_OFF + 1) & ~1);
-  static constexpr int OFF_DV = OFF_FA + R_FA;
-  static constexpr int OFF_NODE = FA ? OFF_FA : OFF_DV + R_DV;   // FA: tail buffers alias the slabs
+  static constexpr int OFF_NODE = OFF_FA;                    // tail / corrector buffers alias the slabs
   static constexpr int OFF_FACE = OFF_NODE + R_NODE;
-  static constexpr int OFF_DH = OFF_NODE;
-  static constexpr int TOTAL = FA ? OFF_FA + (3 * R_FA > R_NODE + R_FACE ? 3 * R_FA : R_NODE + R_FACE)
-                                  : OFF_NODE + (R_ALIAS > R_NODE + R_FACE ? R_ALIAS : R_NODE + R_FACE);
+  static constexpr int TOTAL = OFF_FA + (3 * R_FA > R_NODE + R_FACE ? 3 * R_FA : R_NODE + R_FACE);
   static constexpr size_t SMEM_BYTES = sizeof(double) * TOTAL;
 };
+
 
 
 // ---------------------------------------------------------------------------
@@ -127,45 +105,20 @@ __device__ __forceinline__ void tmem_ld_doubles(uint32_t base, uint32_t stride, 
   for (int i = 0; i < K; ++i) v[i] = tmem_wait_d(lo[i], hi[i]);
 }
 
-// One derivative line of axis A on the FP64 pipe: the NQ inputs of the line
-// into registers, out[i] = sum_j diff[i][j] in[j] with diff from the constant
-// bank (kernel parameters), NQ independent accumulators, written back in place.
-template <int NQ, int SA>
-__device__ __forceinline__ void deriv_line(double* ln, const SweepParams& P) {
-  double in[NQ];
-#pragma unroll
-  for (int j = 0; j < NQ; ++j) in[j] = ln[j * SA];
-  double out[NQ];
-#pragma unroll
-  for (int i = 0; i < NQ; ++i) {
-    double s = P.ops.diff[i][0] * in[0];
-#pragma unroll
-    for (int j = 1; j < NQ; ++j) s = fma(P.ops.diff[i][j], in[j], s);
-    out[i] = s;
-  }
-#pragma unroll
-  for (int i = 0; i < NQ; ++i) ln[i * SA] = out[i];
-}
-
-// LN (derivative engine): 0 = m8n8k4 DMMA tiles (padded to 16 x 12 at n = 10);
-// 1 = one line per thread, diff from the constant bank; 2 = a line per group of
-// ceil(n/2) lanes, each lane two outputs with its two diff rows in registers,
-// the line's inputs broadcast to the group (DFMA-bound, no padding waste).
-template <int NQ, bool FA = true, int LN = 0, int TM = 0>
+template <int NQ>
 __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
-  using S = ShapeHO<NQ, FA>;
+  using S = ShapeHO<NQ>;
   constexpr int DIM = 3, M = 5, NS = S::NS, NF = S::NF, NPT = S::NPT, REC = S::REC;
   constexpr int THREADS = S::THREADS, NW = S::NW, KC = S::KC, MT = S::MT, NT = S::NT;
   constexpr int RR = S::RR, SC = S::SC, P0 = S::P0, P1 = S::P1;
+  constexpr bool TM = S::TM;
 
   extern __shared__ __align__(16) double smem[];
   double* sRed = smem + S::OFF_RED;
   unsigned long long* sSmax = reinterpret_cast<unsigned long long*>(sRed + 2 * NW);
-  double* sFA = smem + S::OFF_FA;     // [M][SC] flux of the current axis
-  double* sDv = smem + S::OFF_DV;     // [M][SC] spatial divergence of the current slice
+  double* sFA = smem + S::OFF_FA;     // [3][M][SC] flux / derivative of the three axes
   double* sN = smem + S::OFF_NODE;    // [M][NS] node staging
   double* sFace = smem + S::OFF_FACE;
-  double* sDH = smem + S::OFF_DH;     // [k][c][THREADS*NPT] (DH_SMEM)
   int* sTab = reinterpret_cast<int*>(smem + S::OFF_TAB);   // [axis][RP]: c*SC + ib*sb + ic*sc2
   ADG_DEBUG_POISON();
 
@@ -344,16 +297,6 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
         afr[mt][kc] = (ii < NQ && jj < NQ) ? P.ops.diff[ii][jj] : 0.0;
       }
   }
-  // LN 2: this lane's two output rows of diff (rows >= NQ are zero dummies)
-  constexpr int TPL = (NQ + 1) / 2;          // lanes per line
-  constexpr int LPW = 32 / TPL;              // lines per warp task
-  const int lrow = 2 * (lane % TPL);
-  double drw0[NQ], drw1[NQ];
-#pragma unroll
-  for (int j = 0; j < NQ; ++j) {
-    drw0[j] = (LN == 2 && lrow < NQ) ? P.ops.diff[lrow][j] : 0.0;
-    drw1[j] = (LN == 2 && lrow + 1 < NQ) ? P.ops.diff[lrow + 1][j] : 0.0;
-  }
   // GEMM column offsets: column r = c*NF + (ib*NQ + ic) of axis a -> padded address
   // of (c, i_a = 0, ib, ic); padded columns clamp to the last real column
   for (int e = tid; e < 3 * S::RP; e += THREADS) {
@@ -364,18 +307,11 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
     sTab[e] = c * SC + (y / NQ) * sb + (y % NQ) * sc2;
   }
   // per-node time line in thread-private (local) memory
-  // (TM: node 0's line is in TMEM; qo holds the others, index n - 1)
-  constexpr int QN = (TM == 1) ? (NPT > 1 ? NPT - 1 : 1) : NPT;
-  constexpr int Q0 = (TM == 1) ? 1 : 0;
+  // (TM: node 0's old iterate is in TMEM; qo holds the others, index n - 1)
+  constexpr int QN = TM ? (NPT > 1 ? NPT - 1 : 1) : NPT;
+  constexpr int Q0 = TM ? 1 : 0;
   double qo[QN][NQ][M];
-  // (TM 2: node 0's divergence history is in TMEM instead; dh holds the others, index n - 1)
-  constexpr int D0 = (TM == 2) ? 1 : 0;
-  constexpr int DN = S::DH_SMEM ? 1 : (NPT - D0 > 0 ? NPT - D0 : 1);
-  double dh[DN][S::DH_SMEM ? 1 : NQ][M];
-  auto dhp = [&](int n, int k, int c) -> double& {
-    if constexpr (S::DH_SMEM) return sDH[(k * M + c) * (THREADS * NPT) + n * THREADS + tid];
-    else return dh[n - D0][k][c];
-  };
+  double dh[NPT][NQ][M];                 // divergence history
   int iters = 0;
   bool failed = false;
   // TM: the time line of the thread's first node lives in TMEM, column
@@ -392,7 +328,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
     tq = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 128);
   }
   auto qo_slice = [&](int n, int k, double (&qq)[M]) {
-    if (TM == 1 && n == 0) {
+    if (TM && n == 0) {
       tmem_ld_doubles<M>(tq + 2 * k, 2 * NQ, qq);
     } else {
 #pragma unroll
@@ -403,7 +339,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
   for (int it = 0; it < cap; ++it) {
     // first iteration: q_t = Q at every time level, so its NQ slices are identical —
     // one is computed and its divergence stored for every k
-    const int nsl = (FA && it == 0) ? 1 : NQ;
+    const int nsl = (it == 0) ? 1 : NQ;
 #pragma unroll 1
     for (int k = 0; k < nsl; ++k) {
       double F[NPT][DIM][M];
@@ -418,196 +354,70 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel_ho(const SweepParams P) {
         }
         flux<DIM>(qq, F[n]);
       }
-if constexpr (FA) {
-        // stage the flux of all three axes (padded natural layout, one slab per axis)
+      // stage the flux of all three axes (padded natural layout, one slab per axis)
 #pragma unroll
-        for (int n = 0; n < NPT; ++n) {
-          if (!an[n]) continue;
+      for (int n = 0; n < NPT; ++n) {
+        if (!an[n]) continue;
 #pragma unroll
-          for (int a = 0; a < DIM; ++a)
+        for (int a = 0; a < DIM; ++a)
 #pragma unroll
-            for (int c = 0; c < M; ++c) sFA[a * S::R_FA + c * SC + pn[n]] = F[n][a][c];
-        }
-        __syncthreads();
-        if constexpr (LN == 2) {
-          // warp task = LPW lines of the slice (any axis); lane group g owns line
-          // task*LPW + g, lane r of the group outputs rows 2r, 2r+1; outputs
-          // overwrite the line after the whole warp has read its inputs
-          constexpr int NTASK = (DIM * RR + LPW - 1) / LPW;
-          const int g = lane / TPL;
-          for (int task = warp; task < NTASK; task += NW) {
-            const int l = task * LPW + g;
-            const bool lv = (g < LPW) && (l < DIM * RR);
-            const int a = (l >= 2 * RR) ? 2 : (l >= RR) ? 1 : 0;
-            const int sa = (a == 0) ? P0 : (a == 1) ? P1 : 1;
-            double* ln = sFA + a * S::R_FA + (lv ? sTab[a * S::RP + l - a * RR] : 0);
-            double o0 = 0.0, o1 = 0.0;
+          for (int c = 0; c < M; ++c) sFA[a * S::R_FA + c * SC + pn[n]] = F[n][a][c];
+      }
+      __syncthreads();
+      for (int item = warp; item < DIM * NT; item += NW) {
+        const int a = item / NT, nt = item - a * NT;
+        const int sa = (a == 0) ? P0 : (a == 1) ? P1 : 1;
+        double* slab = sFA + a * S::R_FA;
+        const int* tab = sTab + a * S::RP;
+        double cacc[MT][2];
 #pragma unroll
-            for (int j = 0; j < NQ; ++j) {
-              const double v = ln[j * sa];
-              o0 = fma(drw0[j], v, o0);
-              o1 = fma(drw1[j], v, o1);
-            }
-            __syncwarp();
-            if (lv) {
-              ln[lrow * sa] = o0;
-              if (lrow + 1 < NQ) ln[(lrow + 1) * sa] = o1;
-            }
-            __syncwarp();
-          }
-        } else if constexpr (LN == 1) {
-          // every derivative line of the slice: l = (axis, column); a line's outputs
-          // overwrite its inputs (lines are disjoint)
-          for (int l = tid; l < DIM * RR; l += THREADS) {
-            if (l < RR) deriv_line<NQ, P0>(sFA + sTab[l], P);
-            else if (l < 2 * RR) deriv_line<NQ, P1>(sFA + S::R_FA + sTab[S::RP + l - RR], P);
-            else deriv_line<NQ, 1>(sFA + 2 * S::R_FA + sTab[2 * S::RP + l - 2 * RR], P);
-          }
-        } else
-        for (int item = warp; item < DIM * NT; item += NW) {
-          const int a = item / NT, nt = item - a * NT;
-          const int sa = (a == 0) ? P0 : (a == 1) ? P1 : 1;
-          double* slab = sFA + a * S::R_FA;
-          const int* tab = sTab + a * S::RP;
-          double cacc[MT][2];
+        for (int mt = 0; mt < MT; ++mt) { cacc[mt][0] = 0.0; cacc[mt][1] = 0.0; }
+        const double* bbase = slab + tab[nt * 8 + (lane >> 2)];
+        double bv[KC];
 #pragma unroll
-          for (int mt = 0; mt < MT; ++mt) { cacc[mt][0] = 0.0; cacc[mt][1] = 0.0; }
-          const double* bbase = slab + tab[nt * 8 + (lane >> 2)];
-          double bv[KC];
+        for (int kc = 0; kc < KC; ++kc) bv[kc] = bbase[min(kc * 4 + (lane & 3), NQ - 1) * sa];
+        __syncwarp();
 #pragma unroll
-          for (int kc = 0; kc < KC; ++kc) bv[kc] = bbase[min(kc * 4 + (lane & 3), NQ - 1) * sa];
-          __syncwarp();
-#pragma unroll
-          for (int kc = 0; kc < KC; ++kc)
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt)
-              dmma_8x8x4(cacc[mt][0], cacc[mt][1], afr[mt][kc], bv[kc], cacc[mt][0], cacc[mt][1]);
+        for (int kc = 0; kc < KC; ++kc)
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt)
+            dmma_8x8x4(cacc[mt][0], cacc[mt][1], afr[mt][kc], bv[kc], cacc[mt][0], cacc[mt][1]);
 #pragma unroll
-            for (int e2 = 0; e2 < 2; ++e2) {
-              const int ip = mt * 8 + (lane >> 2);
-              const int r = nt * 8 + 2 * (lane & 3) + e2;
-              if (ip < NQ && r < RR) slab[tab[r] + ip * sa] = cacc[mt][e2];
-            }
-        }
-        __syncthreads();
+        for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int n = 0; n < NPT; ++n)
-#pragma unroll
-          for (int c = 0; c < M; ++c) {
-            const double v = (sFA[c * SC + pn[n]] + sFA[S::R_FA + c * SC + pn[n]]) +
-                             sFA[2 * S::R_FA + c * SC + pn[n]];
-            if (it == 0) {
-#pragma unroll
-              for (int kk = 0; kk < NQ; ++kk) {
-                if (TM == 2 && n == 0) tmem_st_d(tq + 2 * (NQ * c + kk), v);
-                else dhp(n, kk, c) = v;
-              }
-            } else if (TM == 2 && n == 0) tmem_st_d(tq + 2 * (NQ * c + k), v);
-            else dhp(n, k, c) = v;
+          for (int e2 = 0; e2 < 2; ++e2) {
+            const int ip = mt * 8 + (lane >> 2);
+            const int r = nt * 8 + 2 * (lane & 3) + e2;
+            if (ip < NQ && r < RR) slab[tab[r] + ip * sa] = cacc[mt][e2];
           }
-      } else {
-#pragma unroll 1
-        for (int a = 0; a < DIM; ++a) {
-          // stage F_a in the padded natural layout
-  #pragma unroll
-          for (int n = 0; n < NPT; ++n) {
-            if (!an[n]) continue;
-  #pragma unroll
-            for (int c = 0; c < M; ++c) {
-              const double v = (a == 0) ? F[n][0][c] : (a == 1) ? F[n][1][c] : F[n][2][c];
-              sFA[c * SC + pn[n]] = v;
-            }
-          }
-          __syncthreads();
-          // strides of the contraction axis and of the two other axes (ib < ic in axis order)
-          const int sa = (a == 0) ? P0 : (a == 1) ? P1 : 1;
-          const int sb = (a == 0) ? P1 : P0;
-          const int sc2 = (a == 2) ? P1 : 1;
-          // GEMM tiles: warp w takes n-tiles w, w+NW, ...
-          for (int nt = warp; nt < NT; nt += NW) {
-            double cacc[MT][2];
-  #pragma unroll
-            for (int mt = 0; mt < MT; ++mt) { cacc[mt][0] = 0.0; cacc[mt][1] = 0.0; }
-            // B[j][r]: r = c*NF + (ib*NQ + ic); columns past RR and rows past NQ read a
-            // finite in-range value (their A entries / outputs are zero / discarded)
-            const int rb = min(nt * 8 + (lane >> 2), RR - 1);
-            const int cb = rb / NF, yb = rb % NF;
-            const double* bbase = sFA + cb * SC + (yb / NQ) * sb + (yb % NQ) * sc2;
-  #pragma unroll
-            for (int kc = 0; kc < KC; ++kc) {
-              const int jj = min(kc * 4 + (lane & 3), NQ - 1);
-              const double b = bbase[jj * sa];
-  #pragma unroll
-              for (int mt = 0; mt < MT; ++mt)
-                dmma_8x8x4(cacc[mt][0], cacc[mt][1], afr[mt][kc], b, cacc[mt][0], cacc[mt][1]);
-            }
-            // C[i'][r]: lane holds rows mt*8 + g, columns nt*8 + 2*t4 + {0,1}
-  #pragma unroll
-            for (int mt = 0; mt < MT; ++mt)
-  #pragma unroll
-              for (int e2 = 0; e2 < 2; ++e2) {
-                const int ip = mt * 8 + (lane >> 2);
-                const int r = nt * 8 + 2 * (lane & 3) + e2;
-                if (ip < NQ && r < RR) {
-                  const int c = r / NF, y = r % NF;
-                  const int ad = c * SC + ip * sa + (y / NQ) * sb + (y % NQ) * sc2;
-                  if (a == 0) sDv[ad] = cacc[mt][e2];
-                  else sDv[ad] += cacc[mt][e2];
-                }
-              }
-          }
-          __syncthreads();
-        }
-  #pragma unroll
+      }
+      __syncthreads();
+#pragma unroll
       for (int n = 0; n < NPT; ++n)
 #pragma unroll
-        for (int c = 0; c < M; ++c) dhp(n, k, c) = sDv[c * SC + pn[n]];
-        static_assert(TM != 2, "the TMEM divergence history is wired into the fused-axes path");
-      }
-
+        for (int c = 0; c < M; ++c) {
+          const double v = (sFA[c * SC + pn[n]] + sFA[S::R_FA + c * SC + pn[n]]) +
+                           sFA[2 * S::R_FA + c * SC + pn[n]];
+          if (it == 0) {
+#pragma unroll
+            for (int kk = 0; kk < NQ; ++kk) dh[n][kk][c] = v;
+          } else {
+            dh[n][k][c] = v;
+          }
+        }
     }
-    if constexpr (TM == 2) tmem_wait_st();
     // time contraction + Picard update per node
     BitMax bm;
-#ifndef ADG_HO_CR
-#define ADG_HO_CR 1
-#endif
-#if ADG_HO_CR == 0
-    static_assert(!TM, "the TMEM time line needs the register time contraction (ADG_HO_CR 1)");
-#pragma unroll
-    for (int n = 0; n < NPT; ++n) {
-#pragma unroll 1
-      for (int t = 0; t < NQ; ++t) {
-#pragma unroll
-        for (int c = 0; c < M; ++c) {
-          double acc = 0.0;
-#pragma unroll
-          for (int k = 0; k < NQ; ++k) acc = fma(P.ops.integ[t][k], dhp(n, k, c), acc);
-          const double qn = Qx[n][c] - scale * acc;
-          const double qold = (it == 0) ? Qx[n][c] : qo[n][t][c];
-          const double dd = fabs(qn - qold);
-          if (an[n]) bm.add(dd);
-          qo[n][t][c] = qn;
-        }
-      }
-    }
-#else
 #pragma unroll
     for (int n = 0; n < NPT; ++n) {
 #pragma unroll 1
       for (int c = 0; c < M; ++c) {
         // the divergence history of (n, c) is read once; every time level from registers
         double dk[NQ];
-        if (TM == 2 && n == 0) {
-          tmem_ld_doubles<NQ>(tq + 2 * NQ * c, 2, dk);
-        } else {
 #pragma unroll
-          for (int k = 0; k < NQ; ++k) dk[k] = dhp(n, k, c);
-        }
+        for (int k = 0; k < NQ; ++k) dk[k] = dh[n][k][c];
         double ql[NQ];                                   // TM: the old time line of (0, c)
-        if (TM == 1 && n == 0) {
+        if (TM && n == 0) {
           if (it > 0) tmem_ld_doubles<NQ>(tq + 2 * NQ * c, 2, ql);
           else {
 #pragma unroll
@@ -620,16 +430,15 @@ if constexpr (FA) {
 #pragma unroll
           for (int k = 0; k < NQ; ++k) acc = fma(P.ops.integ[t][k], dk[k], acc);
           const double qn = Qx[n][c] - scale * acc;
-          const double qold = (TM == 1 && n == 0) ? ql[t] : (it == 0) ? Qx[n][c] : qo[n - Q0][t][c];
+          const double qold = (TM && n == 0) ? ql[t] : (it == 0) ? Qx[n][c] : qo[n - Q0][t][c];
           const double dd = fabs(qn - qold);
           if (an[n]) bm.add(dd);
-          if (TM == 1 && n == 0) tmem_st_d(tq + 2 * (NQ * c + t), qn);
+          if (TM && n == 0) tmem_st_d(tq + 2 * (NQ * c + t), qn);
           else qo[n - Q0][t][c] = qn;
         }
       }
     }
-    if constexpr (TM == 1) tmem_wait_st();
-#endif
+    if constexpr (TM) tmem_wait_st();
     iters = it + 1;
     if (__syncthreads_or(bm.bad())) { failed = true; break; }
     const double delta = block_max<NW>(__longlong_as_double((long long)bm.m), sRed);
