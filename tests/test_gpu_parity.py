@@ -286,6 +286,26 @@ def test_gpu_mode_equivalence_forced_dt(cuda_ok):
     assert out["straightforward"][1] == 30 and out["fused"][1] == 11
 
 
+@pytest.mark.parametrize("p", [3, 5, 7, 9])
+def test_gpu_mode_equivalence_3d_kernels(cuda_ok, p):
+    """The same property through the straightforward passes (MODE_SF_PREDICT /
+    MODE_SF_CORRECT) of every dedicated 3D kernel: under a forced step size the two
+    drivers agree to <= 1e-12."""
+    d, L = 3, 1
+    Q0 = scenarios.build("bump", d, L, p, seed=11, noise=1e-3)
+    out = {}
+    for mode in ("straightforward", "fused"):
+        grid = build_grid(d, L, p, d + 2)
+        grid.Q[...] = Q0
+        kern = Kernels(EulerSystem(d), make_basis(p), grid, None)
+        drv = Driver(grid, kern, TimeControl(forced_dt=1e-4), mode, host_sync="run")
+        drv.run(steps=4)
+        out[mode] = np.array(grid.Q)
+        drv.close()
+    scale = np.max(np.abs(out["fused"]))
+    assert np.max(np.abs(out["fused"] - out["straightforward"])) <= 1e-12 * scale
+
+
 def test_gpu_straightforward_final_time(cuda_ok):
     """run(final_time=...) clamps the last step (src/scheduler.py:219-226)."""
     d, L, p = 2, 1, 2
