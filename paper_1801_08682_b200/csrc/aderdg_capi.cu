@@ -358,6 +358,7 @@ struct adg_handle {
   unsigned char* lim_troubled = nullptr;
   int* lim_list = nullptr;
   double* lim_lam = nullptr;
+  double* sm_scratch = nullptr;   // per-SM slots of the p = 9 kernel (previous Picard iterate)
   double* lim_scratch = nullptr;
   long long lim_scratch_cta = 0;
   unsigned lim_grid = 0;
@@ -440,6 +441,7 @@ static SweepParams sweep_params(adg_handle* h, int mode) {
   P.lim_troubled = h->lim ? h->lim_troubled : nullptr;
   P.lim_cur = h->lim ? h->lim_prev[h->sweep_index & 1] : nullptr;
   P.lim_lam = h->lim ? h->lim_lam : nullptr;
+  P.sm_scratch = h->sm_scratch;
   P.spike_step = h->cfg.spike_step;
   P.p = h->cfg.p;
   P.h = h->h;
@@ -639,6 +641,11 @@ adg_status adg_create(const adg_config* cfg, adg_handle** out) {
   CUDA_TRY(h, cudaMalloc(&h->tr[1], tr_bytes));
   CUDA_TRY(h, cudaMalloc(&h->st, sizeof(DevState)));
   CUDA_TRY(h, cudaMalloc(&h->recs, sizeof(StepRecord) * h->rec_cap));
+  if (c.d == 3 && c.p == 9 && c.system == 0) {     // sweep_kernel_p9: one slot per SM (one CTA per SM)
+    int sms = 0;
+    CUDA_TRY(h, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+    CUDA_TRY(h, cudaMalloc(&h->sm_scratch, sizeof(double) * (size_t)sms * ShapeP9::SCRATCH));
+  }
   CUDA_TRY(h, cudaMemsetAsync(h->D, 0, state_bytes, h->stream));        // mesh.py:238-239
   CUDA_TRY(h, cudaMemsetAsync(h->tr[0], 0, tr_bytes, h->stream));
   CUDA_TRY(h, cudaMemsetAsync(h->tr[1], 0, tr_bytes, h->stream));
@@ -659,6 +666,7 @@ void adg_destroy(adg_handle* h) {
   if (h->tr[1]) cudaFree(h->tr[1]);
   if (h->st) cudaFree(h->st);
   if (h->recs) cudaFree(h->recs);
+  if (h->sm_scratch) cudaFree(h->sm_scratch);
   if (h->flush) cudaFree(h->flush);
   void* lim_bufs[] = {h->lim_P, h->lim_R, h->lim_nearest, h->lim_sample, h->lim_rank, h->lim_prev[0],
                       h->lim_prev[1], h->lim_troubled, h->lim_list, h->lim_lam, h->lim_scratch};

@@ -16,9 +16,15 @@
 //     shared memory ([c][k][tid], conflict-free) and component 4 in tensor memory
 //     (columns 100..119): 256 KB of TMEM + 160 KB of shared memory;
 //   * the only copy of the previous iterate that the convergence test
-//     max |q_new - q| needs is streamed through thread-private memory once per
-//     iteration (written and read by the time contraction, 400 KB per cell: the 148
-//     resident cells keep 59 MB in L2) — the slice loop touches no local memory.
+//     max |q_new - q| needs is streamed once per iteration (written and read by the time
+//     contraction, 400 KB per cell) through a per-SM global slot (SweepParams::sm_scratch,
+//     one CTA per SM, indexed by %smid, [line][t][thread]: coalesced): the 148 slots are 60 MB
+//     and mostly stay in the 126 MB L2 (r02 ncu, DRAM bytes per 27^3 sweep: thread-private
+//     local memory 42 GB, this slot 21 GB, the slot with an L2 evict-last cache-hint policy
+//     8 GB but 3 % slower — the cache_hint forms of ld / st cost more than the DRAM traffic
+//     of a kernel that uses 14 % of the HBM bandwidth; a persisting access-policy window on
+//     the launch made it worse, 68 GB).  The kernel's streaming global traffic — Q, D, face
+//     records — uses the evict-first hints __ldcs / __stcs.  The slice loop touches neither.
 //
 // With 160 KB of the shared memory holding state, the spatial derivatives of a slice
 // go one axis at a time through one padded flux slab (45 KB): owners store F_a ->
@@ -57,6 +63,8 @@ struct ShapeP9 {
   static constexpr int R_SLAB = M * SC;                       // one axis' flux / derivative (>= M*NS: tail staging)
   static constexpr int CB = 4;                                // node-B components in shared memory
   static constexpr int R_SB = CB * NQ * THREADS;              // (>= the corrector's signed F* per face)
+  // per-SM global slot: the previous iterate of the convergence test, [node slot][c][t][thread]
+  static constexpr int SCRATCH = 2 * M * NQ * THREADS;
   static constexpr int OFF_RED = 0;
   static constexpr int OFF_SLAB = (R_RED + 1) & ~1;
   static constexpr int OFF_SB = OFF_SLAB + R_SLAB;
@@ -176,7 +184,7 @@ __global__ void __launch_bounds__(ShapeP9::THREADS, 1) sweep_kernel_p9(const Swe
 #pragma unroll
   for (int n = 0; n < 2; ++n)
 #pragma unroll
-    for (int c = 0; c < M; ++c) Qx[n][c] = Qg[xn[n] * M + c];
+    for (int c = 0; c < M; ++c) Qx[n][c] = __ldcs(&Qg[xn[n] * M + c]);
 
   if (mode_corrects(mode)) {
     // ------------- Riemann on the 2d faces (kernels.py:147-179), time-collapsed -------------
@@ -202,9 +210,9 @@ __global__ void __launch_bounds__(ShapeP9::THREADS, 1) sweep_kernel_p9(const Swe
       const double* nb = P.tr_in + ((long long)(f ^ 1) * P.slots + nb_slot[f]) * REC;
       const double* mr = (f & 1) ? own : nb;
       const double* pr = (f & 1) ? nb : own;
-      const double alpha = rusanov_alpha(mr[2 * NF * M], pr[2 * NF * M]);
-      const double fs = __dsub_rn(__dmul_rn(0.5, __dadd_rn(mr[NF * M + yc], pr[NF * M + yc])),
-                                  __dmul_rn(__dmul_rn(0.5, alpha), __dsub_rn(pr[yc], mr[yc])));
+      const double alpha = rusanov_alpha(__ldcs(mr + 2 * NF * M), __ldcs(pr + 2 * NF * M));
+      const double fs = __dsub_rn(__dmul_rn(0.5, __dadd_rn(__ldcs(mr + NF * M + yc), __ldcs(pr + NF * M + yc))),
+                                  __dmul_rn(__dmul_rn(0.5, alpha), __dsub_rn(__ldcs(pr + yc), __ldcs(mr + yc))));
       sFace[e] = (f & 1) ? fs : -fs;
     }
     __syncthreads();
@@ -217,7 +225,7 @@ __global__ void __launch_bounds__(ShapeP9::THREADS, 1) sweep_kernel_p9(const Swe
       idx3(xn[n], i[0], i[1], i[2]);
       double Dx[M];
 #pragma unroll
-      for (int c = 0; c < M; ++c) Dx[c] = Dg[xn[n] * M + c];
+      for (int c = 0; c < M; ++c) Dx[c] = __ldcs(&Dg[xn[n] * M + c]);
 #pragma unroll
       for (int a = 0; a < DIM; ++a) {
         const int y = (a == 0) ? i[1] * NQ + i[2] : (a == 1) ? i[0] * NQ + i[2] : i[0] * NQ + i[1];
@@ -242,7 +250,7 @@ __global__ void __launch_bounds__(ShapeP9::THREADS, 1) sweep_kernel_p9(const Swe
         Qx[n][M - 1] = __dadd_rn(__ddiv_rn(pr, 0.4), __ddiv_rn(__dmul_rn(0.5, jj), rho));
       }
 #pragma unroll
-      for (int c = 0; c < M; ++c) Qg[xn[n] * M + c] = Qx[n][c];
+      for (int c = 0; c < M; ++c) __stcs(&Qg[xn[n] * M + c], Qx[n][c]);
     }
     if (!hasB) {
 #pragma unroll
@@ -319,7 +327,9 @@ __global__ void __launch_bounds__(ShapeP9::THREADS, 1) sweep_kernel_p9(const Swe
 
   // the convergence test's copy of the previous iterate and the initial state, indexed
   // by the rolled (node, component) loop of the time contraction: thread-private memory
-  double qprev[2 * M][NQ];
+  unsigned smid;
+  asm("mov.u32 %0, %%smid;" : "=r"(smid));
+  double* qprev = P.sm_scratch + (size_t)smid * S::SCRATCH + tid;   // [nc][t][THREADS]
   double q0l[2 * M];
 #pragma unroll
   for (int n = 0; n < 2; ++n)
@@ -423,9 +433,9 @@ __global__ void __launch_bounds__(ShapeP9::THREADS, 1) sweep_kernel_p9(const Swe
 #pragma unroll
         for (int k = 0; k < NQ; ++k) acc = fma(P.ops.integ[t][k], dk[k], acc);
         qn[t] = qc - scale * acc;
-        const double qold = (it == 0) ? qc : qprev[nc][t];
+        const double qold = (it == 0) ? qc : qprev[(nc * NQ + t) * THREADS];
         if (n == 0 || hasB) bm.add(fabs(qn[t] - qold));
-        qprev[nc][t] = qn[t];
+        qprev[(nc * NQ + t) * THREADS] = qn[t];
       }
       if (in_tmem) {
         tmem_st10(ta, qn);
@@ -519,7 +529,7 @@ __global__ void __launch_bounds__(ShapeP9::THREADS, 1) sweep_kernel_p9(const Swe
       double v = 0.0;
 #pragma unroll
       for (int i = 0; i < NQ; ++i) v = fma(vec[i], sN[c * NS + xb + i * sa], v);
-      P.tr_out[((long long)(2 * a + side) * P.slots + own_slot) * REC + NF * M + y * M + c] = v;
+      __stcs(&P.tr_out[((long long)(2 * a + side) * P.slots + own_slot) * REC + NF * M + y * M + c], v);
     }
   }
   if (__syncthreads_or(bad)) {
@@ -536,7 +546,7 @@ __global__ void __launch_bounds__(ShapeP9::THREADS, 1) sweep_kernel_p9(const Swe
   for (int n = 0; n < 2; ++n)
     if (an[n])
 #pragma unroll
-      for (int c = 0; c < M; ++c) Dg[xn[n] * M + c] = Dv[n][c] * scale;
+      for (int c = 0; c < M; ++c) __stcs(&Dg[xn[n] * M + c], Dv[n][c] * scale);
 
   // ---------------- q-bar face traces ----------------
   // (the barrier of the error vote above separates the last f-bar trace reads from these stores)
@@ -559,7 +569,7 @@ __global__ void __launch_bounds__(ShapeP9::THREADS, 1) sweep_kernel_p9(const Swe
     double v = 0.0;
 #pragma unroll
     for (int i = 0; i < NQ; ++i) v = fma(vec[i], sN[c * NS + xb + i * sa], v);
-    P.tr_out[((long long)f * P.slots + own_slot) * REC + y * M + c] = v;
+    __stcs(&P.tr_out[((long long)f * P.slots + own_slot) * REC + y * M + c], v);
   }
   // ---------------- s_max over the space-time traces, one time level at a time ----------------
 #pragma unroll 1
