@@ -75,7 +75,8 @@ def single(d, L, p, steps, **kw):
 
 
 @pytest.mark.parametrize("overlap", [True, False])
-@pytest.mark.parametrize("world,d,L,p,steps", [(2, 3, 2, 3, 4), (3, 3, 2, 5, 3), (2, 2, 3, 3, 6)])
+@pytest.mark.parametrize("world,d,L,p,steps", [(2, 3, 2, 3, 4), (3, 3, 2, 5, 3), (2, 2, 3, 3, 6),
+                                                (2, 3, 1, 7, 3), (3, 3, 1, 9, 2)])
 def test_slabs_equal_single_gpu_bitwise(cuda_ok, tmp_path, world, d, L, p, steps, overlap):
     Q, tcs, errs = run_slabs(world, d, L, p, steps, tmp_path, overlap=overlap)
     assert errs == [""] * world
