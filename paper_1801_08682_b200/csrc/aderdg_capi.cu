@@ -641,10 +641,16 @@ adg_status adg_create(const adg_config* cfg, adg_handle** out) {
   CUDA_TRY(h, cudaMalloc(&h->tr[1], tr_bytes));
   CUDA_TRY(h, cudaMalloc(&h->st, sizeof(DevState)));
   CUDA_TRY(h, cudaMalloc(&h->recs, sizeof(StepRecord) * h->rec_cap));
-  if (c.d == 3 && c.p == 9 && c.system == 0) {     // sweep_kernel_p9: one slot per SM (one CTA per SM)
-    int sms = 0;
-    CUDA_TRY(h, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
-    CUDA_TRY(h, cudaMalloc(&h->sm_scratch, sizeof(double) * (size_t)sms * ShapeP9::SCRATCH));
+  if (c.d == 3 && c.p == 9 && c.system == 0) {     // sweep_kernel_p9: one slot per %smid value (one CTA per SM)
+    unsigned* d_n = nullptr;
+    unsigned nsm = 0;
+    CUDA_TRY(h, cudaMalloc(&d_n, sizeof(unsigned)));
+    nsmid_kernel<<<1, 1, 0, h->stream>>>(d_n);
+    CUDA_TRY(h, cudaMemcpyAsync(&nsm, d_n, sizeof(unsigned), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    cudaFree(d_n);
+    if (nsm == 0 || nsm > 4096) return fail(h, ADG_ERR_RUNTIME, "cannot size the per-SM scratch slots");
+    CUDA_TRY(h, cudaMalloc(&h->sm_scratch, sizeof(double) * (size_t)nsm * ShapeP9::SCRATCH));
   }
   CUDA_TRY(h, cudaMemsetAsync(h->D, 0, state_bytes, h->stream));        // mesh.py:238-239
   CUDA_TRY(h, cudaMemsetAsync(h->tr[0], 0, tr_bytes, h->stream));

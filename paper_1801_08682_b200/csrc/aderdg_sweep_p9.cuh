@@ -134,6 +134,14 @@ __device__ __forceinline__ void deriv_line_eo10(double* ln, const SweepParams& P
   }
 }
 
+// number of %smid values of the device (%smid ranges over 0 .. %nsmid - 1, which may exceed
+// the count of enabled SMs): the per-SM scratch slots are sized by it
+__global__ void nsmid_kernel(unsigned* out) {
+  unsigned n;
+  asm("mov.u32 %0, %%nsmid;" : "=r"(n));
+  *out = n;
+}
+
 __global__ void __launch_bounds__(ShapeP9::THREADS, 1) sweep_kernel_p9(const SweepParams P) {
   using S = ShapeP9;
   constexpr int DIM = 3, M = 5, NQ = 10, NS = S::NS, NF = S::NF, REC = S::REC, NW = S::NW;
