@@ -75,7 +75,7 @@ CONFIGS = {
 }
 DEFAULT_CONFIG = "cfg4"
 
-PEAKS_FILE = os.path.join(REPO, "profiles", "fp64_peaks_r01.jsonl")
+PEAKS_FILE = os.path.join(REPO, "profiles", "fp64_peaks_r02.jsonl")
 NCU_TRAFFIC_FILE = os.path.join(REPO, "profiles", "r02", "sweep_traffic.json")
 METRIC = "fp64 DoF-updates/s (3D Euler ADER-DG, fused step)"
 
@@ -539,7 +539,7 @@ def main():
                                            "kernels' share of the step, measured in an instrumented replay of "
                                            "the same steps with CUDA events around every rerun / sweep launch"),
                          "flops_per_step_per_gpu": flops_total / K,
-                         "peak_source": "profiles/fp64_peaks_r01.jsonl (measured DMMA m8n8k4; "
+                         "peak_source": "profiles/fp64_peaks_r02.jsonl (measured DMMA m8n8k4; "
                                         f"DFMA {dfma} TF/s) — MEASURED_PEAKS.json has no fp64 entry",
                          "traffic_per_sweep_launch": traffic_launch,
                          "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum of one full sweep "
