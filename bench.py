@@ -30,7 +30,7 @@ Reported on one JSON line (rank 0):
   roofline      the sweep kernel (fused sweep + rerun passes): algorithmic flops
                 (paper_1801_08682_b200/roofline.py with the measured Picard counts) per
                 step / its time per step, against the measured FP64 peak
-                (profiles/fp64_peaks_r01.jsonl; MEASURED_PEAKS.json has no fp64 entry)
+                (profiles/fp64_peaks_r02.jsonl; MEASURED_PEAKS.json has no fp64 entry)
   cpu_baseline  the CPU oracle port (oracle/aderdg_oracle.py, batched numpy restatement of
                 the reference fused driver) on ONE pinned host core, plus a row with all
                 host cores as BLAS threads; per-cell-step cost measured on a 9^3 sample of
