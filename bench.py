@@ -507,7 +507,9 @@ def main():
     # conditional node fires (a segment's first step, whose condition defaults to 1, and
     # steps after a finish that asked for a rerun)
     sweeps = 2 if (world > 1 and drv.lay.planes_local > 2) else 1
-    launches = timed_rerun_launches + K * (sweeps + 1)
+    # 2D p = 3 on one GPU: the sweep's last CTA is the time control (no finish launch)
+    fused_tc = world == 1 and cfgd["d"] == 2 and cfgd["p"] == 3
+    launches = timed_rerun_launches + K * (sweeps + (0 if fused_tc else 1))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -246,10 +246,18 @@ int adg_device_count(void);
 /* Per-handle launch options (defaults in brackets):
  * ADG_OPT_GRAPH [1]       adg_run / adg_run_timed* capture their steps into one CUDA graph
  * ADG_OPT_COND_RERUN [1]  the rerun pass is a conditional graph node
- * ADG_OPT_HOST_CHUNKS [16] wave-aligned cell chunks of adg_step_host (1..81) */
+ * ADG_OPT_HOST_CHUNKS [16] wave-aligned cell chunks of adg_step_host (1..81)
+ * ADG_OPT_FUSE_FINISH [1] kernels that can (2D p = 3) run the step's time control in the last
+ *                         CTA of the sweep launch instead of a separate launch (one slab)
+ * ADG_OPT_PERSISTENT [1]  kernels that can (2D p = 3) run the step sequences of adg_run /
+ *                         adg_run_timed in ONE cooperative launch with a grid barrier per step
+ *                         (needs ADG_OPT_GRAPH 1; falls back to the step graph when the device
+ *                         refuses the cooperative launch) */
 #define ADG_OPT_GRAPH 1
 #define ADG_OPT_COND_RERUN 2
 #define ADG_OPT_HOST_CHUNKS 3
+#define ADG_OPT_FUSE_FINISH 4
+#define ADG_OPT_PERSISTENT 5
 adg_status adg_set_option(adg_handle* h, int option, int value);
 
 #ifdef __cplusplus

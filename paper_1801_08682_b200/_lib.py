@@ -40,7 +40,7 @@ EXPORTS = (
     "adg_group_init", "adg_group_seed", "adg_group_run", "adg_set_option", "adg_device_count",
 )
 
-ADG_OPT_GRAPH, ADG_OPT_COND_RERUN, ADG_OPT_HOST_CHUNKS = 1, 2, 3
+ADG_OPT_GRAPH, ADG_OPT_COND_RERUN, ADG_OPT_HOST_CHUNKS, ADG_OPT_FUSE_FINISH, ADG_OPT_PERSISTENT = 1, 2, 3, 4, 5
 
 
 class AdgConfig(ctypes.Structure):

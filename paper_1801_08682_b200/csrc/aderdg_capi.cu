@@ -26,6 +26,7 @@
 #include "aderdg_sweep_p5.cuh"
 #include "aderdg_sweep_p7.cuh"
 #include "aderdg_sweep_p9.cuh"
+#include "aderdg_sweep_2d_p3.cuh"
 #include "aderdg_limiter.cuh"
 
 using namespace adg;
@@ -78,10 +79,21 @@ int occ_generic() {
   return occupancy_of(sweep_kernel<PDE, DIM, NQ>, S::THREADS, S::SMEM_BYTES);
 }
 
+// sweep + time control in one launch (the last CTA runs finish_body); kernels without it: null
+typedef void (*launch_fused_fn)(const SweepParams&, const FinishParams&, unsigned* arrive, unsigned grid,
+                                cudaStream_t s);
+
+// `steps` whole realisation steps in one cooperative launch (grid barrier between the steps);
+// returns the launch's cudaError_t, grid = 0 asks for the largest co-resident grid
+typedef cudaError_t (*launch_run_fn)(const SweepParams&, const FinishParams&, unsigned* sync, double* tr0,
+                                     double* tr1, int steps, unsigned cells, cudaStream_t s);
+
 struct Dispatch {
   launch_fn sweep;
   int rec;
   occupancy_fn occ = nullptr;   // resident sweep CTAs per SM (adg_step_host chunking)
+  launch_fused_fn sweep_finish = nullptr;
+  launch_run_fn run = nullptr;
 };
 
 template <int DIM, int NQ>
@@ -189,6 +201,54 @@ Dispatch make_dispatch_p3() {
   return Dispatch{&launch_sweep_p3, ShapeP3::REC, &occ_p3};
 }
 
+// 2D p = 3 (BASELINE cfg 1): 128 threads per cell, one barrier per Picard iteration, optional
+// fused time control (aderdg_sweep_2d_p3.cuh)
+void launch_sweep_2d_p3(const SweepParams& P, unsigned grid, cudaStream_t s) {
+  FusedFinish X;
+  memset(&X, 0, sizeof X);
+  sweep_kernel_2d_p3<<<grid, Shape2P3::THREADS, Shape2P3::SMEM_BYTES, s>>>(P, X);
+}
+
+void launch_sweep_2d_p3_finish(const SweepParams& P, const FinishParams& F, unsigned* arrive, unsigned grid,
+                               cudaStream_t s) {
+  FusedFinish X;
+  X.F = F;
+  X.arrive = arrive;
+  X.on = 1;
+  sweep_kernel_2d_p3<<<grid, Shape2P3::THREADS, Shape2P3::SMEM_BYTES, s>>>(P, X);
+}
+
+int occ_2d_p3() { return occupancy_of(sweep_kernel_2d_p3, Shape2P3::THREADS, Shape2P3::SMEM_BYTES); }
+
+cudaError_t launch_run_2d_p3(const SweepParams& P, const FinishParams& F, unsigned* sync, double* tr0, double* tr1,
+                             int steps, unsigned cells, cudaStream_t s) {
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e == cudaSuccess)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, run_kernel_2d_p3, Shape2P3::THREADS,
+                                                      Shape2P3::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  const unsigned cap = (unsigned)(sms * per_sm);
+  if (cap == 0) return cudaErrorCooperativeLaunchTooLarge;
+  RunParams2P3 R;
+  R.F = F;
+  R.sync = sync;
+  R.tr[0] = tr0;
+  R.tr[1] = tr1;
+  R.steps = steps;
+  SweepParams Pc = P;
+  void* args[] = {(void*)&Pc, (void*)&R};
+  return cudaLaunchCooperativeKernel((const void*)run_kernel_2d_p3, dim3(cells < cap ? cells : cap),
+                                     dim3(Shape2P3::THREADS), args, Shape2P3::SMEM_BYTES, s);
+}
+
+Dispatch make_dispatch_2d_p3() {
+  static_assert(Shape2P3::REC == Shape<2, 4>::REC, "record layout must match");
+  static_assert(Shape2P3::SMEM_BYTES <= 48 * 1024, "no dynamic shared-memory opt-in");
+  return Dispatch{&launch_sweep_2d_p3, Shape2P3::REC, &occ_2d_p3, &launch_sweep_2d_p3_finish, &launch_run_2d_p3};
+}
+
 // subcell limiter kernels (aderdg_limiter.cuh), per PDE plug-in and dimension
 struct LimDispatch {
   void (*detect)(const LimParams&, unsigned, size_t, cudaStream_t);
@@ -273,6 +333,16 @@ bool dispatch_for(int d, int p, int system, Dispatch* out) {
     }
   }
   return dispatch_generic(d, p, out);
+}
+
+// 2D Euler p = 3 under the fused driver (periodic): the latency kernel of BASELINE cfg 1.  The
+// straightforward driver's passes, outflow boundaries and the limiter stay in the generic kernel.
+bool dispatch_small(const adg_config& c, Dispatch* out) {
+  if (c.system == 0 && c.d == 2 && c.p == 3 && c.boundary == 0 && c.driver_mode == 0) {
+    *out = make_dispatch_2d_p3();
+    return true;
+  }
+  return false;
 }
 
 }  // namespace
@@ -379,11 +449,17 @@ struct adg_handle {
   // adg_set_option (explicit, per handle; no environment lookups in the library)
   int opt_graph = 1;                   // ADG_OPT_GRAPH: captured step graphs in adg_run / adg_run_timed*
   int opt_cond_rerun = 1;              // ADG_OPT_COND_RERUN: rerun pass as a conditional graph node
+  int opt_fuse_finish = 1;             // ADG_OPT_FUSE_FINISH: time control inside the sweep launch (kernels that have it)
+  int opt_persistent = 1;              // ADG_OPT_PERSISTENT: whole step sequences in one cooperative launch
+  unsigned* arrive = nullptr;          // [0] CTA arrival counter (fused time control, grid barrier), [1] generation,
+                                       // [2..] one ticket counter per %smid value (2D p = 3 kernel)
+  bool finish_fused = false;           // the sweep in flight carries the time control of its step
   int opt_host_chunks = 16;            // ADG_OPT_HOST_CHUNKS: wave-aligned chunks of adg_step_host
                                        // (cfg 2: 16 -> 1.526 ms, 9 -> 1.557, 23 -> 1.784)
 };
 
 constexpr int ADG_HOST_CHUNKS_MAX = 81;
+constexpr int ADG_SMID_MAX = 1024;           // bound of %nsmid on every device this library targets
 constexpr int ADG_TIMED_NO_PULL = 1 << 16;   // internal adg_run_timed_ex flag: adg_run's graph chunks
 
 static adg_status fail(adg_handle* h, adg_status code, const std::string& msg) {
@@ -442,6 +518,7 @@ static SweepParams sweep_params(adg_handle* h, int mode) {
   P.lim_cur = h->lim ? h->lim_prev[h->sweep_index & 1] : nullptr;
   P.lim_lam = h->lim ? h->lim_lam : nullptr;
   P.sm_scratch = h->sm_scratch;
+  P.sm_ticket = h->arrive + 2;
   P.spike_step = h->cfg.spike_step;
   P.p = h->cfg.p;
   P.h = h->h;
@@ -606,7 +683,7 @@ adg_status adg_create(const adg_config* cfg, adg_handle** out) {
   }
   if (c.boundary == 1 && c.system == 0) {        // ghost faces live in the generic kernel
     if (!dispatch_generic(c.d, c.p, &h->disp)) { h->err = "no generic kernel for this order"; *out = h; return ADG_ERR_CONFIG; }
-  } else if (!dispatch_for(c.d, c.p, c.system, &h->disp)) {
+  } else if (!dispatch_small(c, &h->disp) && !dispatch_for(c.d, c.p, c.system, &h->disp)) {
     snprintf(buf, sizeof buf, "no sm_100a kernel instantiated for d=%d p=%d", c.d, c.p);
     h->err = buf; *out = h; return ADG_ERR_CONFIG;
   }
@@ -641,6 +718,8 @@ adg_status adg_create(const adg_config* cfg, adg_handle** out) {
   CUDA_TRY(h, cudaMalloc(&h->tr[1], tr_bytes));
   CUDA_TRY(h, cudaMalloc(&h->st, sizeof(DevState)));
   CUDA_TRY(h, cudaMalloc(&h->recs, sizeof(StepRecord) * h->rec_cap));
+  CUDA_TRY(h, cudaMalloc(&h->arrive, (2 + ADG_SMID_MAX) * sizeof(unsigned)));
+  CUDA_TRY(h, cudaMemsetAsync(h->arrive, 0, (2 + ADG_SMID_MAX) * sizeof(unsigned), h->stream));
   if (c.d == 3 && c.p == 9 && c.system == 0) {     // sweep_kernel_p9: one slot per %smid value (one CTA per SM)
     unsigned* d_n = nullptr;
     unsigned nsm = 0;
@@ -652,6 +731,12 @@ adg_status adg_create(const adg_config* cfg, adg_handle** out) {
     if (nsm == 0 || nsm > 4096) return fail(h, ADG_ERR_RUNTIME, "cannot size the per-SM scratch slots");
     CUDA_TRY(h, cudaMalloc(&h->sm_scratch, sizeof(double) * (size_t)nsm * ShapeP9::SCRATCH));
   }
+#ifdef ADG_2P3_TIMING
+  if (c.d == 2 && c.p == 3) {                      // tools/cta_timeline.py: 32 stamps per CTA
+    CUDA_TRY(h, cudaMalloc(&h->sm_scratch, sizeof(double) * 32 * (size_t)h->cells_local));
+    CUDA_TRY(h, cudaMemsetAsync(h->sm_scratch, 0, sizeof(double) * 32 * (size_t)h->cells_local, h->stream));
+  }
+#endif
   CUDA_TRY(h, cudaMemsetAsync(h->D, 0, state_bytes, h->stream));        // mesh.py:238-239
   CUDA_TRY(h, cudaMemsetAsync(h->tr[0], 0, tr_bytes, h->stream));
   CUDA_TRY(h, cudaMemsetAsync(h->tr[1], 0, tr_bytes, h->stream));
@@ -659,6 +744,16 @@ adg_status adg_create(const adg_config* cfg, adg_handle** out) {
   memset(&s0, 0, sizeof s0);
   s0.dt_adm = INFINITY;                                                // TimeControl.__init__
   CUDA_TRY(h, cudaMemcpyAsync(h->st, &s0, sizeof s0, cudaMemcpyHostToDevice, h->stream));
+  if (h->disp.run) {
+    // a zero-step launch now: lazy module loading would otherwise bill the cooperative
+    // kernel's first use (~0.4 ms) to a step; a device that refuses it uses the step graph
+    const cudaError_t we = h->disp.run(sweep_params(h, MODE_NORMAL), finish_params(h, 0, 0), h->arrive, h->tr[0],
+                                       h->tr[1], 0, (unsigned)h->cells_local, h->stream);
+    if (we != cudaSuccess) {
+      cudaGetLastError();
+      h->disp.run = nullptr;
+    }
+  }
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   h->hst = s0;
   return ADG_OK;
@@ -672,6 +767,7 @@ void adg_destroy(adg_handle* h) {
   if (h->tr[1]) cudaFree(h->tr[1]);
   if (h->st) cudaFree(h->st);
   if (h->recs) cudaFree(h->recs);
+  if (h->arrive) cudaFree(h->arrive);
   if (h->sm_scratch) cudaFree(h->sm_scratch);
   if (h->flush) cudaFree(h->flush);
   void* lim_bufs[] = {h->lim_P, h->lim_R, h->lim_nearest, h->lim_sample, h->lim_rank, h->lim_prev[0],
@@ -754,6 +850,8 @@ adg_status adg_reset(adg_handle* h) {
   h->hst = s0;
   h->sweep_index = 0;
   h->seeded = false;
+  h->finish_fused = false;
+  CUDA_TRY(h, cudaMemsetAsync(h->arrive, 0, 2 * sizeof(unsigned), h->stream));
   h->err.clear();
   return ADG_OK;
 }
@@ -829,7 +927,18 @@ adg_status adg_phase_sweep_part(adg_handle* h, int part) {
   }
   if (h->sweep_index == 0 && part != ADG_PART_ALL)
     return fail(h, ADG_ERR_CONFIG, "the priming sweep is not split");
-  return launch(h, h->sweep_index == 0 ? MODE_PRIMING : MODE_NORMAL, part);
+  const int mode = h->sweep_index == 0 ? MODE_PRIMING : MODE_NORMAL;
+  // one slab, whole sweep: the kernel's last CTA is the step's time control (adg_phase_finish
+  // then only advances the sweep index)
+  if (part == ADG_PART_ALL && h->disp.sweep_finish && h->opt_fuse_finish && h->cfg.world == 1 &&
+      h->cfg.halo_mode == 0 && !h->lim) {
+    const SweepParams P = sweep_params(h, mode);
+    h->disp.sweep_finish(P, finish_params(h, h->sweep_index == 0 ? 1 : 0, 0), h->arrive, (unsigned)h->cells_local,
+                         h->stream);
+    h->finish_fused = true;
+    return cuda_check(h, cudaGetLastError(), "sweep launch");
+  }
+  return launch(h, mode, part);
 }
 
 adg_status adg_phase_sweep(adg_handle* h) { return adg_phase_sweep_part(h, ADG_PART_ALL); }
@@ -837,7 +946,9 @@ adg_status adg_phase_sweep(adg_handle* h) { return adg_phase_sweep_part(h, ADG_P
 adg_status adg_phase_finish(adg_handle* h) {
   if (!h) return ADG_ERR_CONFIG;
   h->hst_fresh = false;
-  adg_status s = launch_finish(h, (!straightforward(h) && h->sweep_index == 0) ? 1 : 0, 0);
+  adg_status s = ADG_OK;
+  if (h->finish_fused) h->finish_fused = false;    // done by the sweep launch
+  else s = launch_finish(h, (!straightforward(h) && h->sweep_index == 0) ? 1 : 0, 0);
   h->sweep_index += 1;
   return s;
 }
@@ -1101,6 +1212,9 @@ adg_status adg_buffer(adg_handle* h, int which, void** ptr, size_t* bytes) {
     case ADG_BUF_TRACE0: *ptr = h->tr[0]; *bytes = tr_bytes; return ADG_OK;
     case ADG_BUF_TRACE1: *ptr = h->tr[1]; *bytes = tr_bytes; return ADG_OK;
     case ADG_BUF_REDUCE: *ptr = h->st; *bytes = 2 * sizeof(long long); return ADG_OK;
+#ifdef ADG_2P3_TIMING
+    case 99: *ptr = h->sm_scratch; *bytes = sizeof(double) * 32 * (size_t)h->cells_local; return ADG_OK;
+#endif
   }
   return ADG_ERR_CONFIG;
 }
@@ -1151,6 +1265,45 @@ static adg_status enqueue_halo(adg_handle* h, int par);
 // Events: ev[0] / ev[1] bracket the segment; with ADG_TIMED_KERNEL_EVENTS also every
 // rerun / sweep launch (graph nodes that cost gaps: cfg 1 26.6 -> 35.4 us/step, so the
 // throughput run leaves them out and an instrumented replay measures the kernels).
+// `steps` fused steps of a primed single-slab driver in one cooperative launch
+// (Dispatch::run).  *launched = false (and ADG_OK) when the device refuses the cooperative
+// launch: the caller falls back to the step graph.
+static adg_status run_persistent(adg_handle* h, int steps, int flags, double* out, bool* launched) {
+  *launched = false;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  CUDA_TRY(h, cudaEventCreate(&ev[0]));
+  if (cudaEventCreate(&ev[1]) != cudaSuccess) {
+    cudaEventDestroy(ev[0]);
+    return fail(h, ADG_ERR_RUNTIME, "cudaEventCreate failed");
+  }
+  h->hst_fresh = false;
+  h->has_next_cond = false;
+  const SweepParams P = sweep_params(h, MODE_NORMAL);
+  const FinishParams F = finish_params(h, 0, 0);
+  cudaEventRecord(ev[0], h->stream);
+  const cudaError_t le = h->disp.run(P, F, h->arrive, h->tr[0], h->tr[1], steps, (unsigned)h->cells_local, h->stream);
+  if (le != cudaSuccess) {
+    cudaGetLastError();                     // not sticky: nothing was enqueued
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+    return ADG_OK;
+  }
+  *launched = true;
+  h->sweep_index += steps;
+  cudaEventRecord(ev[1], h->stream);
+  adg_status t = cuda_check(h, cudaEventSynchronize(ev[1]), "cudaEventSynchronize");
+  float ms = 0.f;
+  if (t == ADG_OK) t = cuda_check(h, cudaEventElapsedTime(&ms, ev[0], ev[1]), "cudaEventElapsedTime");
+  out[0] = ms;
+  out[1] = 0.0;
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+  if (t != ADG_OK) return t;
+  if (flags & ADG_TIMED_NO_PULL) return ADG_OK;
+  if ((t = pull_state(h)) != ADG_OK) return t;
+  return status_from_state(h);
+}
+
 static adg_status run_steps(adg_handle* h, int steps, int flags, double* out, bool mgpu) {
   if (!h || !out || steps < 1) return ADG_ERR_CONFIG;
   if (mgpu && !h->comm) return fail(h, ADG_ERR_CONFIG, "adg_run_timed_mgpu needs adg_nccl_init");
@@ -1160,6 +1313,13 @@ static adg_status run_steps(adg_handle* h, int steps, int flags, double* out, bo
     return fail(h, ADG_ERR_CONFIG, "adg_run_timed needs a primed driver (run one step first)");
   const bool exchange = mgpu && (h->comm_world > 1 || h->cfg.halo_mode == 1);
   const bool step_ev = (flags & ADG_TIMED_KERNEL_EVENTS) != 0;
+  if (!mgpu && !step_ev && h->disp.run && h->opt_graph && h->opt_persistent && !straightforward(h) &&
+      h->cfg.world == 1 && h->cfg.halo_mode == 0 && !h->lim) {
+    // kernels that have it: the steps as ONE cooperative launch (no graph, no per-step launches)
+    bool launched = false;
+    const adg_status ps = run_persistent(h, steps, flags, out, &launched);
+    if (launched || ps != ADG_OK) return ps;
+  }
   std::vector<cudaEvent_t> ev(step_ev ? 4 * (size_t)steps + 2 : 2, nullptr);
   auto destroy_events = [&] {
     for (cudaEvent_t e : ev)
@@ -1214,6 +1374,10 @@ static adg_status run_steps(adg_handle* h, int steps, int flags, double* out, bo
       CUDA_TRY(h, record(3 + 4 * (size_t)i));
       if (r != ADG_OK) break;
       CUDA_TRY(h, record(4 + 4 * (size_t)i));
+      // the time control of this step (finish_kernel, or the sweep's last CTA) sets the
+      // condition of the next step's rerun node
+      h->has_next_cond = cond && i + 1 < steps;
+      if (h->has_next_cond) h->next_cond = hc[i + 1];
       if (exchange) {
         r = enqueue_halo(h, adg_trace_parity(h));
         if (r == ADG_OK) r = adg_phase_sweep_part(h, ADG_PART_INTERIOR);
@@ -1230,8 +1394,6 @@ static adg_status run_steps(adg_handle* h, int steps, int flags, double* out, bo
         const ncclResult_t nr = nccl_api().allReduce(h->st, h->st, 2, ncclInt64, ncclMax, h->comm, h->stream);
         if (nr != ncclSuccess) return fail(h, ADG_ERR_RUNTIME, nccl_api().errorString(nr));
       }
-      h->has_next_cond = cond && i + 1 < steps;
-      if (h->has_next_cond) h->next_cond = hc[i + 1];
       r = adg_phase_finish(h);
       h->has_next_cond = false;
     }
@@ -1519,6 +1681,8 @@ adg_status adg_set_option(adg_handle* h, int option, int value) {
   switch (option) {
     case ADG_OPT_GRAPH: h->opt_graph = value ? 1 : 0; return ADG_OK;
     case ADG_OPT_COND_RERUN: h->opt_cond_rerun = value ? 1 : 0; return ADG_OK;
+    case ADG_OPT_FUSE_FINISH: h->opt_fuse_finish = value ? 1 : 0; return ADG_OK;
+    case ADG_OPT_PERSISTENT: h->opt_persistent = value ? 1 : 0; return ADG_OK;
     case ADG_OPT_HOST_CHUNKS:
       if (value < 1 || value > ADG_HOST_CHUNKS_MAX) return fail(h, ADG_ERR_CONFIG, "host chunks must be in [1, 81]");
       h->opt_host_chunks = value;

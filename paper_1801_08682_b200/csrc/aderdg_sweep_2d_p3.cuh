@@ -1,0 +1,674 @@
+// aderdg_sweep_2d_p3.cuh — the fused 2D sweep at p = 3 (BASELINE cfg 1: 27^2 cells).
+//
+// 729 cells of 16 nodes cannot fill 148 SMs: the sweep is one cell's latency, so the
+// kernel spends threads on shortening the dependent chain of a cell instead of on
+// throughput.  One CTA of 128 threads per cell:
+//   * Picard loop: thread = (node x, time level t, component pair h); lane = t | h << 2 |
+//     (x & 3) << 3, warp = x >> 2.  The flux of (x, t) is evaluated by both h lanes, lane h
+//     stores axis h (two 16-byte stores); the derivative of a component pair is eight
+//     16-byte loads + 16 FMAs; the four slices of a (node, pair) sit in four adjacent
+//     lanes, so the time contraction is eight width-4 shuffles + 8 FMAs.  Slab layout
+//     [t][axis][x][c] with strides 132 / 66 / 4 / 1: the eight lanes of a quarter-warp hit
+//     eight distinct 16-byte bank groups on every store and load.
+//   * one barrier per Picard iteration: the flux slabs and the vote words alternate
+//     between two buffers; the convergence vote of iteration i rides on the barrier that
+//     publishes the flux of iteration i + 1, which is also the final flux of the tail when
+//     the vote says stop.  The admissibility / lambda / |Q| reductions of the prologue ride
+//     on the first of these barriers.
+//   * tail in two barriers: fbar by (axis, x, c) threads straight from the last slab;
+//     then warps 0-1 do the volume integral and qbar while warps 2-3 evaluate the Rusanov
+//     speeds of all 64 space-time trace nodes at once (half-warp = face, redux max);
+//     then 128 threads project qbar / fbar onto the four faces and write the records.
+//   * every global read of the prologue (time-control words, Q, D, 4d face records) is
+//     issued before the first use.
+//   * optional fused time control (FusedFinish): the last CTA to arrive runs finish_body,
+//     which removes the finish launch from the step (single GPU, fused driver).
+// Arithmetic (operation order, FMA shapes, exact-rounded decisions) is that of the generic
+// kernel (aderdg_kernels.cuh), which this kernel replaces for (Euler, d = 2, p = 3, periodic,
+// fused driver).
+//
+// Reference (src/ = /root/reference/pkg/src/aderdg/): kernels.py:68-229, scheduler.py:370-449.
+#pragma once
+#include "aderdg_kernels.cuh"
+
+namespace adg {
+
+// tools/cta_timeline.py (A/B build with -DADG_2P3_TIMING): thread 0 of every CTA stamps
+// %clock64 at the phase boundaries and %globaltimer at entry / exit into P.sm_scratch
+#ifdef ADG_2P3_TIMING
+#define ADG_TSTAMP(i)                                                                   \
+  do {                                                                                  \
+    if (threadIdx.x == 0 && P.sm_scratch != nullptr)                                    \
+      P.sm_scratch[(blockIdx.x) * 32 + (i)] = (double)clock64();                        \
+  } while (0)
+#define ADG_GSTAMP(i)                                                                   \
+  do {                                                                                  \
+    if (threadIdx.x == 0 && P.sm_scratch != nullptr) {                                  \
+      unsigned long long gt_;                                                           \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_));                           \
+      P.sm_scratch[(blockIdx.x) * 32 + (i)] = (double)gt_;                              \
+    }                                                                                   \
+  } while (0)
+#define ADG_PSTAMP(i)                                                                   \
+  do {                                                                                  \
+    if (ptid == 0 && P.sm_scratch != nullptr)                                           \
+      P.sm_scratch[(blockIdx.x) * 32 + (i)] = (double)clock64();                        \
+  } while (0)
+#define ADG_BSTAMP(i)                                  \
+  do {                                                 \
+    if (ts != nullptr) ts[i] = (double)clock64();      \
+  } while (0)
+#else
+#define ADG_TSTAMP(i) ((void)0)
+#define ADG_GSTAMP(i) ((void)0)
+#define ADG_BSTAMP(i) ((void)0)
+#define ADG_PSTAMP(i) ((void)0)
+#endif
+
+struct Shape2P3 {
+  static constexpr int DIM = 2, M = 4, NQ = 4, NS = 16, NF = 4;
+  static constexpr int THREADS = 128, NWARPS = 4, MINB = 5;
+  static constexpr int REC = 2 * NF * M + 2;
+  static constexpr int PW = 2;                   // Picard warps
+  // flux slab [t][axis][i0][i1][c] (doubles): row stride 18 and time stride 148 put the eight
+  // lanes of a quarter-warp (4 time levels x 2 rows) on eight distinct 16-byte bank groups in
+  // every store and load of the Picard loop
+  static constexpr int RS = NQ * M + 2;          // row (i0) stride
+  static constexpr int AS = NQ * RS;             // axis stride
+  static constexpr int TS = 2 * AS + 4;          // time-level stride
+  static constexpr int SLAB = NQ * TS;
+  static constexpr int XS = NQ * M + 2;          // exchange buffer [i1][i0][t][c]: i0 stride
+  // shared memory (doubles)
+  static constexpr int OFF_Q = 0;                        // [x][c]
+  static constexpr int OFF_FACE = OFF_Q + NS * M;        // signed F* [f][y][c]
+  static constexpr int OFF_SLAB = OFF_FACE + 2 * DIM * NF * M;   // two flux slabs
+  static constexpr int OFF_QT = OFF_SLAB + 2 * SLAB;     // final q [t][x][c]
+  static constexpr int OFF_FB = OFF_QT + NQ * NS * M;    // fbar [a][x][c]
+  static constexpr int OFF_QBAR = OFF_FB + DIM * NS * M; // qbar [x][c]
+  static constexpr int OFF_DV = OFF_QBAR + NS * M;       // divergence exchange of the Picard loop
+  static constexpr int OFF_RED = OFF_DV + NQ * NQ * XS;  // per-warp words, s_max, votes, outcome
+  static constexpr int R_RED = 2 * PW + 2 * DIM + 6;
+  static constexpr int TOTAL = OFF_RED + R_RED;
+  static constexpr size_t SMEM_BYTES = sizeof(double) * TOTAL;
+};
+
+// time control fused into the sweep launch: the last CTA to arrive runs finish_body
+struct FusedFinish {
+  FinishParams F;
+  unsigned* arrive;       // zero between launches
+  int on;
+};
+
+// max of 64-bit patterns over the lanes of `mask` (see warp_max_u64)
+__device__ __forceinline__ unsigned long long group_max_u64(unsigned mask, unsigned long long v) {
+  const unsigned hi = (unsigned)(v >> 32), lo = (unsigned)v;
+  const unsigned mh = __reduce_max_sync(mask, hi);
+  const unsigned ml = __reduce_max_sync(mask, hi == mh ? lo : 0u);
+  return ((unsigned long long)mh << 32) | ml;
+}
+
+// barrier of the two Picard warps (warps 2-3 wait at the CTA barrier behind the loop)
+__device__ __forceinline__ void picard_barrier_2p3() {
+#ifdef ADG_DEBUG_CHECKS
+  unsigned t;
+  asm volatile("mov.u32 %0, %%clock;" : "=r"(t));
+  unsigned x = t ^ ((threadIdx.x >> 5) * 0x9e3779b9u) ^ (blockIdx.x * 0x85ebca6bu);
+  x ^= x >> 13;
+  x *= 0xc2b2ae35u;
+  x ^= x >> 16;
+  if ((x & 3u) == 0u) __nanosleep(x >> 24);
+#endif
+  asm volatile("bar.sync 1, 64;" ::: "memory");
+}
+
+// one pass over the cells: what a sweep launch reads from SweepParams, as values, so that the
+// multi-step kernel below can change them from step to step
+struct Pass2P3 {
+  int mode, sweep;
+  const double* tr_in;
+  double* tr_out;
+};
+
+// The CTA's ticket on its SM: thread 0 takes the next number of a per-SM counter.  The
+// parity of the ticket picks the pair of warps that runs the Picard loop (sweep_2d_p3_body),
+// so that the CTAs resident on an SM alternate between the SM's schedulers.
+__device__ __forceinline__ unsigned sm_ticket_2p3(const SweepParams& P) {
+  unsigned ticket = 0u;
+  if (threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    ticket = atomicAdd(P.sm_ticket + smid, 1u);
+  }
+  return ticket;
+}
+
+__device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pass2P3& W, const long long cell,
+                                                 const unsigned ticket, double* smem) {
+  using S = Shape2P3;
+  using PDE = EulerPDE<2>;
+  constexpr int DIM = 2, M = 4, NQ = 4, NS = 16, NF = 4, REC = S::REC, NW = S::NWARPS;
+  constexpr int TS = S::TS, AS = S::AS, RS = S::RS, XS = S::XS, PW = S::PW;
+  constexpr unsigned FULL = 0xffffffffu;
+
+  double* sQ = smem + S::OFF_Q;
+  double* sFace = smem + S::OFF_FACE;
+  double* sSlab = smem + S::OFF_SLAB;
+  double* sQt = smem + S::OFF_QT;
+  double* sFb = smem + S::OFF_FB;
+  double* sQbar = smem + S::OFF_QBAR;
+  double* sDv = smem + S::OFF_DV;
+  unsigned long long* sWLam = reinterpret_cast<unsigned long long*>(smem + S::OFF_RED);
+  unsigned long long* sWAm = sWLam + PW;
+  unsigned long long* sSmax = sWAm + PW;                               // [2 * DIM]
+  unsigned* sWOk = reinterpret_cast<unsigned*>(sSmax + 2 * DIM);       // [PW]
+  unsigned* sVote = sWOk + PW;                                         // [2][PW], then outcome words
+  unsigned* sOutW = sVote + 2 * PW;                                    // outcome, iterations, slab, warp pair
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  DevState* st = P.st;
+  const int mode = W.mode;
+  const bool corr = mode_corrects(mode);
+  const long long gcell = cell + P.cell_offset;
+  const int plane = (int)(cell / P.plane_cells);
+  const int rest = (int)(cell % P.plane_cells);
+  const long long own_slot = (long long)(plane + 1) * P.plane_cells + rest;
+  double* Qg = P.Q + cell * (NS * M);
+  double* Dg = P.D + cell * (NS * M);
+
+  // neighbour slot across face f (periodic, or the halo slot of an x-slab)
+  auto nb_of = [&](int f) -> long long {
+    const int dir = (f & 1) ? 1 : -1;
+    if ((f >> 1) == 0) {
+      int pl = plane + dir;
+      if (!P.halo) pl = (pl + P.K) % P.K;
+      return (long long)(pl + 1) * P.plane_cells + rest;
+    }
+    const int ia = rest % P.K;
+    const int ja = (ia + dir + P.K) % P.K;
+    return (long long)(plane + 1) * P.plane_cells + rest + (ja - ia);
+  };
+
+  ADG_GSTAMP(0);
+  ADG_TSTAMP(1);
+  // ---------------- every global read of the prologue, issued before the first use ----------------
+  // (L2 loads: in the multi-step kernel other SMs rewrite these words, the neighbours' records
+  // and nothing else between two passes of this CTA, and L1 is not coherent)
+  const int st_status = __ldcg(&st->status);
+  const int st_rerun = __ldcg(&st->rerun_next);
+  const long long st_err = __ldcg(&st->reduce[1]);
+  const int st_step = __ldcg(&st->step);
+  const double scale_old = __ldcg(&st->scale_old), scale_new = __ldcg(&st->scale_new);
+  const int e = tid & 63;
+  double q_in = 0.0, d_in = 0.0;
+  double r_qm = 0.0, r_qp = 0.0, r_fm = 0.0, r_fp = 0.0, r_sm = 0.0, r_sp = 0.0;
+  if (tid < 64) {
+    q_in = __ldcg(Qg + e);
+    if (corr) d_in = __ldcg(Dg + e);
+  } else if (corr) {
+    const int f = e >> 4, yc = e & 15;
+    const double* own = W.tr_in + ((long long)f * P.slots + own_slot) * REC;
+    const double* nb = W.tr_in + ((long long)(f ^ 1) * P.slots + nb_of(f)) * REC;
+    const double* mr = (f & 1) ? own : nb;   // minus side record
+    const double* pr = (f & 1) ? nb : own;   // plus side record
+    r_sm = __ldcg(mr + 2 * NF * M); r_sp = __ldcg(pr + 2 * NF * M);
+    r_qm = __ldcg(mr + yc); r_qp = __ldcg(pr + yc);
+    r_fm = __ldcg(mr + NF * M + yc); r_fp = __ldcg(pr + NF * M + yc);
+  }
+  ADG_TSTAMP(2);   // after issuing the loads
+  if (st_status != 0) return;
+  if (mode == MODE_RERUN && !st_rerun) return;
+  if (corr && st_err != 0) return;                        // a predict pass already failed
+#ifdef ADG_DEBUG_CHECKS
+  if (corr && tid == 0) {
+    long long nbs[2 * DIM];
+    for (int f = 0; f < 2 * DIM; ++f) nbs[f] = nb_of(f);
+    debug_check_records_at<DIM>(P, W.tr_in, expected_stamp_of(mode, W.sweep, st_rerun), st, cell, gcell, own_slot,
+                                nbs, REC, 2 * NF * M);
+  }
+#endif
+
+  ADG_TSTAMP(3);   // time-control words arrived
+  const bool spike = corr && P.spike_step >= 0 && st_step + 1 == P.spike_step;
+  if (corr) {
+    // ------------- Riemann (kernels.py:147-179), time-collapsed -------------
+    if (tid >= 64) {
+      const int f = e >> 4;
+      const double alpha = rusanov_alpha(r_sm, r_sp);
+      // F* = 0.5*(fm+fp) - 0.5*alpha*(qp-qm)   (kernels.py:175)
+      const double fs = __dsub_rn(__dmul_rn(0.5, __dadd_rn(r_fm, r_fp)),
+                                  __dmul_rn(__dmul_rn(0.5, alpha), __dsub_rn(r_qp, r_qm)));
+      sFace[e] = (f & 1) ? fs : -fs;                      // plus side stores -F* (kernels.py:176-177)
+    }
+    __syncthreads();
+    // ------------- integrate_face + update (kernels.py:183-214): thread = (x, c) -------------
+    if (tid < 64) {
+      const int xx = e >> 2, c = e & 3;
+      const int idx[DIM] = {xx >> 2, xx & 3};
+      double Dx = d_in;
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) {
+        const int y = idx[1 - a];
+        const double slo = __dmul_rn(scale_old, P.ops.lift_lo[idx[a]]);
+        const double shi = __dmul_rn(scale_old, P.ops.lift_hi[idx[a]]);
+        Dx = __dsub_rn(Dx, __dmul_rn(slo, sFace[((2 * a) * NF + y) * M + c]));
+        Dx = __dsub_rn(Dx, __dmul_rn(shi, sFace[((2 * a + 1) * NF + y) * M + c]));
+      }
+      q_in = __dadd_rn(q_in, Dx);
+      if (!spike) Qg[e] = q_in;
+    }
+  }
+  if (tid < 64) sQ[e] = q_in;
+  if (tid == 0) sOutW[3] = ticket & 1u;
+  __syncthreads();
+  if (spike) {
+    // Driver._apply_spike (scheduler.py:166-178)
+    if (tid < NS) {
+      double Qx[M];
+#pragma unroll
+      for (int c = 0; c < M; ++c) Qx[c] = sQ[tid * M + c];
+      const double rho = Qx[0];
+      const double pr = pressure_exact<DIM>(Qx);
+#pragma unroll
+      for (int b = 0; b < DIM; ++b) Qx[1 + b] = __dmul_rn(Qx[1 + b], P.spike_factor);
+      double jj = __dmul_rn(Qx[1], Qx[1]);
+#pragma unroll
+      for (int b = 1; b < DIM; ++b) jj = __dadd_rn(jj, __dmul_rn(Qx[1 + b], Qx[1 + b]));
+      Qx[M - 1] = __dadd_rn(__ddiv_rn(pr, 0.4), __ddiv_rn(__dmul_rn(0.5, jj), rho));
+#pragma unroll
+      for (int c = 0; c < M; ++c) sQ[tid * M + c] = Qx[c];
+    }
+    __syncthreads();
+    if (tid < 64) Qg[e] = sQ[e];
+  }
+
+  ADG_TSTAMP(4);   // corrector done, Q published
+  // ---------------- predictor roles ----------------
+  // two Picard warps: thread = (node x, time level t), every component; lane = t |
+  // (i0 & 1) << 2 | i1 << 3, warp & 1 = i0 >> 1.  The other two warps wait at the barrier
+  // behind the loop.  Which pair works follows the CTA's ticket on its SM: the warps of a CTA
+  // sit on the SM's four schedulers by warp index, and the five CTAs of an SM would otherwise
+  // queue their Picard loops on two of them.
+  const int rot = (int)sOutW[3];
+  const int ptid = tid - 64 * rot;                        // 0..63 in the Picard warps
+  const int t = lane & 3, i0 = 2 * (warp & 1) + ((lane >> 2) & 1), i1 = lane >> 3;
+  const int x = i0 * NQ + i1;
+  unsigned* sOut = sVote + 2 * PW;                        // [0] outcome, [1] iterations, [2] final slab
+  if ((warp >> 1) == rot) {
+    const int pw = warp & 1;
+    double qf[M];                                         // q at (x, t), every component
+    {
+      const double2 a = *reinterpret_cast<const double2*>(sQ + x * M);
+      const double2 b = *reinterpret_cast<const double2*>(sQ + x * M + 2);
+      qf[0] = a.x; qf[1] = a.y; qf[2] = b.x; qf[3] = b.y;
+    }
+    const double Qn[M] = {qf[0], qf[1], qf[2], qf[3]};
+    // calc_time_step (kernels.py:216-229) / predict's finiteness check (kernels.py:80-81) and
+    // max |Q| for the Picard tolerance: the four threads of a node evaluate them (no
+    // divergence, the chains overlap the first flux); the per-warp words are read after the
+    // first barrier of the Picard loop
+    {
+      bool ok = true;
+      double lam = 0.0;
+      if (!mode_predict_only(mode)) {
+        ok = PDE::node_lambda(qf, lam, P);
+      } else {
+#pragma unroll
+        for (int c = 0; c < M; ++c) ok = ok && finite(qf[c]);
+      }
+      double am = 0.0;
+#pragma unroll
+      for (int c = 0; c < M; ++c) am = fmax(am, fabs(qf[c]));
+      const bool wok = __all_sync(FULL, ok);
+      const unsigned long long wl = warp_max_u64((unsigned long long)__double_as_longlong(ok ? lam : 0.0));
+      const unsigned long long wa = warp_max_u64((unsigned long long)__double_as_longlong(am));
+      if (lane == 0) {
+        sWOk[pw] = wok ? 1u : 0u;
+        sWLam[pw] = wl;
+        sWAm[pw] = wa;
+      }
+    }
+    ADG_PSTAMP(5);   // lambda / absmax words written
+    if (mode != MODE_SEED) {
+      // ---------------- predictor (kernels.py:68-105) ----------------
+      const double scale = (mode == MODE_RERUN) ? scale_old : scale_new;   // dt / h
+      constexpr int cap = 2 * NQ;
+      double drow0[NQ], drow1[NQ], ig[NQ];
+#pragma unroll
+      for (int j = 0; j < NQ; ++j) {
+        drow0[j] = P.ops.diff[i0][j];
+        drow1[j] = P.ops.diff[i1][j];
+        ig[j] = P.ops.integ[t][j];
+      }
+      const int rd0 = t * TS + i1 * M;                    // axis 0: node (j, i1), + RS j
+      const int rd1 = t * TS + AS + i0 * RS;              // axis 1: node (i0, j), + M j
+      const int wr = t * TS + i0 * RS + i1 * M;
+      const int xo = i1 * (NQ * XS) + i0 * XS;            // this node's slot of the exchange buffer
+      double tol = 0.0;
+      unsigned outcome = 0u;                              // 1 inadmissible / non-finite Q, 2 predictor failed
+      int iters = 0;
+      bool conv = false, bad = false;
+      int it = 0;
+      for (;; ++it) {
+        ADG_PSTAMP(16 + it);
+        double F[DIM][M];
+        PDE::flux(qf, F, P);
+        double* slab = sSlab + (it & 1) * S::SLAB;
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+          *reinterpret_cast<double2*>(slab + wr + a * AS) = make_double2(F[a][0], F[a][1]);
+          *reinterpret_cast<double2*>(slab + wr + a * AS + 2) = make_double2(F[a][2], F[a][3]);
+        }
+        // vote word: bit 0 = every thread converged in the previous iteration, bit 1 = some
+        // difference non-finite
+        const bool wc = __all_sync(FULL, conv);
+        const bool wb = __any_sync(FULL, bad);
+        if (lane == 0) sVote[(it & 1) * PW + pw] = (wc ? 1u : 0u) | (wb ? 2u : 0u);
+        if (it == 2) ADG_PSTAMP(10);
+        picard_barrier_2p3();
+        if (it == 2) ADG_PSTAMP(11);
+        if (it == 0) {
+          const unsigned long long l = sWLam[0] > sWLam[1] ? sWLam[0] : sWLam[1];
+          const unsigned long long am = sWAm[0] > sWAm[1] ? sWAm[0] : sWAm[1];
+          if (!(sWOk[0] & sWOk[1])) {
+            if (ptid == 0) report_error(st, 2 * gcell + (mode_predict_only(mode) ? 1 : 0));
+            outcome = 1u;
+            break;
+          }
+          if (!mode_predict_only(mode) && ptid == 0) atomicMax(&st->reduce[0], (long long)l);
+          tol = 1e-10 * (1.0 + __longlong_as_double((long long)am));
+        }
+        const unsigned v0 = sVote[(it & 1) * PW], v1 = sVote[(it & 1) * PW + 1];
+        if (it > 0) {
+          if ((v0 | v1) & 2u) { outcome = 2u; break; }
+          if ((v0 & v1 & 1u) || it == cap) break;
+        }
+        // divergence of the slice at this node: axis 0 then axis 1 in one chain per component
+        double dv[M];
+#pragma unroll
+        for (int c = 0; c < M; ++c) dv[c] = 0.0;
+#pragma unroll
+        for (int j = 0; j < NQ; ++j) {
+          const double2 lo = *reinterpret_cast<const double2*>(slab + rd0 + j * RS);
+          const double2 hi = *reinterpret_cast<const double2*>(slab + rd0 + j * RS + 2);
+          dv[0] = fma(drow0[j], lo.x, dv[0]); dv[1] = fma(drow0[j], lo.y, dv[1]);
+          dv[2] = fma(drow0[j], hi.x, dv[2]); dv[3] = fma(drow0[j], hi.y, dv[3]);
+        }
+#pragma unroll
+        for (int j = 0; j < NQ; ++j) {
+          const double2 lo = *reinterpret_cast<const double2*>(slab + rd1 + j * M);
+          const double2 hi = *reinterpret_cast<const double2*>(slab + rd1 + j * M + 2);
+          dv[0] = fma(drow1[j], lo.x, dv[0]); dv[1] = fma(drow1[j], lo.y, dv[1]);
+          dv[2] = fma(drow1[j], hi.x, dv[2]); dv[3] = fma(drow1[j], hi.y, dv[3]);
+        }
+        if (it == 2) ADG_PSTAMP(12);
+        // time contraction: the four slices of a node are in four lanes of one warp; they
+        // meet in the node's slot of the exchange buffer (written before, read after a
+        // __syncwarp; the next write comes behind the next Picard barrier)
+        *reinterpret_cast<double2*>(sDv + xo + t * M) = make_double2(dv[0], dv[1]);
+        *reinterpret_cast<double2*>(sDv + xo + t * M + 2) = make_double2(dv[2], dv[3]);
+        __syncwarp();
+        double acc[M];
+#pragma unroll
+        for (int c = 0; c < M; ++c) acc[c] = 0.0;
+#pragma unroll
+        for (int k = 0; k < NQ; ++k) {
+          const double2 lo = *reinterpret_cast<const double2*>(sDv + xo + k * M);
+          const double2 hi = *reinterpret_cast<const double2*>(sDv + xo + k * M + 2);
+          acc[0] = fma(ig[k], lo.x, acc[0]); acc[1] = fma(ig[k], lo.y, acc[1]);
+          acc[2] = fma(ig[k], hi.x, acc[2]); acc[3] = fma(ig[k], hi.y, acc[3]);
+        }
+        BitMax bm;
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          const double qn = Qn[c] - scale * acc[c];
+          bm.add(fabs(qn - qf[c]));
+          qf[c] = qn;
+        }
+        conv = bm.conv(tol);
+        bad = bm.bad();
+        if (it == 2) ADG_PSTAMP(31);
+      }
+      iters = it;
+      // the slab of the last barrier holds the flux of the final iterate at every (t, axis, x, c)
+      if (outcome == 2u && ptid == 0) report_error(st, 2 * gcell + 1);
+      if (outcome == 0u) {
+        *reinterpret_cast<double2*>(sQt + t * (NS * M) + x * M) = make_double2(qf[0], qf[1]);
+        *reinterpret_cast<double2*>(sQt + t * (NS * M) + x * M + 2) = make_double2(qf[2], qf[3]);
+      }
+      if (ptid == 0) {
+        sOut[0] = outcome;
+        sOut[1] = (unsigned)iters;
+        sOut[2] = (unsigned)(it & 1);
+      }
+    }
+  }
+  __syncthreads();
+  if (mode == MODE_SEED) {
+    if (tid == 0) {
+      if (!(sWOk[0] & sWOk[1])) report_error(st, 2 * gcell + 0);
+      else atomicMax(&st->reduce[0], (long long)(sWLam[0] > sWLam[1] ? sWLam[0] : sWLam[1]));
+    }
+    return;
+  }
+  ADG_TSTAMP(6);   // Picard loop done
+  if (sOut[0] != 0u) return;
+  const double scale = (mode == MODE_RERUN) ? scale_old : scale_new;
+  const double* cur = sSlab + sOut[2] * S::SLAB;
+  const int iters = (int)sOut[1];
+
+  // ---------------- tail: fbar, volume integral, traces ----------------
+  {
+    // fbar[a][x][c] = sum_k w_k F_k (integrate_volume, kernels.py:130-143): thread = (a, x, c)
+    const int a = tid >> 6;
+    const int so = (e >> 4) * RS + (e & 15);              // (x, c) in the slab's padded node rows
+    double fb = 0.0;
+    bool badf = false;                                    // predict's check of the final flux (kernels.py:99-101)
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) {
+      const double Fk = cur[k * TS + a * AS + so];
+      badf |= !finite(Fk);
+      fb = fma(P.ops.w[k], Fk, fb);
+    }
+    sFb[a * (NS * M) + e] = fb;
+    if (__syncthreads_or(badf)) {
+      if (tid == 0) report_error(st, 2 * gcell + 1);
+      return;
+    }
+  }
+  if (tid == 0) {
+    atomicAdd((unsigned long long*)&st->picard_iters, (unsigned long long)iters);
+    atomicAdd((unsigned long long*)&st->predicts, 1ull);
+    atomicAdd((unsigned long long*)&st->hist[iters < HIST_BINS ? iters : HIST_BINS - 1], 1ull);
+  }
+  ADG_TSTAMP(7);   // fbar published
+  if (tid < 64) {
+    // volume integral, thread = (x, c); then qbar = sum_t w_t q
+    const int xx = e >> 2, c = e & 3;
+    const int j0 = xx >> 2, j1 = xx & 3;
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) s = fma(P.ops.kvol[j0][j], sFb[(j * NQ + j1) * M + c], s);
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) s = fma(P.ops.kvol[j1][j], sFb[NS * M + (j0 * NQ + j) * M + c], s);
+    Dg[e] = s * scale;
+    double v = 0.0;
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) v = fma(P.ops.w[k], sQt[k * (NS * M) + e], v);
+    sQbar[e] = v;
+  } else {
+    // s_max over the space-time trace of q, per face (Rusanov alpha input, kernels.py:107-128):
+    // thread = (face f, face node y, time level): half-warp = face
+    const int f = e >> 4, y = (e >> 2) & 3, tt = e & 3, a = f >> 1;
+    const double* vec = (f & 1) ? P.ops.right : P.ops.left;
+    const int xb = (a == 0) ? y : NQ * y, sta = (a == 0) ? NQ : 1;
+    double qs[M];
+#pragma unroll
+    for (int c = 0; c < M; ++c) qs[c] = 0.0;
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) {
+      const double vi = vec[i];
+      const double* src = sQt + tt * (NS * M) + (xb + i * sta) * M;
+      const double2 lo = *reinterpret_cast<const double2*>(src);
+      const double2 hi = *reinterpret_cast<const double2*>(src + 2);
+      qs[0] = fma(vi, lo.x, qs[0]); qs[1] = fma(vi, lo.y, qs[1]);
+      qs[2] = fma(vi, hi.x, qs[2]); qs[3] = fma(vi, hi.y, qs[3]);
+    }
+    // PDE::trace_speed(qs, a) with the axis' momentum selected by value (no indexed array)
+    const double pr = pressure_exact<DIM>(qs);
+    const double qa[2] = {qs[0], a ? qs[2] : qs[1]};
+    const double sp = speed_exact<DIM>(qa, 0, pr);
+    const unsigned half = (lane & 16) ? 0xffff0000u : 0x0000ffffu;
+    const unsigned long long m = group_max_u64(half, (unsigned long long)__double_as_longlong(sp));
+    if ((lane & 15) == 0) sSmax[f] = m;
+  }
+  __syncthreads();
+  ADG_TSTAMP(8);   // D stored, qbar / s_max published
+  {
+    // face records: threads 0-63 project qbar, threads 64-127 project fbar; item = (f, y, c)
+    const int f = e >> 4, yc = e & 15, y = yc >> 2, c = yc & 3, a = f >> 1;
+    const double* vec = (f & 1) ? P.ops.right : P.ops.left;
+    const int xb = (a == 0) ? y : NQ * y, sta = (a == 0) ? NQ : 1;
+    const double* src = (tid < 64) ? sQbar : sFb + a * (NS * M);
+    double v = 0.0;
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) v = fma(vec[i], src[(xb + i * sta) * M + c], v);
+    double* rec = W.tr_out + ((long long)f * P.slots + own_slot) * REC;
+    rec[(tid < 64 ? 0 : NF * M) + yc] = v;
+  }
+  if (tid < 2 * DIM) {
+    double* rec = W.tr_out + ((long long)tid * P.slots + own_slot) * REC;
+    rec[2 * NF * M] = __longlong_as_double((long long)sSmax[tid]);
+    rec[2 * NF * M + 1] = record_stamp_of(mode, W.sweep);
+  }
+  ADG_TSTAMP(9);     // records issued
+#ifdef ADG_2P3_TIMING
+  if (tid == 0 && P.sm_scratch != nullptr) P.sm_scratch[blockIdx.x * 32 + 13] = (double)iters;
+#else
+  (void)iters;
+#endif
+}
+
+__global__ void __launch_bounds__(Shape2P3::THREADS, Shape2P3::MINB)
+sweep_kernel_2d_p3(const SweepParams P, const FusedFinish X) {
+  extern __shared__ __align__(16) double smem[];
+  ADG_DEBUG_POISON();
+  const Pass2P3 W{P.mode, P.sweep, P.tr_in, P.tr_out};
+  sweep_2d_p3_body(P, W, sweep_cell(P), sm_ticket_2p3(P), smem);
+  if (X.on) {
+    // the last CTA to arrive has every CTA's reductions behind its fence: it is the time control
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      ADG_TSTAMP(10);
+      __threadfence();
+      ADG_TSTAMP(11);
+      const unsigned n = atomicAdd(X.arrive, 1u);
+#ifdef ADG_2P3_TIMING
+      if (P.sm_scratch != nullptr) P.sm_scratch[blockIdx.x * 32 + 14] = (double)n;
+#endif
+      ADG_TSTAMP(12);
+      if (n == gridDim.x - 1) {
+        __threadfence();
+        *X.arrive = 0u;
+        const int rerun = finish_body(X.F);
+        if (X.F.has_cond) cudaGraphSetConditional(X.F.cond, rerun ? 1u : 0u);
+      }
+    }
+  }
+  ADG_GSTAMP(15);
+}
+
+// ---------------------------------------------------------------------------
+// Multi-step launch: `steps` realisation steps of the fused driver (scheduler.py:190-226:
+// rerun pass when the time control asked for one, sweep, time control) in ONE cooperative
+// kernel.  At 729 cells a step's launches cost as much as its arithmetic; here the steps are
+// separated by a grid barrier (arrival counter + generation word) whose last arriver runs the
+// time control before it releases the others.  CTA b owns the cells b, b + grid, ... in every
+// pass; what other CTAs write between two passes (neighbour records, DevState) is read
+// through L2.  Results are bitwise those of the per-step launches.
+struct RunParams2P3 {
+  FinishParams F;
+  unsigned* sync;           // [0] arrival counter (zero between barriers), [1] generation
+  double* tr[2];            // the two record parities
+  int steps;
+};
+
+template <class LastFn>
+__device__ __forceinline__ void grid_barrier_2p3(unsigned* sync, unsigned& gen, LastFn last, double* ts = nullptr) {
+  (void)ts;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ADG_BSTAMP(26);
+    __threadfence();
+    ADG_BSTAMP(27);
+    const unsigned n = atomicAdd(&sync[0], 1u);
+    ADG_BSTAMP(28);
+    if (n == gridDim.x - 1) {
+      __threadfence();
+      sync[0] = 0u;
+      last();
+      ADG_BSTAMP(29);
+      __threadfence();
+      atomicExch(&sync[1], gen + 1u);                        // release
+      ADG_BSTAMP(30);
+    } else {
+      // acquire loads: what the CTA reads after the barrier is ordered behind the release
+      unsigned g;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(&sync[1]) : "memory");
+      } while (g == gen);
+      ADG_BSTAMP(29);
+      ADG_BSTAMP(30);
+    }
+#ifdef ADG_2P3_TIMING
+    if (ts != nullptr) {
+      ts[14] = (double)n;
+      unsigned long long gt_;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_));
+      ts[15] = (double)gt_;
+    }
+#endif
+  }
+  gen += 1u;
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(Shape2P3::THREADS, Shape2P3::MINB)
+run_kernel_2d_p3(const SweepParams P, const RunParams2P3 R) {
+  extern __shared__ __align__(16) double smem[];
+  ADG_DEBUG_POISON();
+  volatile DevState* vst = P.st;
+  const long long cells = (long long)P.planes_local * P.plane_cells;
+  // every CTA reads the generation before any barrier of this launch can complete
+  unsigned gen = *reinterpret_cast<volatile unsigned*>(&R.sync[1]);
+  const unsigned ticket = sm_ticket_2p3(P);
+#ifdef ADG_DEBUG_CHECKS
+  const long long first = (long long)(gridDim.x - 1 - blockIdx.x);   // reversed cell order (sweep_cell)
+#else
+  const long long first = (long long)blockIdx.x;
+#endif
+  for (int s = 0; s < R.steps; ++s) {
+    if (vst->status != 0) break;                               // uniform: written by the time control only
+    const int sweep = P.sweep + s;
+    const double* tr_in = R.tr[sweep & 1];
+    if (vst->rerun_next) {                                     // _maybe_rerun (scheduler.py:446-449)
+      const Pass2P3 W{MODE_RERUN, sweep, tr_in, R.tr[sweep & 1]};
+      for (long long cell = first; cell < cells; cell += gridDim.x) {
+        sweep_2d_p3_body(P, W, cell, ticket, smem);
+        __syncthreads();
+      }
+      grid_barrier_2p3(R.sync, gen, [] {});
+    }
+    const Pass2P3 W{MODE_NORMAL, sweep, tr_in, R.tr[(sweep & 1) ^ 1]};
+    for (long long cell = first; cell < cells; cell += gridDim.x) {
+      sweep_2d_p3_body(P, W, cell, ticket, smem);
+      __syncthreads();
+    }
+#ifdef ADG_2P3_TIMING
+    grid_barrier_2p3(R.sync, gen, [&] { finish_body(R.F); }, P.sm_scratch ? P.sm_scratch + blockIdx.x * 32 : nullptr);
+#else
+    grid_barrier_2p3(R.sync, gen, [&] { finish_body(R.F); });
+#endif
+  }
+}
+
+}  // namespace adg

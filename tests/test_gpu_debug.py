@@ -56,7 +56,9 @@ CASES = [
     dict(d=3, L=1, p=7, steps=2),                              # p=7 kernel (TMEM + smem state, DMMA tiles)
     dict(d=3, L=1, p=6, steps=2),                              # sweep_kernel_ho, TMEM time line
     dict(d=3, L=1, p=9, steps=2),                              # p=9 kernel (TMEM + smem state, line engine)
-    dict(d=2, L=2, p=3, steps=5, spike_step=3),                # generic 2D kernel + speed spike
+    dict(d=2, L=2, p=3, steps=5, spike_step=3),                # 2D p=3 kernel (fused time control) + speed spike
+    dict(d=2, L=2, p=3, steps=4, inject_rerun=True),           # 2D p=3 kernel, rerun passes
+    dict(d=2, L=2, p=2, steps=4),                              # generic 2D kernel
     dict(d=3, L=1, p=4, steps=3),                              # generic 3D kernel
     dict(d=3, L=2, p=3, steps=4, mode="straightforward"),      # straightforward passes
     dict(d=3, L=1, p=3, steps=3, scen="gauss"),                # advection plug-in

@@ -76,6 +76,7 @@ def test_gpu_matches_reference_golden(cuda_ok, name):
 
 
 @pytest.mark.parametrize("d,L,p,steps,seed", [(3, 2, 3, 3, 7), (2, 2, 4, 6, 3), (3, 1, 4, 4, 11),
+                                              (2, 3, 3, 6, 12), (2, 1, 3, 5, 13),
                                               (2, 2, 7, 3, 5), (3, 2, 5, 2, 1), (3, 1, 6, 3, 2),
                                               (3, 1, 7, 3, 4), (3, 1, 8, 2, 6), (3, 1, 9, 2, 8)])
 def test_gpu_matches_oracle_random_seeds(cuda_ok, d, L, p, steps, seed):
@@ -371,6 +372,32 @@ def test_run_timed_graph_equals_device_run(cuda_ok, flags, d, L, p, steps, kw):
     c.run(steps=steps)                       # adg_run's default: graph chunks
     assert np.array_equal(c.grid.Q, b.grid.Q)
     assert [r["reruns"] for r in c.step_records] == [r["reruns"] for r in b.step_records]
+
+
+@pytest.mark.parametrize("L,steps,kw", [(3, 8, {}), (2, 6, {"inject_rerun": True}), (2, 8, {"spike_step": 3}),
+                                        (1, 5, {}), (4, 4, {}), (4, 4, {"inject_rerun": True})])
+def test_fused_time_control_equals_finish_launch(cuda_ok, L, steps, kw):
+    """2D p = 3 (sweep_kernel_2d_p3 / run_kernel_2d_p3): the multi-step cooperative launch
+    (default), the step graph with the time control run by the last CTA of each sweep launch,
+    the same with a separate finish launch (ADG_OPT_FUSE_FINISH 0), and the plain stream
+    launches: state, step records and counters bitwise."""
+    from paper_1801_08682_b200 import _lib
+    Q0 = scenarios.build("bump", 2, L, 3, seed=6, noise=1e-2)
+    runs = []
+    for fuse, graph, pers in ((1, 1, 1), (1, 1, 0), (0, 1, 0), (1, 0, 0), (0, 0, 0)):
+        drv = make_driver(Q0, 2, L, 3, kw)
+        drv.handle.call("adg_set_option", _lib.ADG_OPT_FUSE_FINISH, fuse)
+        drv.handle.call("adg_set_option", _lib.ADG_OPT_GRAPH, graph)
+        drv.handle.call("adg_set_option", _lib.ADG_OPT_PERSISTENT, pers)
+        drv.run(steps=steps)
+        recs = [(r["step"], r["reruns"], r["T"], r["dt_old"], r["dt_new"], r["dt_adm"], r["picard_iters"],
+                 r["predicts"]) for r in drv.step_records]
+        runs.append((np.array(drv.grid.Q), recs, drv.sweep_count, drv.rerun_count))
+        drv.close()
+    for other in runs[1:]:
+        assert np.array_equal(runs[0][0], other[0])
+        assert runs[0][1:] == other[1:]
+    assert len(runs[0][1]) == steps
 
 
 HIGH = [n for n in golden_names() if n.endswith("_pre") or n.startswith("fourier_d3_L2")]
