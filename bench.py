@@ -434,7 +434,11 @@ def main():
     # per-step algorithmic flops of this rank: K steps of corrector work + the counted
     # Picard iterations / predicts of those steps
     flops_total = roofline.flops_step(d, p, local_cells * K, iters, preds)
-    share = (rep_kern / sum(rep_seg)) if rep_kern > 0 else None
+    # 2D p = 3 on one GPU (cfg 1): each timed segment is ONE cooperative launch of
+    # run_kernel_2d_p3 (sweeps, grid barriers and time control of all its steps): the kernel's
+    # duration is the segment's, and the per-launch replay (the step graph) does not describe it
+    multi_step = world == 1 and d == 2 and p == 3 and args.mode == "fused"
+    share = (rep_kern / sum(rep_seg)) if (rep_kern > 0 and not multi_step) else None
     own_ms_per_step = sum(seg_ms) / K
     kern_ms_per_step = (share * own_ms_per_step) if share else own_ms_per_step
     achieved_tf = (flops_total / K) / (kern_ms_per_step * 1e-3) / 1e12
@@ -507,9 +511,7 @@ def main():
     # conditional node fires (a segment's first step, whose condition defaults to 1, and
     # steps after a finish that asked for a rerun)
     sweeps = 2 if (world > 1 and drv.lay.planes_local > 2) else 1
-    # 2D p = 3 on one GPU: the sweep's last CTA is the time control (no finish launch)
-    fused_tc = world == 1 and cfgd["d"] == 2 and cfgd["p"] == 3
-    launches = timed_rerun_launches + K * (sweeps + (0 if fused_tc else 1))
+    launches = len(seg_ms) if multi_step else timed_rerun_launches + K * (sweeps + 1)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -534,10 +536,13 @@ def main():
             "roofline": {"bound": "tensor", "datapath": "fp64 (DMMA m8n8k4 + DFMA)",
                          "achieved": achieved_tf, "peak": peak_tf,
                          "unit": "TFLOP/s", "frac": achieved_tf / peak_tf, "traffic": traffic,
-                         "kernel": f"sweep kernel d={d} n={p + 1} ({args.mode}: all sweep passes of the step)",
+                         "kernel": ("run_kernel_2d_p3 (one cooperative launch per timed segment: the sweeps, "
+                                    "grid barriers and time control of all its steps)" if multi_step else
+                                    f"sweep kernel d={d} n={p + 1} ({args.mode}: all sweep passes of the step)"),
                          "kernel_ms_per_step": kern_ms_per_step,
                          "kernel_share_of_step": share,
-                         "kernel_timing": ("timed steps (two bracketing events per segment) x the sweep "
+                         "kernel_timing": ("two CUDA events around the launch (= the timed segment)" if multi_step
+                                           else "timed steps (two bracketing events per segment) x the sweep "
                                            "kernels' share of the step, measured in an instrumented replay of "
                                            "the same steps with CUDA events around every rerun / sweep launch"),
                          "flops_per_step_per_gpu": flops_total / K,

@@ -87,7 +87,7 @@ struct Shape2P3 {
   static constexpr int OFF_QBAR = OFF_FB + DIM * NS * M; // qbar [x][c]
   static constexpr int OFF_DV = OFF_QBAR + NS * M;       // divergence exchange of the Picard loop
   static constexpr int OFF_RED = OFF_DV + NQ * NQ * XS;  // per-warp words, s_max, votes, outcome
-  static constexpr int R_RED = 2 * PW + 2 * DIM + 6;
+  static constexpr int R_RED = 2 * PW + 2 * DIM + 12;
   static constexpr int TOTAL = OFF_RED + R_RED;
   static constexpr size_t SMEM_BYTES = sizeof(double) * TOTAL;
 };
@@ -163,6 +163,7 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
   unsigned* sWOk = reinterpret_cast<unsigned*>(sSmax + 2 * DIM);       // [PW]
   unsigned* sVote = sWOk + PW;                                         // [2][PW], then outcome words
   unsigned* sOutW = sVote + 2 * PW;                                    // outcome, iterations, slab, warp pair
+  unsigned long long* sTC = reinterpret_cast<unsigned long long*>(smem + S::OFF_RED + S::R_RED - 6);   // 5 words
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   DevState* st = P.st;
@@ -192,12 +193,17 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
   ADG_TSTAMP(1);
   // ---------------- every global read of the prologue, issued before the first use ----------------
   // (L2 loads: in the multi-step kernel other SMs rewrite these words, the neighbours' records
-  // and nothing else between two passes of this CTA, and L1 is not coherent)
-  const int st_status = __ldcg(&st->status);
-  const int st_rerun = __ldcg(&st->rerun_next);
-  const long long st_err = __ldcg(&st->reduce[1]);
-  const int st_step = __ldcg(&st->step);
-  const double scale_old = __ldcg(&st->scale_old), scale_new = __ldcg(&st->scale_new);
+  // and nothing else between two passes of this CTA, and L1 is not coherent.)  The
+  // time-control words: thread 0 alone (three 16-byte loads), handed to the CTA through shared
+  // memory at the first barrier -- 729 CTAs x 128 threads reading one L2 line is a hot spot.
+  ulonglong2 w_red = make_ulonglong2(0ull, 0ull), w_flag = w_red, w_scale = w_red;
+  if (tid == 0) {
+    static_assert(offsetof(DevState, rerun_next) % 16 == 0 && offsetof(DevState, status) == offsetof(DevState, rerun_next) + 8 &&
+                  offsetof(DevState, step) == offsetof(DevState, rerun_next) + 12, "rerun_next | rerun_this | status | step");
+    w_red = __ldcg(reinterpret_cast<const ulonglong2*>(&st->reduce[0]));
+    w_flag = __ldcg(reinterpret_cast<const ulonglong2*>(&st->rerun_next));
+    w_scale = __ldcg(reinterpret_cast<const ulonglong2*>(&st->scale_old));
+  }
   const int e = tid & 63;
   double q_in = 0.0, d_in = 0.0;
   double r_qm = 0.0, r_qp = 0.0, r_fm = 0.0, r_fp = 0.0, r_sm = 0.0, r_sp = 0.0;
@@ -215,20 +221,40 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
     r_fm = __ldcg(mr + NF * M + yc); r_fp = __ldcg(pr + NF * M + yc);
   }
   ADG_TSTAMP(2);   // after issuing the loads
-  if (st_status != 0) return;
-  if (mode == MODE_RERUN && !st_rerun) return;
-  if (corr && st_err != 0) return;                        // a predict pass already failed
+  if (tid == 0) {
+    sTC[0] = w_red.y;                                     // reduce[1]: error key of a failed pass
+    sTC[1] = w_flag.x;                                    // rerun_next | rerun_this << 32
+    sTC[2] = w_flag.y;                                    // status | step << 32
+    sTC[3] = w_scale.x;                                   // scale_old (bits)
+    sTC[4] = w_scale.y;                                   // scale_new (bits)
+    sOutW[3] = ticket & 1u;
+  }
+  int st_status = 0, st_rerun = 0, st_step = 0;
+  double scale_old = 0.0, scale_new = 0.0;
+  bool spike = false;
+  // after the first CTA barrier of the pass (no global write happens before it)
+#define ADG_2P3_TC_WORDS()                                                          \
+  do {                                                                              \
+    st_rerun = (int)(unsigned)sTC[1];                                               \
+    st_status = (int)(unsigned)sTC[2];                                              \
+    st_step = (int)(unsigned)(sTC[2] >> 32);                                        \
+    scale_old = __longlong_as_double((long long)sTC[3]);                            \
+    scale_new = __longlong_as_double((long long)sTC[4]);                            \
+    spike = corr && P.spike_step >= 0 && st_step + 1 == P.spike_step;               \
+    if (st_status != 0) return;                                                     \
+    if (mode == MODE_RERUN && !st_rerun) return;                                    \
+    if (corr && sTC[0] != 0ull) return; /* a predict pass already failed */         \
+  } while (0)
 #ifdef ADG_DEBUG_CHECKS
-  if (corr && tid == 0) {
+  if (corr && tid == 0 && (unsigned)w_flag.y == 0u && w_red.y == 0ull) {
     long long nbs[2 * DIM];
     for (int f = 0; f < 2 * DIM; ++f) nbs[f] = nb_of(f);
-    debug_check_records_at<DIM>(P, W.tr_in, expected_stamp_of(mode, W.sweep, st_rerun), st, cell, gcell, own_slot,
-                                nbs, REC, 2 * NF * M);
+    debug_check_records_at<DIM>(P, W.tr_in, expected_stamp_of(mode, W.sweep, (int)(unsigned)w_flag.x), st, cell, gcell,
+                                own_slot, nbs, REC, 2 * NF * M);
   }
 #endif
 
   ADG_TSTAMP(3);   // time-control words arrived
-  const bool spike = corr && P.spike_step >= 0 && st_step + 1 == P.spike_step;
   if (corr) {
     // ------------- Riemann (kernels.py:147-179), time-collapsed -------------
     if (tid >= 64) {
@@ -240,6 +266,7 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
       sFace[e] = (f & 1) ? fs : -fs;                      // plus side stores -F* (kernels.py:176-177)
     }
     __syncthreads();
+    ADG_2P3_TC_WORDS();
     // ------------- integrate_face + update (kernels.py:183-214): thread = (x, c) -------------
     if (tid < 64) {
       const int xx = e >> 2, c = e & 3;
@@ -258,8 +285,9 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
     }
   }
   if (tid < 64) sQ[e] = q_in;
-  if (tid == 0) sOutW[3] = ticket & 1u;
   __syncthreads();
+  if (!corr) ADG_2P3_TC_WORDS();
+#undef ADG_2P3_TC_WORDS
   if (spike) {
     // Driver._apply_spike (scheduler.py:166-178)
     if (tid < NS) {
@@ -569,8 +597,8 @@ sweep_kernel_2d_p3(const SweepParams P, const FusedFinish X) {
       if (n == gridDim.x - 1) {
         __threadfence();
         *X.arrive = 0u;
-        const int rerun = finish_body(X.F);
-        if (X.F.has_cond) cudaGraphSetConditional(X.F.cond, rerun ? 1u : 0u);
+        const unsigned fl = finish_body(X.F);
+        if (X.F.has_cond) cudaGraphSetConditional(X.F.cond, (fl & FINISH_RERUN) ? 1u : 0u);
       }
     }
   }
@@ -592,8 +620,14 @@ struct RunParams2P3 {
   int steps;
 };
 
+// The release word is generation | flags: the last arriver's `last()` returns the flags
+// (GB_RERUN: the time control asked for a rerun pass, GB_STOP: the run has a status / a pass
+// failed), every CTA gets them back without another trip to DevState.
+constexpr unsigned GB_RERUN = FINISH_RERUN, GB_STOP = FINISH_STOP, GB_GEN = GB_RERUN - 1u;
+
 template <class LastFn>
-__device__ __forceinline__ void grid_barrier_2p3(unsigned* sync, unsigned& gen, LastFn last, double* ts = nullptr) {
+__device__ __forceinline__ unsigned grid_barrier_2p3(unsigned* sync, unsigned& gen, unsigned* sflags, LastFn last,
+                                                     double* ts = nullptr) {
   (void)ts;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -605,17 +639,19 @@ __device__ __forceinline__ void grid_barrier_2p3(unsigned* sync, unsigned& gen, 
     if (n == gridDim.x - 1) {
       __threadfence();
       sync[0] = 0u;
-      last();
+      const unsigned fl = last();
       ADG_BSTAMP(29);
       __threadfence();
-      atomicExch(&sync[1], gen + 1u);                        // release
+      atomicExch(&sync[1], ((gen + 1u) & GB_GEN) | fl);      // release
+      *sflags = fl;
       ADG_BSTAMP(30);
     } else {
       // acquire loads: what the CTA reads after the barrier is ordered behind the release
       unsigned g;
       do {
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(&sync[1]) : "memory");
-      } while (g == gen);
+      } while ((g & GB_GEN) == gen);
+      *sflags = g & ~GB_GEN;
       ADG_BSTAMP(29);
       ADG_BSTAMP(30);
     }
@@ -628,46 +664,60 @@ __device__ __forceinline__ void grid_barrier_2p3(unsigned* sync, unsigned& gen, 
     }
 #endif
   }
-  gen += 1u;
+  gen = (gen + 1u) & GB_GEN;
   __syncthreads();
+  return *sflags;
 }
 
 __global__ void __launch_bounds__(Shape2P3::THREADS, Shape2P3::MINB)
 run_kernel_2d_p3(const SweepParams P, const RunParams2P3 R) {
   extern __shared__ __align__(16) double smem[];
+  __shared__ unsigned s_flags;
   ADG_DEBUG_POISON();
-  volatile DevState* vst = P.st;
   const long long cells = (long long)P.planes_local * P.plane_cells;
   // every CTA reads the generation before any barrier of this launch can complete
-  unsigned gen = *reinterpret_cast<volatile unsigned*>(&R.sync[1]);
+  unsigned gen = *reinterpret_cast<volatile unsigned*>(&R.sync[1]) & GB_GEN;
   const unsigned ticket = sm_ticket_2p3(P);
+  if (threadIdx.x == 0) {                                     // the state the launch starts from
+    const ulonglong2 w = __ldcg(reinterpret_cast<const ulonglong2*>(&P.st->rerun_next));
+    s_flags = ((unsigned)w.x ? GB_RERUN : 0u) | ((unsigned)w.y ? GB_STOP : 0u);
+  }
+  __syncthreads();
+  unsigned flags = s_flags;
 #ifdef ADG_DEBUG_CHECKS
   const long long first = (long long)(gridDim.x - 1 - blockIdx.x);   // reversed cell order (sweep_cell)
 #else
   const long long first = (long long)blockIdx.x;
 #endif
+#ifdef ADG_2P3_TIMING
+  double* ts = P.sm_scratch ? P.sm_scratch + blockIdx.x * 32 : nullptr;
+#else
+  double* ts = nullptr;
+#endif
   for (int s = 0; s < R.steps; ++s) {
-    if (vst->status != 0) break;                               // uniform: written by the time control only
+    if (flags & GB_STOP) break;                                // uniform: the release word of the last barrier
     const int sweep = P.sweep + s;
     const double* tr_in = R.tr[sweep & 1];
-    if (vst->rerun_next) {                                     // _maybe_rerun (scheduler.py:446-449)
+    bool skip = false;
+    if (flags & GB_RERUN) {                                    // _maybe_rerun (scheduler.py:446-449)
       const Pass2P3 W{MODE_RERUN, sweep, tr_in, R.tr[sweep & 1]};
       for (long long cell = first; cell < cells; cell += gridDim.x) {
         sweep_2d_p3_body(P, W, cell, ticket, smem);
         __syncthreads();
       }
-      grid_barrier_2p3(R.sync, gen, [] {});
+      // a failed predict of the rerun pass (error key in reduce[1]) cancels the sweep
+      skip = (grid_barrier_2p3(R.sync, gen, &s_flags, [&]() -> unsigned {
+                return __ldcg(&P.st->reduce[1]) != 0 ? GB_STOP : 0u;
+              }) & GB_STOP) != 0u;
     }
-    const Pass2P3 W{MODE_NORMAL, sweep, tr_in, R.tr[(sweep & 1) ^ 1]};
-    for (long long cell = first; cell < cells; cell += gridDim.x) {
-      sweep_2d_p3_body(P, W, cell, ticket, smem);
-      __syncthreads();
+    if (!skip) {
+      const Pass2P3 W{MODE_NORMAL, sweep, tr_in, R.tr[(sweep & 1) ^ 1]};
+      for (long long cell = first; cell < cells; cell += gridDim.x) {
+        sweep_2d_p3_body(P, W, cell, ticket, smem);
+        __syncthreads();
+      }
     }
-#ifdef ADG_2P3_TIMING
-    grid_barrier_2p3(R.sync, gen, [&] { finish_body(R.F); }, P.sm_scratch ? P.sm_scratch + blockIdx.x * 32 : nullptr);
-#else
-    grid_barrier_2p3(R.sync, gen, [&] { finish_body(R.F); });
-#endif
+    flags = grid_barrier_2p3(R.sync, gen, &s_flags, [&]() -> unsigned { return finish_body(R.F); }, ts);
   }
 }
 
