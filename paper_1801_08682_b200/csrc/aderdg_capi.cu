@@ -451,15 +451,13 @@ struct adg_handle {
   int opt_cond_rerun = 1;              // ADG_OPT_COND_RERUN: rerun pass as a conditional graph node
   int opt_fuse_finish = 1;             // ADG_OPT_FUSE_FINISH: time control inside the sweep launch (kernels that have it)
   int opt_persistent = 1;              // ADG_OPT_PERSISTENT: whole step sequences in one cooperative launch
-  unsigned* arrive = nullptr;          // [0] CTA arrival counter (fused time control, grid barrier), [1] generation,
-                                       // [2..] one ticket counter per %smid value (2D p = 3 kernel)
+  unsigned* arrive = nullptr;          // [0] CTA arrival counter (fused time control, grid barrier), [1] generation
   bool finish_fused = false;           // the sweep in flight carries the time control of its step
   int opt_host_chunks = 16;            // ADG_OPT_HOST_CHUNKS: wave-aligned chunks of adg_step_host
                                        // (cfg 2: 16 -> 1.526 ms, 9 -> 1.557, 23 -> 1.784)
 };
 
 constexpr int ADG_HOST_CHUNKS_MAX = 81;
-constexpr int ADG_SMID_MAX = 1024;           // bound of %nsmid on every device this library targets
 constexpr int ADG_TIMED_NO_PULL = 1 << 16;   // internal adg_run_timed_ex flag: adg_run's graph chunks
 
 static adg_status fail(adg_handle* h, adg_status code, const std::string& msg) {
@@ -518,7 +516,6 @@ static SweepParams sweep_params(adg_handle* h, int mode) {
   P.lim_cur = h->lim ? h->lim_prev[h->sweep_index & 1] : nullptr;
   P.lim_lam = h->lim ? h->lim_lam : nullptr;
   P.sm_scratch = h->sm_scratch;
-  P.sm_ticket = h->arrive + 2;
   P.spike_step = h->cfg.spike_step;
   P.p = h->cfg.p;
   P.h = h->h;
@@ -718,8 +715,8 @@ adg_status adg_create(const adg_config* cfg, adg_handle** out) {
   CUDA_TRY(h, cudaMalloc(&h->tr[1], tr_bytes));
   CUDA_TRY(h, cudaMalloc(&h->st, sizeof(DevState)));
   CUDA_TRY(h, cudaMalloc(&h->recs, sizeof(StepRecord) * h->rec_cap));
-  CUDA_TRY(h, cudaMalloc(&h->arrive, (2 + ADG_SMID_MAX) * sizeof(unsigned)));
-  CUDA_TRY(h, cudaMemsetAsync(h->arrive, 0, (2 + ADG_SMID_MAX) * sizeof(unsigned), h->stream));
+  CUDA_TRY(h, cudaMalloc(&h->arrive, 2 * sizeof(unsigned)));
+  CUDA_TRY(h, cudaMemsetAsync(h->arrive, 0, 2 * sizeof(unsigned), h->stream));
   if (c.d == 3 && c.p == 9 && c.system == 0) {     // sweep_kernel_p9: one slot per %smid value (one CTA per SM)
     unsigned* d_n = nullptr;
     unsigned nsm = 0;

@@ -51,7 +51,7 @@ namespace adg {
   } while (0)
 #define ADG_PSTAMP(i)                                                                   \
   do {                                                                                  \
-    if (ptid == 0 && P.sm_scratch != nullptr)                                           \
+    if (threadIdx.x == 0 && P.sm_scratch != nullptr)                                     \
       P.sm_scratch[(blockIdx.x) * 32 + (i)] = (double)clock64();                        \
   } while (0)
 #define ADG_BSTAMP(i)                                  \
@@ -129,21 +129,8 @@ struct Pass2P3 {
   double* tr_out;
 };
 
-// The CTA's ticket on its SM: thread 0 takes the next number of a per-SM counter.  The
-// parity of the ticket picks the pair of warps that runs the Picard loop (sweep_2d_p3_body),
-// so that the CTAs resident on an SM alternate between the SM's schedulers.
-__device__ __forceinline__ unsigned sm_ticket_2p3(const SweepParams& P) {
-  unsigned ticket = 0u;
-  if (threadIdx.x == 0) {
-    unsigned smid;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    ticket = atomicAdd(P.sm_ticket + smid, 1u);
-  }
-  return ticket;
-}
-
 __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pass2P3& W, const long long cell,
-                                                 const unsigned ticket, double* smem) {
+                                                 double* smem) {
   using S = Shape2P3;
   using PDE = EulerPDE<2>;
   constexpr int DIM = 2, M = 4, NQ = 4, NS = 16, NF = 4, REC = S::REC, NW = S::NWARPS;
@@ -162,7 +149,6 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
   unsigned long long* sSmax = sWAm + PW;                               // [2 * DIM]
   unsigned* sWOk = reinterpret_cast<unsigned*>(sSmax + 2 * DIM);       // [PW]
   unsigned* sVote = sWOk + PW;                                         // [2][PW], then outcome words
-  unsigned* sOutW = sVote + 2 * PW;                                    // outcome, iterations, slab, warp pair
   unsigned long long* sTC = reinterpret_cast<unsigned long long*>(smem + S::OFF_RED + S::R_RED - 6);   // 5 words
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -227,7 +213,6 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
     sTC[2] = w_flag.y;                                    // status | step << 32
     sTC[3] = w_scale.x;                                   // scale_old (bits)
     sTC[4] = w_scale.y;                                   // scale_new (bits)
-    sOutW[3] = ticket & 1u;
   }
   int st_status = 0, st_rerun = 0, st_step = 0;
   double scale_old = 0.0, scale_new = 0.0;
@@ -311,18 +296,15 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
 
   ADG_TSTAMP(4);   // corrector done, Q published
   // ---------------- predictor roles ----------------
-  // two Picard warps: thread = (node x, time level t), every component; lane = t |
-  // (i0 & 1) << 2 | i1 << 3, warp & 1 = i0 >> 1.  The other two warps wait at the barrier
-  // behind the loop.  Which pair works follows the CTA's ticket on its SM: the warps of a CTA
-  // sit on the SM's four schedulers by warp index, and the five CTAs of an SM would otherwise
-  // queue their Picard loops on two of them.
-  const int rot = (int)sOutW[3];
-  const int ptid = tid - 64 * rot;                        // 0..63 in the Picard warps
+  // warps 0-1 run the Picard loop: thread = (node x, time level t), every component; lane = t |
+  // (i0 & 1) << 2 | i1 << 3, warp = i0 >> 1.  Warps 2-3 wait at the barrier behind the loop.
+  // (Alternating the working pair between the CTAs of an SM, by a per-SM ticket, changed
+  // nothing: the loop is bound by the SM's shared-memory wavefronts.)
   const int t = lane & 3, i0 = 2 * (warp & 1) + ((lane >> 2) & 1), i1 = lane >> 3;
   const int x = i0 * NQ + i1;
   unsigned* sOut = sVote + 2 * PW;                        // [0] outcome, [1] iterations, [2] final slab
-  if ((warp >> 1) == rot) {
-    const int pw = warp & 1;
+  if (warp < PW) {
+    const int pw = warp;
     double qf[M];                                         // q at (x, t), every component
     {
       const double2 a = *reinterpret_cast<const double2*>(sQ + x * M);
@@ -398,11 +380,11 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
           const unsigned long long l = sWLam[0] > sWLam[1] ? sWLam[0] : sWLam[1];
           const unsigned long long am = sWAm[0] > sWAm[1] ? sWAm[0] : sWAm[1];
           if (!(sWOk[0] & sWOk[1])) {
-            if (ptid == 0) report_error(st, 2 * gcell + (mode_predict_only(mode) ? 1 : 0));
+            if (tid == 0) report_error(st, 2 * gcell + (mode_predict_only(mode) ? 1 : 0));
             outcome = 1u;
             break;
           }
-          if (!mode_predict_only(mode) && ptid == 0) atomicMax(&st->reduce[0], (long long)l);
+          if (!mode_predict_only(mode) && tid == 0) atomicMax(&st->reduce[0], (long long)l);
           tol = 1e-10 * (1.0 + __longlong_as_double((long long)am));
         }
         const unsigned v0 = sVote[(it & 1) * PW], v1 = sVote[(it & 1) * PW + 1];
@@ -458,12 +440,12 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
       }
       iters = it;
       // the slab of the last barrier holds the flux of the final iterate at every (t, axis, x, c)
-      if (outcome == 2u && ptid == 0) report_error(st, 2 * gcell + 1);
+      if (outcome == 2u && tid == 0) report_error(st, 2 * gcell + 1);
       if (outcome == 0u) {
         *reinterpret_cast<double2*>(sQt + t * (NS * M) + x * M) = make_double2(qf[0], qf[1]);
         *reinterpret_cast<double2*>(sQt + t * (NS * M) + x * M + 2) = make_double2(qf[2], qf[3]);
       }
-      if (ptid == 0) {
+      if (tid == 0) {
         sOut[0] = outcome;
         sOut[1] = (unsigned)iters;
         sOut[2] = (unsigned)(it & 1);
@@ -581,7 +563,7 @@ sweep_kernel_2d_p3(const SweepParams P, const FusedFinish X) {
   extern __shared__ __align__(16) double smem[];
   ADG_DEBUG_POISON();
   const Pass2P3 W{P.mode, P.sweep, P.tr_in, P.tr_out};
-  sweep_2d_p3_body(P, W, sweep_cell(P), sm_ticket_2p3(P), smem);
+  sweep_2d_p3_body(P, W, sweep_cell(P), smem);
   if (X.on) {
     // the last CTA to arrive has every CTA's reductions behind its fence: it is the time control
     __syncthreads();
@@ -677,7 +659,6 @@ run_kernel_2d_p3(const SweepParams P, const RunParams2P3 R) {
   const long long cells = (long long)P.planes_local * P.plane_cells;
   // every CTA reads the generation before any barrier of this launch can complete
   unsigned gen = *reinterpret_cast<volatile unsigned*>(&R.sync[1]) & GB_GEN;
-  const unsigned ticket = sm_ticket_2p3(P);
   if (threadIdx.x == 0) {                                     // the state the launch starts from
     const ulonglong2 w = __ldcg(reinterpret_cast<const ulonglong2*>(&P.st->rerun_next));
     s_flags = ((unsigned)w.x ? GB_RERUN : 0u) | ((unsigned)w.y ? GB_STOP : 0u);
@@ -702,7 +683,7 @@ run_kernel_2d_p3(const SweepParams P, const RunParams2P3 R) {
     if (flags & GB_RERUN) {                                    // _maybe_rerun (scheduler.py:446-449)
       const Pass2P3 W{MODE_RERUN, sweep, tr_in, R.tr[sweep & 1]};
       for (long long cell = first; cell < cells; cell += gridDim.x) {
-        sweep_2d_p3_body(P, W, cell, ticket, smem);
+        sweep_2d_p3_body(P, W, cell, smem);
         __syncthreads();
       }
       // a failed predict of the rerun pass (error key in reduce[1]) cancels the sweep
@@ -713,7 +694,7 @@ run_kernel_2d_p3(const SweepParams P, const RunParams2P3 R) {
     if (!skip) {
       const Pass2P3 W{MODE_NORMAL, sweep, tr_in, R.tr[(sweep & 1) ^ 1]};
       for (long long cell = first; cell < cells; cell += gridDim.x) {
-        sweep_2d_p3_body(P, W, cell, ticket, smem);
+        sweep_2d_p3_body(P, W, cell, smem);
         __syncthreads();
       }
     }
