@@ -82,10 +82,15 @@ struct Shape2P3 {
   static constexpr int OFF_Q = 0;                        // [x][c]
   static constexpr int OFF_FACE = OFF_Q + NS * M;        // signed F* [f][y][c]
   static constexpr int OFF_SLAB = OFF_FACE + 2 * DIM * NF * M;   // two flux slabs
-  static constexpr int OFF_QT = OFF_SLAB + 2 * SLAB;     // final q [t][x][c]
-  static constexpr int OFF_FB = OFF_QT + NQ * NS * M;    // fbar [a][x][c]
-  static constexpr int OFF_QBAR = OFF_FB + DIM * NS * M; // qbar [x][c]
-  static constexpr int OFF_DV = OFF_QBAR + NS * M;       // divergence exchange of the Picard loop
+  // tail buffers, padded like the slab: final q [t][i0][i1][c] with row stride 18 and level
+  // stride 76 (16-byte accesses of the Picard and trace threads conflict-free), fbar / qbar
+  // [i0][i1][c] with row stride 20 (8-byte face projections along either axis conflict-free)
+  static constexpr int QTS = NQ * RS + 4;        // time-level stride of the final q
+  static constexpr int BS = NQ * M + 4;          // row stride of fbar / qbar
+  static constexpr int OFF_QT = OFF_SLAB + 2 * SLAB;
+  static constexpr int OFF_FB = OFF_QT + NQ * QTS;       // fbar [a][i0][i1][c]
+  static constexpr int OFF_QBAR = OFF_FB + DIM * NQ * BS;
+  static constexpr int OFF_DV = OFF_QBAR + NQ * BS;      // divergence exchange of the Picard loop
   static constexpr int OFF_RED = OFF_DV + NQ * NQ * XS;  // per-warp words, s_max, votes, outcome
   static constexpr int R_RED = 2 * PW + 2 * DIM + 12;
   static constexpr int TOTAL = OFF_RED + R_RED;
@@ -134,7 +139,7 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
   using S = Shape2P3;
   using PDE = EulerPDE<2>;
   constexpr int DIM = 2, M = 4, NQ = 4, NS = 16, NF = 4, REC = S::REC, NW = S::NWARPS;
-  constexpr int TS = S::TS, AS = S::AS, RS = S::RS, XS = S::XS, PW = S::PW;
+  constexpr int TS = S::TS, AS = S::AS, RS = S::RS, XS = S::XS, PW = S::PW, QTS = S::QTS, BS = S::BS;
   constexpr unsigned FULL = 0xffffffffu;
 
   double* sQ = smem + S::OFF_Q;
@@ -442,8 +447,8 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
       // the slab of the last barrier holds the flux of the final iterate at every (t, axis, x, c)
       if (outcome == 2u && tid == 0) report_error(st, 2 * gcell + 1);
       if (outcome == 0u) {
-        *reinterpret_cast<double2*>(sQt + t * (NS * M) + x * M) = make_double2(qf[0], qf[1]);
-        *reinterpret_cast<double2*>(sQt + t * (NS * M) + x * M + 2) = make_double2(qf[2], qf[3]);
+        *reinterpret_cast<double2*>(sQt + t * QTS + i0 * RS + i1 * M) = make_double2(qf[0], qf[1]);
+        *reinterpret_cast<double2*>(sQt + t * QTS + i0 * RS + i1 * M + 2) = make_double2(qf[2], qf[3]);
       }
       if (tid == 0) {
         sOut[0] = outcome;
@@ -479,7 +484,7 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
       badf |= !finite(Fk);
       fb = fma(P.ops.w[k], Fk, fb);
     }
-    sFb[a * (NS * M) + e] = fb;
+    sFb[a * (NQ * BS) + (e >> 4) * BS + (e & 15)] = fb;
     if (__syncthreads_or(badf)) {
       if (tid == 0) report_error(st, 2 * gcell + 1);
       return;
@@ -497,29 +502,34 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
     const int j0 = xx >> 2, j1 = xx & 3;
     double s = 0.0;
 #pragma unroll
-    for (int j = 0; j < NQ; ++j) s = fma(P.ops.kvol[j0][j], sFb[(j * NQ + j1) * M + c], s);
+    for (int j = 0; j < NQ; ++j) s = fma(P.ops.kvol[j0][j], sFb[j * BS + j1 * M + c], s);
 #pragma unroll
-    for (int j = 0; j < NQ; ++j) s = fma(P.ops.kvol[j1][j], sFb[NS * M + (j0 * NQ + j) * M + c], s);
+    for (int j = 0; j < NQ; ++j) s = fma(P.ops.kvol[j1][j], sFb[NQ * BS + j0 * BS + j * M + c], s);
     Dg[e] = s * scale;
     double v = 0.0;
 #pragma unroll
-    for (int k = 0; k < NQ; ++k) v = fma(P.ops.w[k], sQt[k * (NS * M) + e], v);
-    sQbar[e] = v;
+    for (int k = 0; k < NQ; ++k) v = fma(P.ops.w[k], sQt[k * QTS + j0 * RS + (e & 15)], v);
+    sQbar[j0 * BS + (e & 15)] = v;
   } else {
     // s_max over the space-time trace of q, per face (Rusanov alpha input, kernels.py:107-128):
     // thread = (face f, face node y, time level): half-warp = face
     const int f = e >> 4, y = (e >> 2) & 3, tt = e & 3, a = f >> 1;
     const double* vec = (f & 1) ? P.ops.right : P.ops.left;
-    const int xb = (a == 0) ? y : NQ * y, sta = (a == 0) ? NQ : 1;
+    // trace line of face node y: nodes (i, y) across axis 0, (y, i) across axis 1
+    const int xb = (a == 0) ? y * M : y * RS, sta = (a == 0) ? RS : M;
+    // axis 0: the eight lanes of a quarter-warp (4 levels x 2 face nodes) sit on even 16-byte
+    // groups only; odd face nodes fetch their upper component pair first
+    const int sw = (a == 0 && (y & 1)) ? 2 : 0;
     double qs[M];
 #pragma unroll
     for (int c = 0; c < M; ++c) qs[c] = 0.0;
 #pragma unroll
     for (int i = 0; i < NQ; ++i) {
       const double vi = vec[i];
-      const double* src = sQt + tt * (NS * M) + (xb + i * sta) * M;
-      const double2 lo = *reinterpret_cast<const double2*>(src);
-      const double2 hi = *reinterpret_cast<const double2*>(src + 2);
+      const double* src = sQt + tt * QTS + xb + i * sta;
+      const double2 u = *reinterpret_cast<const double2*>(src + sw);
+      const double2 v = *reinterpret_cast<const double2*>(src + (sw ^ 2));
+      const double2 lo = sw ? v : u, hi = sw ? u : v;
       qs[0] = fma(vi, lo.x, qs[0]); qs[1] = fma(vi, lo.y, qs[1]);
       qs[2] = fma(vi, hi.x, qs[2]); qs[3] = fma(vi, hi.y, qs[3]);
     }
@@ -537,11 +547,11 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
     // face records: threads 0-63 project qbar, threads 64-127 project fbar; item = (f, y, c)
     const int f = e >> 4, yc = e & 15, y = yc >> 2, c = yc & 3, a = f >> 1;
     const double* vec = (f & 1) ? P.ops.right : P.ops.left;
-    const int xb = (a == 0) ? y : NQ * y, sta = (a == 0) ? NQ : 1;
-    const double* src = (tid < 64) ? sQbar : sFb + a * (NS * M);
+    const int xb = (a == 0) ? y * M : y * BS, sta = (a == 0) ? BS : M;
+    const double* src = (tid < 64) ? sQbar : sFb + a * (NQ * BS);
     double v = 0.0;
 #pragma unroll
-    for (int i = 0; i < NQ; ++i) v = fma(vec[i], src[(xb + i * sta) * M + c], v);
+    for (int i = 0; i < NQ; ++i) v = fma(vec[i], src[xb + i * sta + c], v);
     double* rec = W.tr_out + ((long long)f * P.slots + own_slot) * REC;
     rec[(tid < 64 ? 0 : NF * M) + yc] = v;
   }

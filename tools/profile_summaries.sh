@@ -9,7 +9,8 @@ SRC=$1; OUT=$2
 mkdir -p $OUT
 declare -A K=( [cfg2]=_ZN3adg15sweep_kernel_p3ENS_11SweepParamsE [cfg3_p5]=_ZN3adg15sweep_kernel_p5ENS_11SweepParamsE
                [cfg4]=_ZN3adg15sweep_kernel_p5ENS_11SweepParamsE [cfg3_p7]=_ZN3adg15sweep_kernel_p7ENS_11SweepParamsE
-               [cfg3_p9]=_ZN3adg15sweep_kernel_p9ENS_11SweepParamsE )
+               [cfg3_p9]=_ZN3adg15sweep_kernel_p9ENS_11SweepParamsE
+               [cfg1]=_ZN3adg18sweep_kernel_2d_p3ENS_11SweepParamsENS_11FusedFinishE )
 for c in "${!K[@]}"; do
   [ -f $SRC/full_${c}_raw.csv.gz ] || continue
   {
