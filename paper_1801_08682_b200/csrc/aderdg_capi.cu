@@ -728,6 +728,12 @@ adg_status adg_create(const adg_config* cfg, adg_handle** out) {
     if (nsm == 0 || nsm > 4096) return fail(h, ADG_ERR_RUNTIME, "cannot size the per-SM scratch slots");
     CUDA_TRY(h, cudaMalloc(&h->sm_scratch, sizeof(double) * (size_t)nsm * ShapeP9::SCRATCH));
   }
+#ifdef ADG_P5_TIMING
+  if (c.d == 3 && c.p == 5) {                      // tools/p5_timeline.py: 8 stamps per CTA
+    CUDA_TRY(h, cudaMalloc(&h->sm_scratch, sizeof(double) * 8 * (size_t)h->cells_local));
+    CUDA_TRY(h, cudaMemsetAsync(h->sm_scratch, 0, sizeof(double) * 8 * (size_t)h->cells_local, h->stream));
+  }
+#endif
 #ifdef ADG_2P3_TIMING
   if (c.d == 2 && c.p == 3) {                      // tools/cta_timeline.py: 32 stamps per CTA
     CUDA_TRY(h, cudaMalloc(&h->sm_scratch, sizeof(double) * 32 * (size_t)h->cells_local));
@@ -1209,6 +1215,9 @@ adg_status adg_buffer(adg_handle* h, int which, void** ptr, size_t* bytes) {
     case ADG_BUF_TRACE0: *ptr = h->tr[0]; *bytes = tr_bytes; return ADG_OK;
     case ADG_BUF_TRACE1: *ptr = h->tr[1]; *bytes = tr_bytes; return ADG_OK;
     case ADG_BUF_REDUCE: *ptr = h->st; *bytes = 2 * sizeof(long long); return ADG_OK;
+#ifdef ADG_P5_TIMING
+    case 98: *ptr = h->sm_scratch; *bytes = sizeof(double) * 8 * (size_t)h->cells_local; return ADG_OK;
+#endif
 #ifdef ADG_2P3_TIMING
     case 99: *ptr = h->sm_scratch; *bytes = sizeof(double) * 32 * (size_t)h->cells_local; return ADG_OK;
 #endif

@@ -183,8 +183,36 @@ struct ShapeP5 {
   static_assert(STR >= DIM * ACOL + 4 && STR % 16 == 8 && ACOL % 16 == 8, "operand row layout");
 };
 
+// tools/p5_timeline.py (A/B build with -DADG_P5_TIMING): thread 0 stamps clock64 / globaltimer
+#ifdef ADG_P5_TIMING
+#define ADG_P5_STAMP(i)                                                                              \
+  do {                                                                                               \
+    if (threadIdx.x == 0 && P.sm_scratch != nullptr) P.sm_scratch[blockIdx.x * 8 + (i)] = (double)clock64(); \
+  } while (0)
+#define ADG_P5_GSTAMP(i)                                                                             \
+  do {                                                                                               \
+    if (threadIdx.x == 0 && P.sm_scratch != nullptr) {                                               \
+      unsigned long long g_;                                                                         \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_));                                         \
+      P.sm_scratch[blockIdx.x * 8 + (i)] = (double)g_;                                               \
+    }                                                                                                \
+  } while (0)
+#else
+#define ADG_P5_STAMP(i) ((void)0)
+#define ADG_P5_GSTAMP(i) ((void)0)
+#endif
+
 __global__ void __launch_bounds__(ShapeP5::THREADS, 2) sweep_kernel_p5(const SweepParams P) {
   using S = ShapeP5;
+  ADG_P5_GSTAMP(0);
+#ifdef ADG_P5_TIMING
+  if (threadIdx.x == 0 && P.sm_scratch != nullptr) {
+    unsigned sm_;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_));
+    P.sm_scratch[blockIdx.x * 8 + 6] = (double)sm_;
+  }
+#endif
+  ADG_P5_STAMP(1);
   constexpr int DIM = 3, M = 5, NQ = 6, NS = S::NS, NF = S::NF, REC = S::REC, NW = S::NW;
   constexpr int THREADS = S::THREADS, ACOL = S::ACOL, FBUF = S::FBUF;
 
@@ -380,7 +408,9 @@ __global__ void __launch_bounds__(ShapeP5::THREADS, 2) sweep_kernel_p5(const Swe
   // the 512), warp w on lanes 32*(w%4) and columns (w/4)*128.. : q[t][c] at column
   // 2(6c+t), the slice divergences dv[k][c] at 64 + 2(5k+c)
   __shared__ uint32_t s_tmem;
+  ADG_P5_STAMP(2);
   if (warp == 0) tmem_alloc_cols<256>(&s_tmem);
+  ADG_P5_STAMP(3);
   tmem_fence_before();
   double absmax;
   {
@@ -609,7 +639,9 @@ __global__ void __launch_bounds__(ShapeP5::THREADS, 2) sweep_kernel_p5(const Swe
   failed = __syncthreads_or(act && bad) || failed;
   // every TMEM access of the CTA precedes the barrier above: release the columns
   tmem_fence_after();
+  ADG_P5_STAMP(4);
   if (warp == 0) tmem_dealloc_cols<256>(s_tmem);
+  ADG_P5_STAMP(5);
   if (failed) {
     if (tid == 0) {
       report_error(st, 2 * gcell + 1);
@@ -722,6 +754,7 @@ __global__ void __launch_bounds__(ShapeP5::THREADS, 2) sweep_kernel_p5(const Swe
     rec[2 * NF * M] = __longlong_as_double((long long)sSmax[tid]);
     rec[2 * NF * M + 1] = record_stamp(P);
   }
+  ADG_P5_GSTAMP(7);
 }
 
 }  // namespace adg
