@@ -3,13 +3,14 @@
 // 729 cells of 16 nodes cannot fill 148 SMs: the sweep is one cell's latency, so the
 // kernel spends threads on shortening the dependent chain of a cell instead of on
 // throughput.  One CTA of 128 threads per cell:
-//   * Picard loop: thread = (node x, time level t, component pair h); lane = t | h << 2 |
-//     (x & 3) << 3, warp = x >> 2.  The flux of (x, t) is evaluated by both h lanes, lane h
-//     stores axis h (two 16-byte stores); the derivative of a component pair is eight
-//     16-byte loads + 16 FMAs; the four slices of a (node, pair) sit in four adjacent
-//     lanes, so the time contraction is eight width-4 shuffles + 8 FMAs.  Slab layout
-//     [t][axis][x][c] with strides 132 / 66 / 4 / 1: the eight lanes of a quarter-warp hit
-//     eight distinct 16-byte bank groups on every store and load.
+//   * Picard loop on two warps: thread = (node x, time level t), every component; lane = i1 |
+//     (i0 & 1) << 2 | t << 3, warp = i0 >> 1.  Axis-1 derivative from registers: one
+//     DMMA.8x8x4 per component (the node's flux in the A fragment, interleaved diff^T in B, the
+//     result in the owning lane), issued before the barrier; axis 0 through the flux slab
+//     [t][i0][i1][c] (eight 16-byte loads + 16 FMAs); the four slices of a node meet in an
+//     exchange buffer (same warp: __syncwarp) for the time contraction.  Row strides 18 and the
+//     time stride 148 put the eight lanes of a quarter-warp on eight distinct 16-byte bank
+//     groups in every store and load of the loop.
 //   * one barrier per Picard iteration: the flux slabs and the vote words alternate
 //     between two buffers; the convergence vote of iteration i rides on the barrier that
 //     publishes the flux of iteration i + 1, which is also the final flux of the tail when
@@ -23,13 +24,15 @@
 //     issued before the first use.
 //   * optional fused time control (FusedFinish): the last CTA to arrive runs finish_body,
 //     which removes the finish launch from the step (single GPU, fused driver).
-// Arithmetic (operation order, FMA shapes, exact-rounded decisions) is that of the generic
-// kernel (aderdg_kernels.cuh), which this kernel replaces for (Euler, d = 2, p = 3, periodic,
-// fused driver).
+// Arithmetic is that of the generic kernel (aderdg_kernels.cuh: operation order, FMA shapes,
+// exact-rounded decisions), which this kernel replaces for (Euler, d = 2, p = 3, periodic, fused
+// driver), except for the divergence: axis-0 chain + axis-1 DMMA instead of one chain over
+// both axes (a rounding-level difference, as in sweep_kernel_p3).
 //
 // Reference (src/ = /root/reference/pkg/src/aderdg/): kernels.py:68-229, scheduler.py:370-449.
 #pragma once
 #include "aderdg_kernels.cuh"
+#include "aderdg_sweep_p3.cuh"   // dmma_8x8x4
 
 namespace adg {
 
@@ -301,11 +304,13 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
 
   ADG_TSTAMP(4);   // corrector done, Q published
   // ---------------- predictor roles ----------------
-  // warps 0-1 run the Picard loop: thread = (node x, time level t), every component; lane = t |
-  // (i0 & 1) << 2 | i1 << 3, warp = i0 >> 1.  Warps 2-3 wait at the barrier behind the loop.
+  // warps 0-1 run the Picard loop: thread = (node x, time level t), every component; lane = i1 |
+  // (i0 & 1) << 2 | t << 3, warp = i0 >> 1.  Warps 2-3 wait at the barrier behind the loop.
   // (Alternating the working pair between the CTAs of an SM, by a per-SM ticket, changed
   // nothing: the loop is bound by the SM's shared-memory wavefronts.)
-  const int t = lane & 3, i0 = 2 * (warp & 1) + ((lane >> 2) & 1), i1 = lane >> 3;
+  // lane = i1 | (i0 & 1) << 2 | t << 3: the axis-1 line of a node sits in lanes & 3, where the
+  // DMMA A fragment wants its k index
+  const int i1 = lane & 3, i0 = 2 * (warp & 1) + ((lane >> 2) & 1), t = lane >> 3;
   const int x = i0 * NQ + i1;
   unsigned* sOut = sVote + 2 * PW;                        // [0] outcome, [1] iterations, [2] final slab
   if (warp < PW) {
@@ -347,32 +352,38 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
       // ---------------- predictor (kernels.py:68-105) ----------------
       const double scale = (mode == MODE_RERUN) ? scale_old : scale_new;   // dt / h
       constexpr int cap = 2 * NQ;
-      double drow0[NQ], drow1[NQ], ig[NQ];
+      double drow0[NQ], ig[NQ];
 #pragma unroll
       for (int j = 0; j < NQ; ++j) {
         drow0[j] = P.ops.diff[i0][j];
-        drow1[j] = P.ops.diff[i1][j];
         ig[j] = P.ops.integ[t][j];
       }
       const int rd0 = t * TS + i1 * M;                    // axis 0: node (j, i1), + RS j
-      const int rd1 = t * TS + AS + i0 * RS;              // axis 1: node (i0, j), + M j
       const int wr = t * TS + i0 * RS + i1 * M;
-      const int xo = i1 * (NQ * XS) + i0 * XS;            // this node's slot of the exchange buffer
+      const int xo = i0 * (NQ * XS) + i1 * XS;            // this node's slot of the exchange buffer
+      // B fragment of the axis-1 derivative: B[k = lane & 3][n = lane >> 2] = diff[n / 2][k], n even
+      const double bfrag = ((lane >> 2) & 1) ? 0.0 : P.ops.diff[lane >> 3][lane & 3];
       double tol = 0.0;
       unsigned outcome = 0u;                              // 1 inadmissible / non-finite Q, 2 predictor failed
       int iters = 0;
       bool conv = false, bad = false;
       int it = 0;
+      double F[DIM][M];
       for (;; ++it) {
         ADG_PSTAMP(16 + it);
-        double F[DIM][M];
         PDE::flux(qf, F, P);
         double* slab = sSlab + (it & 1) * S::SLAB;
+        // axis 1 from registers: one DMMA per component (the node's flux in A, interleaved
+        // diff^T in B, the result in the lane that owns the node); only axis 0 goes through
+        // the slab (axis 1 of the final iterate is stored behind the loop, for fbar)
+        double d1[M];
 #pragma unroll
-        for (int a = 0; a < DIM; ++a) {
-          *reinterpret_cast<double2*>(slab + wr + a * AS) = make_double2(F[a][0], F[a][1]);
-          *reinterpret_cast<double2*>(slab + wr + a * AS + 2) = make_double2(F[a][2], F[a][3]);
+        for (int c = 0; c < M; ++c) {
+          double z;
+          dmma_8x8x4(d1[c], z, F[1][c], bfrag, 0.0, 0.0);
         }
+        *reinterpret_cast<double2*>(slab + wr) = make_double2(F[0][0], F[0][1]);
+        *reinterpret_cast<double2*>(slab + wr + 2) = make_double2(F[0][2], F[0][3]);
         // vote word: bit 0 = every thread converged in the previous iteration, bit 1 = some
         // difference non-finite
         const bool wc = __all_sync(FULL, conv);
@@ -397,7 +408,7 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
           if ((v0 | v1) & 2u) { outcome = 2u; break; }
           if ((v0 & v1 & 1u) || it == cap) break;
         }
-        // divergence of the slice at this node: axis 0 then axis 1 in one chain per component
+        // divergence of the slice at this node: the axis-0 chain from the slab + the axis-1 DMMA
         double dv[M];
 #pragma unroll
         for (int c = 0; c < M; ++c) dv[c] = 0.0;
@@ -409,12 +420,7 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
           dv[2] = fma(drow0[j], hi.x, dv[2]); dv[3] = fma(drow0[j], hi.y, dv[3]);
         }
 #pragma unroll
-        for (int j = 0; j < NQ; ++j) {
-          const double2 lo = *reinterpret_cast<const double2*>(slab + rd1 + j * M);
-          const double2 hi = *reinterpret_cast<const double2*>(slab + rd1 + j * M + 2);
-          dv[0] = fma(drow1[j], lo.x, dv[0]); dv[1] = fma(drow1[j], lo.y, dv[1]);
-          dv[2] = fma(drow1[j], hi.x, dv[2]); dv[3] = fma(drow1[j], hi.y, dv[3]);
-        }
+        for (int c = 0; c < M; ++c) dv[c] += d1[c];
         if (it == 2) ADG_PSTAMP(12);
         // time contraction: the four slices of a node are in four lanes of one warp; they
         // meet in the node's slot of the exchange buffer (written before, read after a
@@ -447,6 +453,9 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
       // the slab of the last barrier holds the flux of the final iterate at every (t, axis, x, c)
       if (outcome == 2u && tid == 0) report_error(st, 2 * gcell + 1);
       if (outcome == 0u) {
+        double* slab = sSlab + (it & 1) * S::SLAB + AS;
+        *reinterpret_cast<double2*>(slab + wr) = make_double2(F[1][0], F[1][1]);
+        *reinterpret_cast<double2*>(slab + wr + 2) = make_double2(F[1][2], F[1][3]);
         *reinterpret_cast<double2*>(sQt + t * QTS + i0 * RS + i1 * M) = make_double2(qf[0], qf[1]);
         *reinterpret_cast<double2*>(sQt + t * QTS + i0 * RS + i1 * M + 2) = make_double2(qf[2], qf[3]);
       }

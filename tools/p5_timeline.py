@@ -45,6 +45,11 @@ def main():
           f"(globaltimer), entry -> TMEM alloc {(t[:, 2] - t[:, 1]).mean():.0f} clk")
     print(f"tcgen05.alloc (+ relinquish) {(t[:, 3] - t[:, 2]).mean():.0f} clk (max {(t[:, 3] - t[:, 2]).max():.0f}), "
           f"tcgen05.dealloc {(t[:, 5] - t[:, 4]).mean():.0f} clk (max {(t[:, 5] - t[:, 4]).max():.0f})")
+    clk_ns = 1.965
+    pic = (t[:, 4] - t[:, 3]) / clk_ns
+    pro = (t[:, 2] - t[:, 1]) / clk_ns
+    print(f"phases (ns): prologue up to the allocation {pro.mean():.0f}, Picard loop + final flux {pic.mean():.0f} "
+          f"(min {pic.min():.0f}, max {pic.max():.0f}), tail {(life - pro - pic).mean() - (t[:, 5] - t[:, 4]).mean() / clk_ns:.0f}")
     wall = t[:, 7].max() - t[:, 0].min()
     sms = np.unique(t[:, 6])
     busy = np.array([life[t[:, 6] == s].sum() for s in sms])
