@@ -164,8 +164,8 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
   const int mode = W.mode;
   const bool corr = mode_corrects(mode);
   const long long gcell = cell + P.cell_offset;
-  const int plane = (int)(cell / P.plane_cells);
-  const int rest = (int)(cell % P.plane_cells);
+  const int plane = (int)cell / P.plane_cells;            // (local cells fit 32 bits: 32-bit division)
+  const int rest = (int)cell % P.plane_cells;
   const long long own_slot = (long long)(plane + 1) * P.plane_cells + rest;
   double* Qg = P.Q + cell * (NS * M);
   double* Dg = P.D + cell * (NS * M);
@@ -322,32 +322,7 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
       qf[0] = a.x; qf[1] = a.y; qf[2] = b.x; qf[3] = b.y;
     }
     const double Qn[M] = {qf[0], qf[1], qf[2], qf[3]};
-    // calc_time_step (kernels.py:216-229) / predict's finiteness check (kernels.py:80-81) and
-    // max |Q| for the Picard tolerance: the four threads of a node evaluate them (no
-    // divergence, the chains overlap the first flux); the per-warp words are read after the
-    // first barrier of the Picard loop
-    {
-      bool ok = true;
-      double lam = 0.0;
-      if (!mode_predict_only(mode)) {
-        ok = PDE::node_lambda(qf, lam, P);
-      } else {
-#pragma unroll
-        for (int c = 0; c < M; ++c) ok = ok && finite(qf[c]);
-      }
-      double am = 0.0;
-#pragma unroll
-      for (int c = 0; c < M; ++c) am = fmax(am, fabs(qf[c]));
-      const bool wok = __all_sync(FULL, ok);
-      const unsigned long long wl = warp_max_u64((unsigned long long)__double_as_longlong(ok ? lam : 0.0));
-      const unsigned long long wa = warp_max_u64((unsigned long long)__double_as_longlong(am));
-      if (lane == 0) {
-        sWOk[pw] = wok ? 1u : 0u;
-        sWLam[pw] = wl;
-        sWAm[pw] = wa;
-      }
-    }
-    ADG_PSTAMP(5);   // lambda / absmax words written
+    ADG_PSTAMP(5);
     if (mode != MODE_SEED) {
       // ---------------- predictor (kernels.py:68-105) ----------------
       const double scale = (mode == MODE_RERUN) ? scale_old : scale_new;   // dt / h
@@ -392,17 +367,6 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
         if (it == 2) ADG_PSTAMP(10);
         picard_barrier_2p3();
         if (it == 2) ADG_PSTAMP(11);
-        if (it == 0) {
-          const unsigned long long l = sWLam[0] > sWLam[1] ? sWLam[0] : sWLam[1];
-          const unsigned long long am = sWAm[0] > sWAm[1] ? sWAm[0] : sWAm[1];
-          if (!(sWOk[0] & sWOk[1])) {
-            if (tid == 0) report_error(st, 2 * gcell + (mode_predict_only(mode) ? 1 : 0));
-            outcome = 1u;
-            break;
-          }
-          if (!mode_predict_only(mode) && tid == 0) atomicMax(&st->reduce[0], (long long)l);
-          tol = 1e-10 * (1.0 + __longlong_as_double((long long)am));
-        }
         const unsigned v0 = sVote[(it & 1) * PW], v1 = sVote[(it & 1) * PW + 1];
         if (it > 0) {
           if ((v0 | v1) & 2u) { outcome = 2u; break; }
@@ -445,6 +409,18 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
           bm.add(fabs(qn - qf[c]));
           qf[c] = qn;
         }
+        if (it == 0) {
+          // warp 2's words (admissibility, lambda, max |Q|) are first needed here: nothing of
+          // this pass has left the CTA yet
+          asm volatile("bar.sync 2, 96;" ::: "memory");
+          if (!sWOk[0]) {
+            if (tid == 0) report_error(st, 2 * gcell + (mode_predict_only(mode) ? 1 : 0));
+            outcome = 1u;
+            break;
+          }
+          if (!mode_predict_only(mode) && tid == 0) atomicMax(&st->reduce[0], (long long)sWLam[0]);
+          tol = 1e-10 * (1.0 + __longlong_as_double((long long)sWAm[0]));
+        }
         conv = bm.conv(tol);
         bad = bm.bad();
         if (it == 2) ADG_PSTAMP(31);
@@ -465,12 +441,44 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
         sOut[2] = (unsigned)(it & 1);
       }
     }
+  } else if (warp == PW) {
+    // warp 2, idle during the Picard loop: calc_time_step (kernels.py:216-229) / predict's
+    // finiteness check (kernels.py:80-81) and max |Q| for the Picard tolerance, lane = node.
+    // The Picard warps pick the words up at the end of their first iteration (barrier 2).
+    bool ok = true;
+    double lam = 0.0, am = 0.0;
+    if (lane < NS) {
+      double qn[M];
+      const double2 a = *reinterpret_cast<const double2*>(sQ + lane * M);
+      const double2 b = *reinterpret_cast<const double2*>(sQ + lane * M + 2);
+      qn[0] = a.x; qn[1] = a.y; qn[2] = b.x; qn[3] = b.y;
+      if (!mode_predict_only(mode)) {
+        ok = PDE::node_lambda(qn, lam, P);
+      } else {
+#pragma unroll
+        for (int c = 0; c < M; ++c) ok = ok && finite(qn[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < M; ++c) am = fmax(am, fabs(qn[c]));
+    }
+    const bool wok = __all_sync(FULL, ok);
+    const unsigned long long wl = warp_max_u64((unsigned long long)__double_as_longlong(ok ? lam : 0.0));
+    const unsigned long long wa = warp_max_u64((unsigned long long)__double_as_longlong(am));
+    if (lane == 0) {
+      sWOk[0] = wok ? 1u : 0u;
+      sWLam[0] = wl;
+      sWAm[0] = wa;
+    }
+    if (mode != MODE_SEED) {
+      __threadfence_block();
+      asm volatile("bar.arrive 2, 96;" ::: "memory");
+    }
   }
   __syncthreads();
   if (mode == MODE_SEED) {
     if (tid == 0) {
-      if (!(sWOk[0] & sWOk[1])) report_error(st, 2 * gcell + 0);
-      else atomicMax(&st->reduce[0], (long long)(sWLam[0] > sWLam[1] ? sWLam[0] : sWLam[1]));
+      if (!sWOk[0]) report_error(st, 2 * gcell + 0);
+      else atomicMax(&st->reduce[0], (long long)sWLam[0]);
     }
     return;
   }
