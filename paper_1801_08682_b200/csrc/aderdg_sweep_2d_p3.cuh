@@ -339,7 +339,7 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
       // B fragment of the axis-1 derivative: B[k = lane & 3][n = lane >> 2] = diff[n / 2][k], n even
       const double bfrag = ((lane >> 2) & 1) ? 0.0 : P.ops.diff[lane >> 3][lane & 3];
       double tol = 0.0;
-      unsigned outcome = 0u;                              // 1 inadmissible / non-finite Q, 2 predictor failed
+      unsigned outcome = 0u;                              // 2: predictor failed (non-finite difference)
       int iters = 0;
       bool conv = false, bad = false;
       int it = 0;
@@ -410,15 +410,9 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
           qf[c] = qn;
         }
         if (it == 0) {
-          // warp 2's words (admissibility, lambda, max |Q|) are first needed here: nothing of
-          // this pass has left the CTA yet
+          // warp 2's max |Q| is first needed here (its admissibility / lambda words follow at
+          // the barrier behind the loop: the loop itself lets nothing out of the CTA)
           asm volatile("bar.sync 2, 96;" ::: "memory");
-          if (!sWOk[0]) {
-            if (tid == 0) report_error(st, 2 * gcell + (mode_predict_only(mode) ? 1 : 0));
-            outcome = 1u;
-            break;
-          }
-          if (!mode_predict_only(mode) && tid == 0) atomicMax(&st->reduce[0], (long long)sWLam[0]);
           tol = 1e-10 * (1.0 + __longlong_as_double((long long)sWAm[0]));
         }
         conv = bm.conv(tol);
@@ -427,7 +421,6 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
       }
       iters = it;
       // the slab of the last barrier holds the flux of the final iterate at every (t, axis, x, c)
-      if (outcome == 2u && tid == 0) report_error(st, 2 * gcell + 1);
       if (outcome == 0u) {
         double* slab = sSlab + (it & 1) * S::SLAB + AS;
         *reinterpret_cast<double2*>(slab + wr) = make_double2(F[1][0], F[1][1]);
@@ -442,36 +435,40 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
       }
     }
   } else if (warp == PW) {
-    // warp 2, idle during the Picard loop: calc_time_step (kernels.py:216-229) / predict's
-    // finiteness check (kernels.py:80-81) and max |Q| for the Picard tolerance, lane = node.
-    // The Picard warps pick the words up at the end of their first iteration (barrier 2).
-    bool ok = true;
-    double lam = 0.0, am = 0.0;
+    // warp 2, idle during the Picard loop, lane = node: max |Q| for the Picard tolerance (the
+    // Picard warps pick it up at the end of their first iteration, barrier 2), then
+    // calc_time_step (kernels.py:216-229) / predict's finiteness check (kernels.py:80-81),
+    // three exact divisions and a root per node, read behind the loop.
+    double qn[M] = {0.0, 0.0, 0.0, 0.0};
     if (lane < NS) {
-      double qn[M];
       const double2 a = *reinterpret_cast<const double2*>(sQ + lane * M);
       const double2 b = *reinterpret_cast<const double2*>(sQ + lane * M + 2);
       qn[0] = a.x; qn[1] = a.y; qn[2] = b.x; qn[3] = b.y;
+    }
+    double am = 0.0;
+#pragma unroll
+    for (int c = 0; c < M; ++c) am = fmax(am, fabs(qn[c]));
+    const unsigned long long wa = warp_max_u64((unsigned long long)__double_as_longlong(am));
+    if (lane == 0) sWAm[0] = wa;
+    if (mode != MODE_SEED) {
+      __threadfence_block();
+      asm volatile("bar.arrive 2, 96;" ::: "memory");
+    }
+    bool ok = true;
+    double lam = 0.0;
+    if (lane < NS) {
       if (!mode_predict_only(mode)) {
         ok = PDE::node_lambda(qn, lam, P);
       } else {
 #pragma unroll
         for (int c = 0; c < M; ++c) ok = ok && finite(qn[c]);
       }
-#pragma unroll
-      for (int c = 0; c < M; ++c) am = fmax(am, fabs(qn[c]));
     }
     const bool wok = __all_sync(FULL, ok);
     const unsigned long long wl = warp_max_u64((unsigned long long)__double_as_longlong(ok ? lam : 0.0));
-    const unsigned long long wa = warp_max_u64((unsigned long long)__double_as_longlong(am));
     if (lane == 0) {
       sWOk[0] = wok ? 1u : 0u;
       sWLam[0] = wl;
-      sWAm[0] = wa;
-    }
-    if (mode != MODE_SEED) {
-      __threadfence_block();
-      asm volatile("bar.arrive 2, 96;" ::: "memory");
     }
   }
   __syncthreads();
@@ -483,7 +480,16 @@ __device__ __forceinline__ void sweep_2d_p3_body(const SweepParams& P, const Pas
     return;
   }
   ADG_TSTAMP(6);   // Picard loop done
-  if (sOut[0] != 0u) return;
+  // calc_time_step comes before predict (scheduler.py:370-449): its verdict first
+  if (!sWOk[0]) {
+    if (tid == 0) report_error(st, 2 * gcell + (mode_predict_only(mode) ? 1 : 0));
+    return;
+  }
+  if (sOut[0] != 0u) {
+    if (tid == 0) report_error(st, 2 * gcell + 1);
+    return;
+  }
+  if (!mode_predict_only(mode) && tid == 0) atomicMax(&st->reduce[0], (long long)sWLam[0]);
   const double scale = (mode == MODE_RERUN) ? scale_old : scale_new;
   const double* cur = sSlab + sOut[2] * S::SLAB;
   const int iters = (int)sOut[1];
