@@ -714,6 +714,7 @@ adg_status adg_create(const adg_config* cfg, adg_handle** out) {
   CUDA_TRY(h, cudaMalloc(&h->tr[0], tr_bytes));
   CUDA_TRY(h, cudaMalloc(&h->tr[1], tr_bytes));
   CUDA_TRY(h, cudaMalloc(&h->st, sizeof(DevState)));
+  if (h->rec_cap & (h->rec_cap - 1)) return fail(h, ADG_ERR_CONFIG, "the step-record ring is a power of two");
   CUDA_TRY(h, cudaMalloc(&h->recs, sizeof(StepRecord) * h->rec_cap));
   CUDA_TRY(h, cudaMalloc(&h->arrive, 2 * sizeof(unsigned)));
   CUDA_TRY(h, cudaMemsetAsync(h->arrive, 0, 2 * sizeof(unsigned), h->stream));
